@@ -1,0 +1,113 @@
+/*
+ * mlra_b200.h -- C ABI of the B200 (sm_100a) decode-attention kernels for the latent
+ * attention family (MLRA-4 / MLA) and its GQA comparison variant.
+ *
+ * The reference (arxiv 2603.02188 "attnkit") has no FFI: its operator boundary is the
+ * Python decode API. Each entry point below replaces one piece of that path; the
+ * reference function it stands in for is cited per function (paths relative to
+ * /root/reference/pkg/src/attnkit/). INTEGRATION.md shows the ctypes binding a
+ * maintainer would add on the reference side.
+ *
+ * Conventions
+ *  - Every pointer is a device pointer unless stated otherwise; bf16 buffers are passed
+ *    as void* (IEEE bfloat16, row-major, contiguous), fp32 as float*.
+ *  - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t, NULL =
+ *    legacy default stream). No call allocates device memory: the caller owns all
+ *    buffers and sizes the split-KV workspace with mlra_workspace_bytes().
+ *  - Return value: 0 on success, otherwise a negative MLRA_ERR_* code; the message of
+ *    the last failure on the calling thread is available from mlra_last_error().
+ *  - Calls on different streams may run concurrently from different host threads.
+ */
+#ifndef MLRA_B200_H
+#define MLRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLRA_OK 0
+#define MLRA_ERR_SHAPE (-1)   /* ShapeMismatchError (errors.py:8) */
+#define MLRA_ERR_CONFIG (-2)  /* ConfigError (errors.py:16)        */
+#define MLRA_ERR_NUMERIC (-3) /* NumericError (errors.py:12)       */
+#define MLRA_ERR_CUDA (-4)    /* launch / runtime failure          */
+
+/* ABI version (major*100 + minor). */
+int mlra_version(void);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* mlra_last_error(void);
+
+/* Number of SMs of the current device (used to size split-KV grids). */
+int mlra_num_sms(void);
+
+/*
+ * K0 -- append one token row per sequence to the paged cache.
+ * Replaces decode.py:129-150 (append_owned) -> cache.py:44-57 (KvCache.append).
+ *   rows        [B, W] bf16, W = NB*DLAT + DR  ([latent block 0 | ... | rope])
+ *   block_table [B, max_pages] int32 page ids; positions [B] int32 token slot to write
+ *   pool        [num_pages*page_size, W] bf16
+ */
+int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_t* positions, int B, int W,
+                      int page_size, int max_pages, void* pool, void* stream);
+
+/*
+ * K1 -- query absorption (decode.py:155-167 absorb_query, applied per branch at :224).
+ *   q_nope [B, H, DH] bf16, q_rope [B, H, DR] bf16
+ *   w_uk   [H, DH, NB*DLAT] bf16: head-major pre-pack of the branch slices of W^UK
+ *          (weights.py:91-93 layout (d_c, h*d_h), rows b*DLAT.. of branch b)
+ *   q_abs  [B, NB, H, DLAT] bf16 out = score_scale * q_nope_h . W^UK_(b),(h)^T
+ *   q_rope_out [B, H, DR] bf16 out = score_scale * q_rope
+ *   score_scale = tau * log2(e)  (tau: config.py:100-112)
+ */
+int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
+                      int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream);
+
+/* Bytes of fp32 split-KV partials needed by mlra_decode_partials / mlra_decode_step. */
+size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit);
+
+/* Split count used when the caller passes nsplit <= 0 (fills the SMs for this batch). */
+int mlra_default_splits(int B, int max_seqlen, int NB, int SUB);
+
+/*
+ * K2 -- split-KV flash-decode over the paged latent cache (tcgen05 + TMA).
+ * Replaces decode.py:217-230 (attend_local, latent branch) + cache.py:59-66 (read).
+ *   q_abs [B, NB, H, DLAT], q_rope [B, H, DR]   (K1 outputs, pre-scaled)
+ *   pool  [num_pages*page_size, W] bf16 with W = NB*DLAT + DR; DLAT = SUB*DLS,
+ *         DLS in {64,128}; DR in {16,32,48,64}; page_size a multiple of 64
+ *   seqlens [B] int32 (>= 1)
+ *   o_part   [B, nsplit, NB, H, DLAT] fp32 out (per-split normalised latent mixture)
+ *   lse_part [B, nsplit, NB, H]       fp32 out (per-split log2-sum-exp)
+ */
+int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
+                         const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
+                         int DLS, int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream);
+
+/*
+ * K3 -- merge split partials, W^UV up-projection, ascending branch sum, alpha scaling.
+ * Replaces decode.py:228 (einsum mc,cmp->mp) + decode.py:264-285 (reduce_contributions).
+ *   w_uv [H, NB*DLAT, DH] bf16 head-major pre-pack of W^UV (weights.py:91-93)
+ *   out  [B, H, DH] fp32 = alpha * sum_b Z_b . W^UV_(b),(h)     (upproj = 1)
+ *        [B, NB, H, DLAT] fp32 = alpha * Z_b                      (upproj = 0)
+ *   alpha = alpha_attn (latent.py:56-61: 1/sqrt(branches) for mlra, 1 otherwise)
+ */
+int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, int B, int H, int NB,
+                 int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream);
+
+/*
+ * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.
+ * Replaces decode.py:304-305 (attend_local + reduce_contributions inside
+ * absorbed_decode_step) for every unit a device owns.
+ *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device)
+ */
+int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
+                     const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
+                     int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
+                     int nsplit, float score_scale, float alpha, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLRA_B200_H */

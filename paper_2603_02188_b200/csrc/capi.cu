@@ -1,0 +1,247 @@
+// C ABI of libmlra_b200.so (include/mlra_b200.h): argument validation, TMA descriptor
+// encoding, kernel selection and launch. No allocation, no synchronisation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <mutex>
+#include "../../include/mlra_b200.h"
+#include "aux_kernels.cuh"
+#include "decode_kernel.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MLRA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return MLRA_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+constexpr int kSmemBudget = 232448 - 1024;  // 227 KB opt-in minus static smem / slack
+
+struct Choice {
+  int T, NPAD, DLS;
+};
+
+template <int T, int NPAD, int DLS>
+int launch_decode(const CUtensorMap& map, mlra::DecodeParams p, int head_groups, cudaStream_t stream) {
+  using L = mlra::DecodeLayout<T, NPAD, DLS>;
+  const int q_chunks = p.NB * p.SUB * (DLS / 64) + 1;
+  const int fixed = 1024 + q_chunks * L::kQChunkBytes + 2 * L::kPBytes + L::kScratchBytes;
+  int rope_slots = 3;
+  int lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
+  lat_slots = lat_slots > 16 ? 16 : lat_slots;
+  if (lat_slots < 2 * p.SUB + 1)
+    return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
+                2 * p.SUB + 1);
+  p.lat_slots = lat_slots;
+  p.rope_slots = rope_slots;
+  const int smem = L::smem_bytes(p.NB, p.SUB, lat_slots, rope_slots);
+  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS>;
+  static unsigned attr_done = 0;  // per instantiation, one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !(attr_done & (1u << dev))) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) != cudaSuccess)
+      return cuda_check("cudaFuncSetAttribute(decode)");
+    if (dev < 32) attr_done |= 1u << dev;
+  }
+  dim3 grid(p.nsplit, p.B, head_groups);
+  kern<<<grid, mlra::kNumThreads, smem, stream>>>(map, p);
+  return cuda_check("mlra_decode_kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlra_version(void) { return 100; }
+
+const char* mlra_last_error(void) { return g_err; }
+
+int mlra_num_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(MLRA_ERR_CUDA, "cudaGetDevice failed");
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return fail(MLRA_ERR_CUDA, "cudaDeviceGetAttribute failed");
+  return n;
+}
+
+int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_t* positions, int B, int W,
+                      int page_size, int max_pages, void* pool, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (W <= 0 || W % 8 != 0) return fail(MLRA_ERR_SHAPE, "cache_append: row width %d must be a positive multiple of 8", W);
+  if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append: bad page geometry");
+  mlra::cache_append_kernel<<<B, 64, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(rows), block_table, positions, W, page_size, max_pages,
+      static_cast<__nv_bfloat16*>(pool));
+  return cuda_check("cache_append launch");
+}
+
+int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
+                      int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (H <= 0 || DH <= 0 || NB <= 0 || DLAT <= 0 || DLAT % 2 != 0 || DR < 0)
+    return fail(MLRA_ERR_SHAPE, "absorb_query: bad dims H=%d DH=%d NB=%d DLAT=%d DR=%d", H, DH, NB, DLAT, DR);
+  constexpr int SEQ = 4;
+  dim3 grid(H, (B + SEQ - 1) / SEQ);
+  const int smem = SEQ * DH * sizeof(float);
+  mlra::absorb_query_kernel<SEQ><<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(q_rope),
+      static_cast<const __nv_bfloat16*>(w_uk), static_cast<__nv_bfloat16*>(q_abs),
+      static_cast<__nv_bfloat16*>(q_rope_out), B, H, DH, NB * DLAT, DLAT, DR, score_scale);
+  return cuda_check("absorb_query launch");
+}
+
+size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
+         al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4);
+}
+
+int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
+  int sms = mlra_num_sms();
+  if (sms <= 0) sms = 148;
+  const int T = (NB * SUB == 1) ? 128 : 64;
+  const int tiles = (max_seqlen + T - 1) / T;
+  int s = (sms + B - 1) / B;  // one wave of CTAs (1 CTA / SM)
+  if (s > tiles) s = tiles;
+  if (s > 64) s = 64;
+  return s < 1 ? 1 : s;
+}
+
+int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
+                         const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
+                         int DLS, int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
+  if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
+  if (DLS != 64 && DLS != 128) return fail(MLRA_ERR_CONFIG, "decode: sub-block width %d not in {64,128}", DLS);
+  if (DR < 16 || DR > 64 || DR % 16 != 0) return fail(MLRA_ERR_CONFIG, "decode: rope width %d not in {16..64}/16", DR);
+  if (page_size <= 0 || page_size % 64 != 0) return fail(MLRA_ERR_CONFIG, "decode: page_size %d not a multiple of 64", page_size);
+  if (nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "decode: nsplit %d not in [1,64]", nsplit);
+  if (H < 1) return fail(MLRA_ERR_SHAPE, "decode: H=%d", H);
+  const int DLAT = SUB * DLS;
+  const int W = NB * DLAT + DR;
+  auto encode = get_encode();
+  if (!encode) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {cuuint64_t(W), cuuint64_t(num_pages) * cuuint64_t(page_size)};
+  cuuint64_t strides[1] = {cuuint64_t(W) * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled failed (%d): pool %p W=%d", int(cr), pool, W);
+
+  mlra::DecodeParams p{};
+  p.q_abs = static_cast<const __nv_bfloat16*>(q_abs);
+  p.q_rope = static_cast<const __nv_bfloat16*>(q_rope);
+  p.block_table = block_table;
+  p.seqlens = seqlens;
+  p.o_part = o_part;
+  p.lse_part = lse_part;
+  p.B = B; p.H = H; p.NB = NB; p.SUB = SUB; p.DR = DR; p.W = W;
+  p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit;
+  p.rescale_threshold = mlra::kRescaleThreshold;
+  if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool t128 = (NB * SUB == 1);
+  const int npad = H <= 16 ? 16 : (H <= 32 ? 32 : 64);
+  const int hgroups = (H + npad - 1) / npad;
+  if (DLS == 128) {
+    if (t128) {
+      if (npad == 16) return launch_decode<128, 16, 128>(map, p, hgroups, st);
+      if (npad == 32) return launch_decode<128, 32, 128>(map, p, hgroups, st);
+      return launch_decode<128, 64, 128>(map, p, hgroups, st);
+    }
+    if (npad == 16) return launch_decode<64, 16, 128>(map, p, hgroups, st);
+    if (npad == 32) return launch_decode<64, 32, 128>(map, p, hgroups, st);
+    return launch_decode<64, 64, 128>(map, p, hgroups, st);
+  }
+  if (t128) {
+    if (npad == 16) return launch_decode<128, 16, 64>(map, p, hgroups, st);
+    if (npad == 32) return launch_decode<128, 32, 64>(map, p, hgroups, st);
+    return launch_decode<128, 64, 64>(map, p, hgroups, st);
+  }
+  if (npad == 16) return launch_decode<64, 16, 64>(map, p, hgroups, st);
+  if (npad == 32) return launch_decode<64, 32, 64>(map, p, hgroups, st);
+  return launch_decode<64, 64, 64>(map, p, hgroups, st);
+}
+
+int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, int B, int H, int NB,
+                 int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
+  if (upproj && (DH % 2 != 0 || DH > 512)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d", DH);
+  constexpr int SEQ = 4;
+  const int threads = 256;
+  const int kslices = upproj ? threads / (DH / 2) : 1;
+  size_t zf = size_t(SEQ) * NB * DLAT;
+  size_t rf = size_t(kslices) * SEQ * DH;
+  const size_t smem = (zf > rf ? zf : rf) * sizeof(float);
+  if (smem > 200 * 1024) return fail(MLRA_ERR_CONFIG, "combine: smem %zu too large", smem);
+  static unsigned attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !(attr_done & (1u << dev))) {
+    cudaFuncSetAttribute(mlra::combine_kernel<SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (dev < 32) attr_done |= 1u << dev;
+  }
+  dim3 grid(H, (B + SEQ - 1) / SEQ);
+  mlra::combine_kernel<SEQ><<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+      o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT, DH, nsplit, alpha, upproj);
+  return cuda_check("combine launch");
+}
+
+int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
+                     const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
+                     int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
+                     int nsplit, float score_scale, float alpha, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  const int DLAT = SUB * DLS;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  void* q_abs = ws;
+  ws += al(size_t(B) * NB * H * DLAT * 2);
+  void* q_rope_s = ws;
+  ws += al(size_t(B) * H * DR * 2);
+  float* o_part = reinterpret_cast<float*>(ws);
+  ws += al(size_t(B) * nsplit * NB * H * DLAT * 4);
+  float* lse_part = reinterpret_cast<float*>(ws);
+  int rc = mlra_absorb_query(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
+  if (rc) return rc;
+  rc = mlra_decode_partials(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                            page_size, max_pages, num_pages, nsplit, stream);
+  if (rc) return rc;
+  return mlra_combine(o_part, lse_part, w_uv, out, B, H, NB, DLAT, DH, nsplit, alpha, 1, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+"""Torch-facing wrappers over the C ABI: one function per kernel, stream-ordered on the
+current torch CUDA stream, no host synchronisation.
+
+Tensors are plain torch CUDA tensors (bf16 for cache / queries / weights, fp32 for
+partials and outputs, int32 for page tables). Shapes follow include/mlra_b200.h.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .errors import ConfigError, ShapeMismatchError
+
+LOG2E = 1.4426950408889634
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(t: torch.Tensor, dtype, name: str, dim: int | None = None) -> None:
+    if not t.is_cuda:
+        raise ShapeMismatchError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ShapeMismatchError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ShapeMismatchError(f"{name} must be contiguous")
+    if dim is not None and t.dim() != dim:
+        raise ShapeMismatchError(f"{name} must be {dim}-D, got shape {tuple(t.shape)}")
+
+
+def num_sms() -> int:
+    return _lib.load().mlra_num_sms()
+
+
+def default_splits(batch: int, max_seqlen: int, nb: int, sub: int) -> int:
+    return _lib.load().mlra_default_splits(batch, max_seqlen, nb, sub)
+
+
+def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch.Tensor, pool: torch.Tensor,
+                 page_size: int) -> None:
+    """K0: pool[page(pos), pos % page_size] = rows[s] for every sequence s."""
+    _need(rows, torch.bfloat16, "rows", 2)
+    _need(block_table, torch.int32, "block_table", 2)
+    _need(positions, torch.int32, "positions", 1)
+    _need(pool, torch.bfloat16, "pool", 2)
+    B, W = rows.shape
+    if pool.shape[1] != W:
+        raise ShapeMismatchError(f"cache append: row width {W} != pool width {pool.shape[1]}")
+    rc = _lib.load().mlra_cache_append(rows.data_ptr(), block_table.data_ptr(), positions.data_ptr(), B, W,
+                                       page_size, block_table.shape[1], pool.data_ptr(), _stream())
+    _lib.check(rc, "mlra_cache_append")
+
+
+def absorb_query(q_nope: torch.Tensor, q_rope: torch.Tensor, w_uk_packed: torch.Tensor, nb: int, dlat: int,
+                 score_scale: float, out: tuple[torch.Tensor, torch.Tensor] | None = None):
+    """K1: q_abs [B, NB, H, DLAT] and scaled q_rope [B, H, DR] (both bf16)."""
+    _need(q_nope, torch.bfloat16, "q_nope", 3)
+    _need(q_rope, torch.bfloat16, "q_rope", 3)
+    _need(w_uk_packed, torch.bfloat16, "w_uk", 3)
+    B, H, DH = q_nope.shape
+    DR = q_rope.shape[2]
+    if tuple(w_uk_packed.shape) != (H, DH, nb * dlat):
+        raise ShapeMismatchError(f"w_uk packed shape {tuple(w_uk_packed.shape)} != {(H, DH, nb * dlat)}")
+    if out is None:
+        q_abs = torch.empty((B, nb, H, dlat), dtype=torch.bfloat16, device=q_nope.device)
+        q_rs = torch.empty((B, H, DR), dtype=torch.bfloat16, device=q_nope.device)
+    else:
+        q_abs, q_rs = out
+    rc = _lib.load().mlra_absorb_query(q_nope.data_ptr(), q_rope.data_ptr(), w_uk_packed.data_ptr(),
+                                       q_abs.data_ptr(), q_rs.data_ptr(), B, H, DH, nb, dlat, DR,
+                                       float(score_scale), _stream())
+    _lib.check(rc, "mlra_absorb_query")
+    return q_abs, q_rs
+
+
+def decode_partials(q_abs: torch.Tensor, q_rope: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor,
+                    seqlens: torch.Tensor, page_size: int, nb: int, sub: int, dls: int, nsplit: int,
+                    out: tuple[torch.Tensor, torch.Tensor] | None = None):
+    """K2: split-KV partials (o_part [B, nsplit, NB, H, DLAT], lse_part [B, nsplit, NB, H])."""
+    _need(q_abs, torch.bfloat16, "q_abs", 4)
+    _need(q_rope, torch.bfloat16, "q_rope", 3)
+    _need(pool, torch.bfloat16, "pool", 2)
+    _need(block_table, torch.int32, "block_table", 2)
+    _need(seqlens, torch.int32, "seqlens", 1)
+    B, NB, H, DLAT = q_abs.shape
+    DR = q_rope.shape[2]
+    if NB != nb or DLAT != sub * dls:
+        raise ShapeMismatchError(f"q_abs shape {tuple(q_abs.shape)} inconsistent with nb={nb} sub={sub} dls={dls}")
+    W = nb * DLAT + DR
+    if pool.shape[1] != W or pool.shape[0] % page_size:
+        raise ShapeMismatchError(f"pool shape {tuple(pool.shape)} inconsistent with row width {W}/page {page_size}")
+    if out is None:
+        o_part = torch.empty((B, nsplit, NB, H, DLAT), dtype=torch.float32, device=q_abs.device)
+        lse_part = torch.empty((B, nsplit, NB, H), dtype=torch.float32, device=q_abs.device)
+    else:
+        o_part, lse_part = out
+    rc = _lib.load().mlra_decode_partials(q_abs.data_ptr(), q_rope.data_ptr(), pool.data_ptr(),
+                                          block_table.data_ptr(), seqlens.data_ptr(), o_part.data_ptr(),
+                                          lse_part.data_ptr(), B, H, NB, sub, dls, DR, page_size,
+                                          block_table.shape[1], pool.shape[0] // page_size, nsplit, _stream())
+    _lib.check(rc, "mlra_decode_partials")
+    return o_part, lse_part
+
+
+def combine(o_part: torch.Tensor, lse_part: torch.Tensor, w_uv_packed: torch.Tensor | None, alpha: float,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    """K3: merge splits; with w_uv_packed [H, NB*DLAT, DH] also up-project and branch-sum."""
+    _need(o_part, torch.float32, "o_part", 5)
+    _need(lse_part, torch.float32, "lse_part", 4)
+    B, nsplit, NB, H, DLAT = o_part.shape
+    upproj = w_uv_packed is not None
+    if upproj:
+        _need(w_uv_packed, torch.bfloat16, "w_uv", 3)
+        DH = w_uv_packed.shape[2]
+        if tuple(w_uv_packed.shape[:2]) != (H, NB * DLAT):
+            raise ShapeMismatchError(f"w_uv packed shape {tuple(w_uv_packed.shape)} != {(H, NB * DLAT, DH)}")
+        shape = (B, H, DH)
+    else:
+        DH = DLAT
+        shape = (B, NB, H, DLAT)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=o_part.device)
+    rc = _lib.load().mlra_combine(o_part.data_ptr(), lse_part.data_ptr(),
+                                  w_uv_packed.data_ptr() if upproj else None, out.data_ptr(), B, H, NB, DLAT, DH,
+                                  nsplit, float(alpha), int(upproj), _stream())
+    _lib.check(rc, "mlra_combine")
+    return out
+
+
+class DecodeWorkspace:
+    """Device scratch for one fused decode step (sized by mlra_workspace_bytes)."""
+
+    def __init__(self, batch: int, heads: int, nb: int, dlat: int, dr: int, nsplit: int, device):
+        nbytes = _lib.load().mlra_workspace_bytes(batch, heads, nb, dlat, dr, nsplit)
+        self.key = (batch, heads, nb, dlat, dr, nsplit)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
+                sub: int, dls: int, nsplit: int, score_scale: float, alpha: float, workspace: DecodeWorkspace,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1 + K2 + K3 through the single C-ABI entry point mlra_decode_step."""
+    B, H, DH = q_nope.shape
+    DR = q_rope.shape[2]
+    dlat = sub * dls
+    if workspace.key != (B, H, nb, dlat, DR, nsplit):
+        raise ConfigError(f"workspace sized for {workspace.key}, call needs {(B, H, nb, dlat, DR, nsplit)}")
+    if out is None:
+        out = torch.empty((B, H, DH), dtype=torch.float32, device=q_nope.device)
+    rc = _lib.load().mlra_decode_step(q_nope.data_ptr(), q_rope.data_ptr(), w_uk_packed.data_ptr(),
+                                      w_uv_packed.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
+                                      seqlens.data_ptr(), out.data_ptr(), workspace.buf.data_ptr(), B, H, DH, nb,
+                                      sub, dls, DR, page_size, block_table.shape[1], pool.shape[0] // page_size,
+                                      nsplit, float(score_scale), float(alpha), _stream())
+    _lib.check(rc, "mlra_decode_step")
+    return out
+
+
+def score_scale(tau: float) -> float:
+    """Scale folded into the queries: scores are evaluated in the log2 domain."""
+    return float(tau) * LOG2E
+
+
+def latent_geometry(dlat: int) -> tuple[int, int]:
+    """(SUB, DLS): split a branch latent of width dlat into sub-blocks of 128 (or 64)."""
+    if dlat % 128 == 0:
+        return dlat // 128, 128
+    if dlat == 64:
+        return 1, 64
+    raise ConfigError(f"latent width {dlat} per branch must be 64 or a multiple of 128")
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+__all__ = [n for n in dir() if not n.startswith("_") and n not in ("math", "torch")]
