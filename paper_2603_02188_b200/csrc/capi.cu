@@ -43,27 +43,31 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-constexpr int kSmemBudget = 232448 - 1024;  // 227 KB opt-in minus static smem / slack
+constexpr int kSmemBudget = 232448;  // 227 KB opt-in dynamic smem (the kernel has no static smem)
 
-struct Choice {
-  int T, NPAD, DLS;
-};
-
-template <int T, int NPAD, int DLS>
-int launch_decode(const CUtensorMap& map, mlra::DecodeParams p, int head_groups, cudaStream_t stream) {
+template <int T, int NPAD, int DLS, int NB>
+int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra::DecodeParams p, int head_groups,
+                  cudaStream_t stream) {
   using L = mlra::DecodeLayout<T, NPAD, DLS>;
-  const int q_chunks = p.NB * p.SUB * (DLS / 64) + 1;
-  const int fixed = 1024 + q_chunks * L::kQChunkBytes + 2 * L::kPBytes + L::kScratchBytes;
-  int rope_slots = 3;
-  int lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
-  lat_slots = lat_slots > 16 ? 16 : lat_slots;
+  const int q_chunks = NB * p.SUB * (DLS / 64) + 1;
+  const int fixed = q_chunks * L::kQChunkBytes + 2 * L::kPBytes + L::kScratchBytes;
+  // Rope ring: up to 4 tiles deep for one-branch configs; shrink it before the latent ring.
+  int rope_slots = (NB == 1 && p.SUB == 1) ? 4 : (T == 64 ? 3 : 2);
+  int lat_slots = 0;
+  for (;; --rope_slots) {
+    lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
+    if (lat_slots >= 2 * p.SUB + 2 || rope_slots == 2) break;
+  }
+  if (lat_slots > mlra::kMaxLat) lat_slots = mlra::kMaxLat;
+  // QK(r+1) is issued while PV(r) still holds its sub-blocks: 2*SUB resident + 1 in flight
   if (lat_slots < 2 * p.SUB + 1)
     return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
                 2 * p.SUB + 1);
   p.lat_slots = lat_slots;
   p.rope_slots = rope_slots;
-  const int smem = L::smem_bytes(p.NB, p.SUB, lat_slots, rope_slots);
-  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS>;
+  const int smem = L::smem_bytes(NB, p.SUB, lat_slots, rope_slots);
+  if (smem > kSmemBudget) return fail(MLRA_ERR_CONFIG, "decode: smem %d exceeds budget", smem);
+  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS, NB>;
   static unsigned attr_done = 0;  // per instantiation, one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -73,8 +77,18 @@ int launch_decode(const CUtensorMap& map, mlra::DecodeParams p, int head_groups,
     if (dev < 32) attr_done |= 1u << dev;
   }
   dim3 grid(p.nsplit, p.B, head_groups);
-  kern<<<grid, mlra::kNumThreads, smem, stream>>>(map, p);
+  kern<<<grid, mlra::kNumThreads, smem, stream>>>(lat_map, rope_map, p);
   return cuda_check("mlra_decode_kernel launch");
+}
+
+// TMEM columns used: 2 S slots + NB*SUB O blocks, NPAD each (<= 512).
+int pick_npad(int H, int NB, int SUB) {
+  // registers: the softmax keeps NB x NPAD/2 sum partials per thread; cap NB = 4 at NPAD = 32
+  if (NB == 4) return H <= 16 ? 16 : 32;
+  for (int npad : {16, 32, 64}) {
+    if (H <= npad && (2 + NB * SUB) * npad <= 512) return npad;
+  }
+  return (2 + NB * SUB) * 64 <= 512 ? 64 : 32;  // more head groups, each re-reading the tile
 }
 
 }  // namespace
@@ -128,9 +142,10 @@ size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
   int sms = mlra_num_sms();
   if (sms <= 0) sms = 148;
-  const int T = (NB * SUB == 1) ? 128 : 64;
+  const int T = (SUB == 1) ? 128 : 64;
   const int tiles = (max_seqlen + T - 1) / T;
-  int s = (sms + B - 1) / B;  // one wave of CTAs (1 CTA / SM)
+  int s = sms / B;  // one wave of CTAs (1 CTA / SM); a partial second wave costs a full round
+  if (s < 1) s = 1;
   if (s > tiles) s = tiles;
   if (s > 64) s = 64;
   return s < 1 ? 1 : s;
@@ -151,15 +166,31 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
   const int W = NB * DLAT + DR;
   auto encode = get_encode();
   if (!encode) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap map;
-  cuuint64_t dims[2] = {cuuint64_t(W), cuuint64_t(num_pages) * cuuint64_t(page_size)};
-  cuuint64_t strides[1] = {cuuint64_t(W) * 2};
-  cuuint32_t box[2] = {64, 64};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled failed (%d): pool %p W=%d", int(cr), pool, W);
+  const int T = (SUB == 1) ? 128 : 64;  // SUB > 1 (MLA) keeps 2*SUB sub-blocks resident: 64-token tiles
+  const int box_rows = (page_size % T == 0) ? T : 64;
+  const cuuint64_t total_rows = cuuint64_t(num_pages) * cuuint64_t(page_size);
+  CUtensorMap rope_map, lat_map;
+  {
+    cuuint64_t dims[2] = {cuuint64_t(W), total_rows};
+    cuuint64_t strides[1] = {cuuint64_t(W) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&rope_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(2d) failed (%d): W=%d", int(cr), W);
+  }
+  {
+    // {64 columns, rows, latent chunk}: chunk stride 128 B, row stride W*2 B
+    cuuint64_t dims[3] = {64, total_rows, cuuint64_t(NB * DLAT / 64)};
+    cuuint64_t strides[2] = {cuuint64_t(W) * 2, 128};
+    cuuint32_t box[3] = {64, cuuint32_t(T), cuuint32_t(DLS / 64)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = encode(&lat_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d): W=%d", int(cr), W);
+  }
 
   mlra::DecodeParams p{};
   p.q_abs = static_cast<const __nv_bfloat16*>(q_abs);
@@ -168,32 +199,38 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
   p.seqlens = seqlens;
   p.o_part = o_part;
   p.lse_part = lse_part;
-  p.B = B; p.H = H; p.NB = NB; p.SUB = SUB; p.DR = DR; p.W = W;
-  p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit;
+  p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
+  p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
+  if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool t128 = (NB * SUB == 1);
-  const int npad = H <= 16 ? 16 : (H <= 32 ? 32 : 64);
+  const bool t128 = (T == 128);
+  const int npad = pick_npad(H, NB, SUB);
   const int hgroups = (H + npad - 1) / npad;
+#define MLRA_NPAD(TT, DD, NBB)                                                      \
+  do {                                                                              \
+    if (npad == 16) return launch_decode<TT, 16, DD, NBB>(lat_map, rope_map, p, hgroups, st); \
+    if (npad == 32) return launch_decode<TT, 32, DD, NBB>(lat_map, rope_map, p, hgroups, st); \
+    return launch_decode<TT, 64, DD, NBB>(lat_map, rope_map, p, hgroups, st);     \
+  } while (0)
+#define MLRA_DISPATCH(TT, DD)                                                                 \
+  do {                                                                                        \
+    if (NB == 1) MLRA_NPAD(TT, DD, 1);                                                        \
+    if (NB == 2) MLRA_NPAD(TT, DD, 2);                                                        \
+    if (npad == 16) return launch_decode<TT, 16, DD, 4>(lat_map, rope_map, p, hgroups, st);   \
+    return launch_decode<TT, 32, DD, 4>(lat_map, rope_map, p, hgroups, st);                   \
+  } while (0)
+  if (NB == 3) return fail(MLRA_ERR_CONFIG, "decode: NB=3 branches per device is not a TP layout");
+  if (!t128 && NB != 1) return fail(MLRA_ERR_CONFIG, "decode: multi-block latents (SUB>1) need NB=1");
   if (DLS == 128) {
-    if (t128) {
-      if (npad == 16) return launch_decode<128, 16, 128>(map, p, hgroups, st);
-      if (npad == 32) return launch_decode<128, 32, 128>(map, p, hgroups, st);
-      return launch_decode<128, 64, 128>(map, p, hgroups, st);
-    }
-    if (npad == 16) return launch_decode<64, 16, 128>(map, p, hgroups, st);
-    if (npad == 32) return launch_decode<64, 32, 128>(map, p, hgroups, st);
-    return launch_decode<64, 64, 128>(map, p, hgroups, st);
+    if (t128) MLRA_DISPATCH(128, 128);
+    MLRA_NPAD(64, 128, 1);
   }
-  if (t128) {
-    if (npad == 16) return launch_decode<128, 16, 64>(map, p, hgroups, st);
-    if (npad == 32) return launch_decode<128, 32, 64>(map, p, hgroups, st);
-    return launch_decode<128, 64, 64>(map, p, hgroups, st);
-  }
-  if (npad == 16) return launch_decode<64, 16, 64>(map, p, hgroups, st);
-  if (npad == 32) return launch_decode<64, 32, 64>(map, p, hgroups, st);
-  return launch_decode<64, 64, 64>(map, p, hgroups, st);
+  if (t128) MLRA_DISPATCH(128, 64);
+  MLRA_NPAD(64, 64, 1);
+#undef MLRA_DISPATCH
+#undef MLRA_NPAD
 }
 
 int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, int B, int H, int NB,

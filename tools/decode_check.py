@@ -13,13 +13,14 @@ sys.path.insert(0, ".")
 from paper_2603_02188_b200 import ops  # noqa: E402
 
 
-def make_case(B, H, DH, NB, DLAT, DR, lens, page_size=64, seed=0, dev="cuda"):
+def make_case(B, H, DH, NB, DLAT, DR, lens, page_size=64, seed=0, dev="cuda", contiguous=False):
     g = torch.Generator(device="cpu").manual_seed(seed)
     W = NB * DLAT + DR
     max_len = max(lens)
     max_pages = ops.ceil_div(max_len, page_size) + 1
     num_pages = B * max_pages + 3
-    perm = torch.randperm(num_pages, generator=g)[: B * max_pages].reshape(B, max_pages).to(torch.int32)
+    order = torch.arange(num_pages) if contiguous else torch.randperm(num_pages, generator=g)
+    perm = order[: B * max_pages].reshape(B, max_pages).to(torch.int32)
     pool = (torch.randn(num_pages * page_size, W, generator=g) * 1.5).to(torch.bfloat16)
     q_nope = torch.randn(B, H, DH, generator=g).to(torch.bfloat16)
     q_rope = torch.randn(B, H, DR, generator=g).to(torch.bfloat16)
@@ -65,7 +66,11 @@ def rel(a, b):
 def main():
     torch.manual_seed(0)
     cases = [
-        # name, B, H, DH, NB, DLAT, DR, lens, nsplit
+        # name, B, H, DH, NB, DLAT, DR, lens, nsplit[, page_size]
+        ("tiny-tp1-p128", 1, 4, 64, 4, 64, 32, [512], 4, 128),
+        ("p-tp4-p128", 3, 24, 128, 1, 128, 64, [1000, 4096, 77], 5, 128),
+        ("p-tp1-p256", 3, 24, 128, 4, 128, 64, [1000, 4096, 77], 5, 256),
+        ("mla-p128", 2, 24, 128, 1, 512, 64, [2000, 300], 4, 128),
         ("tiny-tp1", 1, 4, 64, 4, 64, 32, [512], 4),
         ("tiny-tp4", 1, 4, 64, 1, 64, 32, [512], 2),
         ("p-tp4", 3, 24, 128, 1, 128, 64, [1000, 4096, 77], 5),
@@ -76,8 +81,8 @@ def main():
         ("mla-tp4-6h", 2, 6, 128, 1, 512, 64, [2500, 65], 3),
     ]
     ok = True
-    for name, B, H, DH, NB, DLAT, DR, lens, nsplit in cases:
-        c = make_case(B, H, DH, NB, DLAT, DR, lens)
+    for name, B, H, DH, NB, DLAT, DR, lens, nsplit, *ps in cases:
+        c = make_case(B, H, DH, NB, DLAT, DR, lens, page_size=ps[0] if ps else 64)
         sub, dls = ops.latent_geometry(DLAT)
         scale = ops.score_scale((DH + DR) ** -0.5)
         alpha = 0.5
@@ -94,9 +99,12 @@ def main():
         ok &= good
         print(f"{name:12s} z_err={ez:.3e} out_err={eo:.3e} {'OK' if good else 'FAIL'}", flush=True)
     # quick timing of the TP4 / TP1 headline shapes
-    for name, NB, DLAT in (("p-tp4 B16 32K", 1, 128), ("p-tp1 B16 32K", 4, 128), ("mla B16 32K", 1, 512)):
+    for name, NB, DLAT, ps, contig in (("p-tp4 B16 32K", 1, 128, 64, False), ("p-tp4 B16 32K", 1, 128, 128, False),
+                                      ("p-tp4 B16 32K", 1, 128, 128, True), ("p-tp1 B16 32K", 4, 128, 128, False),
+                                      ("mla B16 32K", 1, 512, 128, False)):
         B, H, DH, DR, L = 16, 24, 128, 64, 32768
-        c = make_case(B, H, DH, NB, DLAT, DR, [L] * B)
+        name = f"{name} page={ps}{' contiguous' if contig else ''}"
+        c = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=ps, contiguous=contig)
         sub, dls = ops.latent_geometry(DLAT)
         nsplit = ops.default_splits(B, L, NB, sub)
         scale = ops.score_scale((DH + DR) ** -0.5)
