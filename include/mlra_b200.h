@@ -90,6 +90,8 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
  * Replaces decode.py:228 (einsum mc,cmp->mp) + decode.py:264-285 (reduce_contributions).
  *   w_uv [H, NB*DLAT, DH] bf16 head-major pre-pack of W^UV (weights.py:91-93)
  *   out  [B, H, DH] fp32 = alpha * sum_b Z_b . W^UV_(b),(h)     (upproj = 1)
+ *        [B, NB, H, DH] fp32 = alpha * Z_b . W^UV_(b),(h)         (upproj = 2: per-branch
+ *                              contributions, the (head, vec) list of attend_local)
  *        [B, NB, H, DLAT] fp32 = alpha * Z_b                      (upproj = 0)
  *   alpha = alpha_attn (latent.py:56-61: 1/sqrt(branches) for mlra, 1 otherwise)
  */

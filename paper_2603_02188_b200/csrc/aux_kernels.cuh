@@ -117,40 +117,45 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
     }
     return;
   }
-  // thread -> (d pair, k slice); partial sums over k slices reduced through smem
+  // thread -> (d pair, k slice); partial sums over k slices reduced through smem.
+  // upproj == 1: one accumulation over all NB*DLAT latent columns (ascending branch order)
+  //              -> out[s, h, :];  upproj == 2: per branch -> out[s, b, h, :] (no branch sum).
   const int DH2 = DH / 2;
   const int kslices = blockDim.x / DH2;
   const int d2 = threadIdx.x % DH2, ks = threadIdx.x / DH2;
   const __nv_bfloat162* w = reinterpret_cast<const __nv_bfloat162*>(w_uv + size_t(h) * NCOL * DH);
-  float acc[SEQ][2];
+  const int nout = (upproj == 2) ? NB : 1;
+  const int kspan = (upproj == 2) ? DLAT : NCOL;
+  float* red = z + SEQ * NCOL;  // [kslices][SEQ][DH] (host sizes the smem for both regions)
+  for (int ob = 0; ob < nout; ++ob) {
+    float acc[SEQ][2];
 #pragma unroll
-  for (int j = 0; j < SEQ; ++j) acc[j][0] = acc[j][1] = 0.f;
-  if (ks < kslices) {
-    for (int k = ks; k < NCOL; k += kslices) {
-      const float2 wv = __bfloat1622float2(w[size_t(k) * DH2 + d2]);
+    for (int j = 0; j < SEQ; ++j) acc[j][0] = acc[j][1] = 0.f;
+    if (ks < kslices) {
+      for (int k = ob * kspan + ks; k < (ob + 1) * kspan; k += kslices) {
+        const float2 wv = __bfloat1622float2(w[size_t(k) * DH2 + d2]);
+#pragma unroll
+        for (int j = 0; j < SEQ; ++j) {
+          const float zz = z[j * NCOL + k];
+          acc[j][0] = fmaf(zz, wv.x, acc[j][0]);
+          acc[j][1] = fmaf(zz, wv.y, acc[j][1]);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < SEQ; ++j) {
-        const float zz = z[j * NCOL + k];
-        acc[j][0] = fmaf(zz, wv.x, acc[j][0]);
-        acc[j][1] = fmaf(zz, wv.y, acc[j][1]);
+        red[(ks * SEQ + j) * DH + 2 * d2] = acc[j][0];
+        red[(ks * SEQ + j) * DH + 2 * d2 + 1] = acc[j][1];
       }
     }
-  }
-  __syncthreads();  // z no longer needed: reuse it for the k-slice reduction
-  float* red = z;   // [kslices][SEQ][DH]
-  if (ks < kslices) {
-#pragma unroll
-    for (int j = 0; j < SEQ; ++j) {
-      red[(ks * SEQ + j) * DH + 2 * d2] = acc[j][0];
-      red[(ks * SEQ + j) * DH + 2 * d2 + 1] = acc[j][1];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nseq * DH; i += blockDim.x) {
+      const int j = i / DH, d = i % DH;
+      float v = 0.f;
+      for (int k = 0; k < kslices; ++k) v += red[(k * SEQ + j) * DH + d];
+      if (upproj == 2) out[((size_t(s0 + j) * NB + ob) * H + h) * DH + d] = alpha * v;
+      else out[(size_t(s0 + j) * H + h) * DH + d] = alpha * v;
     }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nseq * DH; i += blockDim.x) {
-    const int j = i / DH, d = i % DH;
-    float v = 0.f;
-    for (int k = 0; k < kslices; ++k) v += red[(k * SEQ + j) * DH + d];
-    out[(size_t(s0 + j) * H + h) * DH + d] = alpha * v;
+    __syncthreads();
   }
 }
 

@@ -162,6 +162,8 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
   if (page_size <= 0 || page_size % 64 != 0) return fail(MLRA_ERR_CONFIG, "decode: page_size %d not a multiple of 64", page_size);
   if (nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "decode: nsplit %d not in [1,64]", nsplit);
   if (H < 1) return fail(MLRA_ERR_SHAPE, "decode: H=%d", H);
+  if (NB == 3) return fail(MLRA_ERR_CONFIG, "decode: NB=3 branches per device is not a TP layout");
+  if (SUB > 1 && NB != 1) return fail(MLRA_ERR_CONFIG, "decode: multi-block latents (SUB>1) need NB=1");
   const int DLAT = SUB * DLS;
   const int W = NB * DLAT + DR;
   auto encode = get_encode();
@@ -169,28 +171,51 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
   const int T = (SUB == 1) ? 128 : 64;  // SUB > 1 (MLA) keeps 2*SUB sub-blocks resident: 64-token tiles
   const int box_rows = (page_size % T == 0) ? T : 64;
   const cuuint64_t total_rows = cuuint64_t(num_pages) * cuuint64_t(page_size);
-  CUtensorMap rope_map, lat_map;
-  {
-    cuuint64_t dims[2] = {cuuint64_t(W), total_rows};
-    cuuint64_t strides[1] = {cuuint64_t(W) * 2};
-    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult cr = encode(&rope_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(2d) failed (%d): W=%d", int(cr), W);
+  // Tensor maps are pure host descriptors; cache the last few per thread so a decode loop
+  // over the same pool does not re-encode them every step.
+  struct MapEntry {
+    const void* pool;
+    cuuint64_t rows;
+    int W, T, box_rows, DLS, nlat;
+    CUtensorMap lat, rope;
+  };
+  thread_local MapEntry cache[8];
+  thread_local int cache_next = 0;
+  const int nlat = NB * DLAT / 64;
+  MapEntry* hit = nullptr;
+  for (auto& e : cache)
+    if (e.pool == pool && e.rows == total_rows && e.W == W && e.T == T && e.box_rows == box_rows && e.DLS == DLS &&
+        e.nlat == nlat)
+      hit = &e;
+  if (!hit) {
+    MapEntry e{pool, total_rows, W, T, box_rows, DLS, nlat, {}, {}};
+    {
+      cuuint64_t dims[2] = {cuuint64_t(W), total_rows};
+      cuuint64_t strides[1] = {cuuint64_t(W) * 2};
+      cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult cr = encode(&e.rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(2d) failed (%d): W=%d", int(cr), W);
+    }
+    {
+      // {64 columns, rows, latent chunk}: chunk stride 128 B, row stride W*2 B
+      cuuint64_t dims[3] = {64, total_rows, cuuint64_t(nlat)};
+      cuuint64_t strides[2] = {cuuint64_t(W) * 2, 128};
+      cuuint32_t box[3] = {64, cuuint32_t(T), cuuint32_t(DLS / 64)};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUresult cr = encode(&e.lat, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d): W=%d", int(cr), W);
+    }
+    cache[cache_next] = e;
+    hit = &cache[cache_next];
+    cache_next = (cache_next + 1) % 8;
   }
-  {
-    // {64 columns, rows, latent chunk}: chunk stride 128 B, row stride W*2 B
-    cuuint64_t dims[3] = {64, total_rows, cuuint64_t(NB * DLAT / 64)};
-    cuuint64_t strides[2] = {cuuint64_t(W) * 2, 128};
-    cuuint32_t box[3] = {64, cuuint32_t(T), cuuint32_t(DLS / 64)};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult cr = encode(&lat_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d): W=%d", int(cr), W);
-  }
+  const CUtensorMap& lat_map = hit->lat;
+  const CUtensorMap& rope_map = hit->rope;
 
   mlra::DecodeParams p{};
   p.q_abs = static_cast<const __nv_bfloat16*>(q_abs);
@@ -221,8 +246,6 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
     if (npad == 16) return launch_decode<TT, 16, DD, 4>(lat_map, rope_map, p, hgroups, st);   \
     return launch_decode<TT, 32, DD, 4>(lat_map, rope_map, p, hgroups, st);                   \
   } while (0)
-  if (NB == 3) return fail(MLRA_ERR_CONFIG, "decode: NB=3 branches per device is not a TP layout");
-  if (!t128 && NB != 1) return fail(MLRA_ERR_CONFIG, "decode: multi-block latents (SUB>1) need NB=1");
   if (DLS == 128) {
     if (t128) MLRA_DISPATCH(128, 128);
     MLRA_NPAD(64, 128, 1);
@@ -237,13 +260,14 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
                  int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
-  if (upproj && (DH % 2 != 0 || DH > 512)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d", DH);
+  if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
+  if (upproj && (DH % 2 != 0 || DH > 256)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not even / <= 256", DH);
   constexpr int SEQ = 4;
   const int threads = 256;
   const int kslices = upproj ? threads / (DH / 2) : 1;
-  size_t zf = size_t(SEQ) * NB * DLAT;
-  size_t rf = size_t(kslices) * SEQ * DH;
-  const size_t smem = (zf > rf ? zf : rf) * sizeof(float);
+  const size_t zf = size_t(SEQ) * NB * DLAT;
+  const size_t rf = upproj ? size_t(kslices) * SEQ * DH : 0;
+  const size_t smem = (zf + rf) * sizeof(float);
   if (smem > 200 * 1024) return fail(MLRA_ERR_CONFIG, "combine: smem %zu too large", smem);
   static unsigned attr_done = 0;
   int dev = 0;
