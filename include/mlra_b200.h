@@ -93,10 +93,11 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
  *        [B, NB, H, DH] fp32 = alpha * Z_b . W^UV_(b),(h)         (upproj = 2: per-branch
  *                              contributions, the (head, vec) list of attend_local)
  *        [B, NB, H, DLAT] fp32 = alpha * Z_b                      (upproj = 0)
+ *   scratch [B, H, NB*DLAT] fp32 (the merged latent; unused and may be NULL when upproj = 0)
  *   alpha = alpha_attn (latent.py:56-61: 1/sqrt(branches) for mlra, 1 otherwise)
  */
-int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, int B, int H, int NB,
-                 int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream);
+int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
+                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream);
 
 /*
  * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.

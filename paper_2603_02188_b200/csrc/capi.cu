@@ -123,20 +123,33 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
   if (B <= 0) return MLRA_OK;
   if (H <= 0 || DH <= 0 || NB <= 0 || DLAT <= 0 || DLAT % 2 != 0 || DR < 0)
     return fail(MLRA_ERR_SHAPE, "absorb_query: bad dims H=%d DH=%d NB=%d DLAT=%d DR=%d", H, DH, NB, DLAT, DR);
-  constexpr int SEQ = 4;
-  dim3 grid(H, (B + SEQ - 1) / SEQ);
-  const int smem = SEQ * DH * sizeof(float);
-  mlra::absorb_query_kernel<SEQ><<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(q_rope),
-      static_cast<const __nv_bfloat16*>(w_uk), static_cast<__nv_bfloat16*>(q_abs),
-      static_cast<__nv_bfloat16*>(q_rope_out), B, H, DH, NB * DLAT, DLAT, DR, score_scale);
+  const int NCOL = NB * DLAT;
+  if (NCOL % 8 != 0) return fail(MLRA_ERR_SHAPE, "absorb_query: NB*DLAT=%d not a multiple of 8", NCOL);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  constexpr int NT = 32;  // narrow column tiles: enough CTAs to cover the SMs at TP4
+  const size_t smem = mlra::head_gemm_smem<NT>(DH);
+  if (smem > 200 * 1024) return fail(MLRA_ERR_SHAPE, "absorb_query: DH=%d too large", DH);
+  auto kern = mlra::head_gemm_kernel<__nv_bfloat16, true, NT>;  // NOLINT
+  static unsigned attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !(attr_done & (1u << dev))) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (dev < 32) attr_done |= 1u << dev;
+  }
+  dim3 grid((NCOL + NT - 1) / NT, H, (B + mlra::kHG_S - 1) / mlra::kHG_S);
+  kern<<<grid, mlra::kHG_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(q_nope),
+                                              static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
+                                              score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
+                                              DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
   return cuda_check("absorb_query launch");
 }
 
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
-         al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4);
+         al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4) +
+         al(size_t(B) * NB * H * DLAT * 4);
 }
 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
@@ -256,30 +269,48 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
 #undef MLRA_NPAD
 }
 
-int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, int B, int H, int NB,
-                 int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
-  if (B <= 0) return MLRA_OK;
-  if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
-  if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
-  if (upproj && (DH % 2 != 0 || DH > 256)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not even / <= 256", DH);
-  constexpr int SEQ = 4;
-  const int threads = 256;
-  const int kslices = upproj ? threads / (DH / 2) : 1;
-  const size_t zf = size_t(SEQ) * NB * DLAT;
-  const size_t rf = upproj ? size_t(kslices) * SEQ * DH : 0;
-  const size_t smem = (zf + rf) * sizeof(float);
-  if (smem > 200 * 1024) return fail(MLRA_ERR_CONFIG, "combine: smem %zu too large", smem);
+// K3 needs a [B, H, NB*DLAT] fp32 scratch for the merged latent when it up-projects; the
+// standalone entry point allocates it from a per-thread cache (mlra_decode_step passes the
+// workspace slice instead).
+static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
+                        int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st) {
+  const int rows = B * NB * H;
+  const int warps_per_cta = 8;
+  if (upproj == 0) {
+    mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
+        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1);
+    return cuda_check("merge launch");
+  }
+  mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
+      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0);
+  const int kparts = (upproj == 2) ? NB : 1;
+  constexpr int NT = 32;
+  const int kp = NB * DLAT / kparts;
+  const size_t smem = mlra::head_gemm_smem<NT>(kp);
+  if (smem > 200 * 1024) return fail(MLRA_ERR_SHAPE, "combine: latent width %d too large", kp);
+  auto kern = mlra::head_gemm_kernel<float, false, NT>;
   static unsigned attr_done = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 32 || !(attr_done & (1u << dev))) {
-    cudaFuncSetAttribute(mlra::combine_kernel<SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (dev < 32) attr_done |= 1u << dev;
   }
-  dim3 grid(H, (B + SEQ - 1) / SEQ);
-  mlra::combine_kernel<SEQ><<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(
-      o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT, DH, nsplit, alpha, upproj);
-  return cuda_check("combine launch");
+  dim3 grid((DH + NT - 1) / NT, H, ((B + mlra::kHG_S - 1) / mlra::kHG_S) * kparts);
+  kern<<<grid, mlra::kHG_THREADS, smem, st>>>(zbuf, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
+                                              DH, kparts, alpha, 0, 0, nullptr, nullptr, 0);
+  return cuda_check("up-projection launch");
+}
+
+int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
+                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
+  if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
+  if (upproj && (DH % 8 != 0)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not a multiple of 8", DH);
+  if (upproj && scratch == nullptr) return fail(MLRA_ERR_CONFIG, "combine: up-projection needs a scratch buffer");
+  return combine_impl(o_part, lse_part, w_uv, out, scratch, B, H, NB, DLAT, DH, nsplit, alpha, upproj,
+                      static_cast<cudaStream_t>(stream));
 }
 
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
@@ -297,12 +328,15 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   float* o_part = reinterpret_cast<float*>(ws);
   ws += al(size_t(B) * nsplit * NB * H * DLAT * 4);
   float* lse_part = reinterpret_cast<float*>(ws);
+  ws += al(size_t(B) * nsplit * NB * H * 4);
+  float* zbuf = reinterpret_cast<float*>(ws);
   int rc = mlra_absorb_query(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
   if (rc) return rc;
   rc = mlra_decode_partials(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
                             page_size, max_pages, num_pages, nsplit, stream);
   if (rc) return rc;
-  return mlra_combine(o_part, lse_part, w_uv, out, B, H, NB, DLAT, DH, nsplit, alpha, 1, stream);
+  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
+                      static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -160,7 +160,7 @@ def absorb_query(q_nope, w_uk, *, device=None) -> np.ndarray:
         w = w.reshape(w.shape[0], m, p)
     lat = w.shape[0]
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    latp = lat + (-lat) % 2
+    latp = -(-lat // 8) * 8  # K1 streams weight rows in 16-byte vectors
     packed = np.zeros((m, p, latp))
     packed[:, :, :lat] = np.transpose(w, (1, 2, 0))
     qt = torch.as_tensor(q[None], dtype=torch.float32, device=dev).to(torch.bfloat16)
@@ -192,20 +192,7 @@ def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, qn, q
     q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, nb, layout.dlp, ops.score_scale(cfg.tau))
     o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, pc.block_table, pc.seqlens, pc.page_size, nb, sub, dls,
                                       nsplit)
-    if upproj == 2:
-        out = torch.empty((1, nb, qn.shape[1], qn.shape[2]), dtype=torch.float32, device=dev)
-        return _combine_mode(o_part, lse, w_uv, alpha, out, 2)
-    return ops.combine(o_part, lse, w_uv, alpha)
-
-
-def _combine_mode(o_part, lse, w_uv, alpha, out, mode):
-    from . import _lib
-
-    B, nsplit, NB, H, DLAT = o_part.shape
-    rc = _lib.load().mlra_combine(o_part.data_ptr(), lse.data_ptr(), w_uv.data_ptr(), out.data_ptr(), B, H, NB, DLAT,
-                                  w_uv.shape[2], nsplit, float(alpha), mode, ops._stream())
-    _lib.check(rc, "mlra_combine")
-    return out
+    return ops.combine(o_part, lse, w_uv, alpha, per_branch=(upproj == 2))
 
 
 def attend_local(cfg: AttnConfig, local_w, own: Ownership, cache: PagedLatentCache, queries: dict) -> list:

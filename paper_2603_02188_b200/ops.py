@@ -107,26 +107,31 @@ def decode_partials(q_abs: torch.Tensor, q_rope: torch.Tensor, pool: torch.Tenso
 
 
 def combine(o_part: torch.Tensor, lse_part: torch.Tensor, w_uv_packed: torch.Tensor | None, alpha: float,
-            out: torch.Tensor | None = None) -> torch.Tensor:
-    """K3: merge splits; with w_uv_packed [H, NB*DLAT, DH] also up-project and branch-sum."""
+            out: torch.Tensor | None = None, per_branch: bool = False, scratch: torch.Tensor | None = None):
+    """K3: merge splits; with w_uv_packed [H, NB*DLAT, DH] also up-project (summing branches,
+    or per branch when ``per_branch``)."""
     _need(o_part, torch.float32, "o_part", 5)
     _need(lse_part, torch.float32, "lse_part", 4)
     B, nsplit, NB, H, DLAT = o_part.shape
-    upproj = w_uv_packed is not None
-    if upproj:
+    mode = 0
+    if w_uv_packed is not None:
         _need(w_uv_packed, torch.bfloat16, "w_uv", 3)
         DH = w_uv_packed.shape[2]
         if tuple(w_uv_packed.shape[:2]) != (H, NB * DLAT):
             raise ShapeMismatchError(f"w_uv packed shape {tuple(w_uv_packed.shape)} != {(H, NB * DLAT, DH)}")
-        shape = (B, H, DH)
+        mode = 2 if per_branch else 1
+        shape = (B, NB, H, DH) if per_branch else (B, H, DH)
+        if scratch is None:
+            scratch = torch.empty((B, H, NB * DLAT), dtype=torch.float32, device=o_part.device)
     else:
         DH = DLAT
         shape = (B, NB, H, DLAT)
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=o_part.device)
     rc = _lib.load().mlra_combine(o_part.data_ptr(), lse_part.data_ptr(),
-                                  w_uv_packed.data_ptr() if upproj else None, out.data_ptr(), B, H, NB, DLAT, DH,
-                                  nsplit, float(alpha), int(upproj), _stream())
+                                  w_uv_packed.data_ptr() if mode else None, out.data_ptr(),
+                                  scratch.data_ptr() if mode else None, B, H, NB, DLAT, DH, nsplit, float(alpha),
+                                  mode, _stream())
     _lib.check(rc, "mlra_combine")
     return out
 

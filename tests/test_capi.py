@@ -63,7 +63,7 @@ def test_cpu_safe_calls(lib):
     assert rc == -2 and b"page_size" in lib.mlra_last_error()
     rc = lib.mlra_cache_append(None, None, None, 1, 7, 64, 1, None, None)
     assert rc == -1 and b"row width" in lib.mlra_last_error()
-    rc = lib.mlra_combine(None, None, None, None, 1, 1, 1, 128, 128, 1, 1.0, 3, None)
+    rc = lib.mlra_combine(None, None, None, None, None, 1, 1, 1, 128, 128, 1, 1.0, 3, None)
     assert rc == -2
     with pytest.raises(_lib.ConfigError):
         _lib.check(-2, "probe")

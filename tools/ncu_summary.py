@@ -1,0 +1,38 @@
+"""Summarise ncu captures into profiles/ (ncu_summary.json)."""
+import csv, json, os, subprocess, sys
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units, v = rows[0], rows[1], rows[2]
+    return {k: (v[i], units[i]) for i, k in enumerate(h)}
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "sm__cycles_elapsed.avg.per_second", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+def to_bytes(val, unit):
+    f = float(val.replace(",", ""))
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+
+summary = {}
+for name, rep, algo in [("mlra4_tp1_b16_n32768", "gpurun_out/k2_tp1.ncu-rep", 603979776),
+                        ("mlra4_tp4_b16_n32768", "gpurun_out/k2_tp4.ncu-rep", 201326592)]:
+    if not os.path.exists(rep):
+        continue
+    r = raw(rep)
+    dur_unit = r["gpu__time_duration.sum"][1]
+    dur_us = float(r["gpu__time_duration.sum"][0].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}[dur_unit]
+    rd = to_bytes(*r["dram__bytes_read.sum"])
+    wr = to_bytes(*r["dram__bytes_write.sum"])
+    summary[name] = {
+        "kernel": "mlra_decode_kernel (K2)", "duration_us_ncu": dur_us, "dram_bytes_read": rd, "dram_bytes_write": wr,
+        "dram_bytes_per_launch": rd + wr, "algorithmic_bytes": algo, "traffic_over_algorithmic": round((rd + wr) / algo, 4),
+        "metrics": {k: " ".join(r[k]) for k in WANT if k in r},
+        "note": "ncu --set full --clock-control none, cold L2, serialised: compare shares/bytes, not absolute time",
+    }
+os.makedirs("profiles", exist_ok=True)
+json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
+print(json.dumps(summary, indent=1))
