@@ -65,7 +65,9 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_
 int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream);
 
-/* Bytes of fp32 split-KV partials needed by mlra_decode_partials / mlra_decode_step. */
+/* Bytes of device workspace mlra_decode_step needs (split-KV partials, absorbed queries,
+ * merge scratch and per-sequence barrier state). Zero-initialise it once before first use;
+ * the barrier state is self-resetting afterwards. */
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit);
 
 /* Split count used when the caller passes nsplit <= 0 (fills the SMs for this batch). */
@@ -103,7 +105,10 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.
  * Replaces decode.py:304-305 (attend_local + reduce_contributions inside
  * absorbed_decode_step) for every unit a device owns.
- *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device)
+ * When B * nsplit * head_groups <= SM count, this is ONE cooperative kernel launch: the
+ * query absorption and the split merge + up-projection run inside the decode kernel around
+ * two self-resetting per-sequence barriers; otherwise K1, K2, K3 are launched in turn.
+ *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  */
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
                      const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,

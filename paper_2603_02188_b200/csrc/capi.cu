@@ -76,8 +76,18 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
       return cuda_check("cudaFuncSetAttribute(decode)");
     if (dev < 32) attr_done |= 1u << dev;
   }
-  dim3 grid(p.nsplit, p.B, head_groups);
-  kern<<<grid, mlra::kNumThreads, smem, stream>>>(lat_map, rope_map, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.nsplit, p.B, head_groups);
+  cfg.blockDim = dim3(mlra::kNumThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // fused mode spins on per-sequence barriers
+  attr[0].val.cooperative = p.fused ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, lat_map, rope_map, p) != cudaSuccess)
+    return cuda_check("mlra_decode_kernel launch");
   return cuda_check("mlra_decode_kernel launch");
 }
 
@@ -149,7 +159,7 @@ size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) 
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
          al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4) +
-         al(size_t(B) * NB * H * DLAT * 4);
+         al(size_t(B) * NB * H * DLAT * 4) + al(size_t(B) * ((H + 15) / 16) * 4 * sizeof(int));
 }
 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
@@ -164,9 +174,33 @@ int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
   return s < 1 ? 1 : s;
 }
 
+struct FusedArgs {
+  const void* q_nope;
+  const void* q_rope_in;
+  const void* w_uk;
+  const void* w_uv;
+  float* out;
+  int* sync;
+  int DH;
+  float score_scale, alpha;
+};
+
+static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
+                       const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
+                       int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
+                       const FusedArgs* fa);
+
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
                          int DLS, int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream) {
+  return decode_impl(q_abs, q_rope, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
+                     max_pages, num_pages, nsplit, stream, nullptr);
+}
+
+static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
+                       const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
+                       int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
+                       const FusedArgs* fa) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -239,6 +273,18 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
   p.lse_part = lse_part;
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
+  if (fa != nullptr) {
+    p.fused = 1;
+    p.q_nope = static_cast<const __nv_bfloat16*>(fa->q_nope);
+    p.q_rope_in = static_cast<const __nv_bfloat16*>(fa->q_rope_in);
+    p.w_uk = static_cast<const __nv_bfloat16*>(fa->w_uk);
+    p.w_uv = static_cast<const __nv_bfloat16*>(fa->w_uv);
+    p.out = fa->out;
+    p.sync = fa->sync;
+    p.DH = fa->DH;
+    p.score_scale = fa->score_scale;
+    p.alpha = fa->alpha;
+  }
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
   if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
@@ -330,6 +376,25 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   float* lse_part = reinterpret_cast<float*>(ws);
   ws += al(size_t(B) * nsplit * NB * H * 4);
   float* zbuf = reinterpret_cast<float*>(ws);
+  ws += al(size_t(B) * NB * H * DLAT * 4);
+  int* sync = reinterpret_cast<int*>(ws);
+  // Fused single-kernel step when every split of every (sequence, head group) can be
+  // co-resident (1 CTA per SM): K1 and K3 run inside K2 around two per-sequence barriers.
+  const int npad = pick_npad(H, NB, SUB);
+  const int hgroups = (H + npad - 1) / npad;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // The fused single-kernel step (K1/K3 folded into K2 behind grid/sequence barriers) is
+  // opt-in: it measured slower than K1 -> K2 -> K3 for MLRA-4 (cross-CTA barriers cost 2-4 us
+  // each on B200 and its W^UV pass is latency-bound), see profiles/ROUND1.md.
+  const bool fused_ok = getenv("MLRA_FUSED") != nullptr && (DH % 8) == 0 && DH <= 128 && NB * DLAT <= 512 &&
+                        nsplit <= 64 && long(B) * nsplit * hgroups <= sms;
+  if (fused_ok) {
+    FusedArgs fa{q_nope, q_rope, w_uk, w_uv, out, sync, DH, score_scale, alpha};
+    return decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                       page_size, max_pages, num_pages, nsplit, stream, &fa);
+  }
   int rc = mlra_absorb_query(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
   if (rc) return rc;
   rc = mlra_decode_partials(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,

@@ -46,10 +46,25 @@ struct DecodeParams {
   int box_rows;                 // token rows per TMA box: T when pages hold whole tiles, else 64
   float rescale_threshold;      // lazy-rescale threshold (log2 units)
   long long* trace;             // debug: per-round clock64 events of CTA (0,0,0), or null
+  // ---- fused mode (fused = 1): K1 and K3 folded into this kernel ---------------------------
+  // The nsplit CTAs of one (sequence, head group) each absorb a slice of the heads into q_abs
+  // (used as an L2-resident workspace), meet at a per-sequence barrier, run the split-KV
+  // attention, meet again after writing their partials, and each merges + up-projects its
+  // slice of heads into `out`. Needs every CTA of a sequence co-resident (cooperative launch).
+  int fused;
+  int DH;                       // query/output head width
+  float score_scale, alpha;     // tau*log2(e), alpha_attn
+  const __nv_bfloat16* q_nope;  // [B, H, DH]
+  const __nv_bfloat16* q_rope_in;  // [B, H, DR] (unscaled)
+  const __nv_bfloat16* w_uk;    // [H][DH][NB*DLAT]
+  const __nv_bfloat16* w_uv;    // [H][NB*DLAT][DH]
+  float* out;                   // [B, H, DH] = alpha * sum_b Z_b W^UV_b
+  int* sync;                    // [B * head_groups * 4] self-resetting barrier state (zeroed once)
 };
 
 constexpr int kNumThreads = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
 constexpr int kSoftThreads = 256;
+
 constexpr float kRescaleThreshold = 8.0f;  // P stays <= 2^8 between rescales
 constexpr int kMaxLat = 16, kMaxRope = 8;
 
@@ -76,14 +91,71 @@ struct DecodeLayout {
 __device__ __forceinline__ void trace_event(long long* trace, int ev, int r) {
   // events: 0 TMA issue of unit r, 1 QK(r) issue, 2 PV(r) issue, 3 S(r) seen, 4 P(r) done,
   //         5 MMA iteration r done, 6 QK(r) data ready (lat_full observed)
+  //         (softmax sub-phases) 7 S in registers, 8 vote done, 9 P slot free, 10 P stored
   if (trace != nullptr && r < 256 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-    trace[ev * 256 + r] = clock64();
+    trace[(ev < 7 ? ev * 256 : 12032 + (ev - 7) * 256) + r] = clock64();
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
   return t;
+}
+
+// Sense-reversing barrier across the `n` CTAs of one sequence (called by ONE thread per CTA).
+// Self-resetting: the last arriver zeroes the counter and flips the flag, so the state can be
+// reused by the next launch (and inside CUDA graphs) without host resets.
+__device__ __forceinline__ void seq_barrier(int* cnt, int* flag, int n) {
+  volatile int* vflag = flag;
+  const int old = *vflag;  // read before arriving: the flip needs our arrival
+  __threadfence();
+  if (atomicAdd(cnt, 1) == n - 1) {
+    atomicExch(cnt, 0);
+    __threadfence();
+    atomicExch(flag, old ^ 1);
+  } else {
+    while (*vflag == old) __nanosleep(64);
+  }
+  __threadfence();
+}
+
+// y[c] = scale * sum_k x[k] * W[k][c] for c in one 8-column octet, W bf16 row-major with row
+// stride ldw, x either bf16 (absorb: query row) or fp32 in smem (up-projection: merged latent).
+// Warp-cooperative: lane j accumulates rows k = j, j+32, ... with 16-byte loads (all issued
+// before use), then a butterfly over the 32 lanes; every lane returns the 8 sums.
+template <int K_PER_LANE_MAX, typename Tx>
+__device__ __forceinline__ void warp_gemv_octet(const __nv_bfloat16* __restrict__ W, size_t ldw, const Tx* x, int K,
+                                                float (&y)[8]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) y[j] = 0.f;
+  uint4 wv[K_PER_LANE_MAX];
+#pragma unroll
+  for (int i = 0; i < K_PER_LANE_MAX; ++i) {
+    const int k = lane + 32 * i;
+    wv[i] = (k < K) ? __ldg(reinterpret_cast<const uint4*>(W + size_t(k) * ldw)) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < K_PER_LANE_MAX; ++i) {
+    const int k = lane + 32 * i;
+    float xv = 0.f;
+    if (k < K) {
+      if constexpr (sizeof(Tx) == 2) xv = __bfloat162float(x[k]);
+      else xv = x[k];
+    }
+    const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(w2[j]);
+      y[2 * j] = fmaf(xv, f.x, y[2 * j]);
+      y[2 * j + 1] = fmaf(xv, f.y, y[2 * j + 1]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) y[j] += __shfl_xor_sync(0xffffffffu, y[j], off);
+  }
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -159,40 +231,127 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int i = 0; i < 4; ++i) mbar_init(&o_done[i], 1);
     mbar_init(o_final, 1);
+    tmem_base_sh[1] = 0;  // debug-trace check of the final CTA barrier
     fence_barrier_init();
     tma_prefetch_desc(&lat_map);
     tma_prefetch_desc(&rope_map);
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_sh);
 
-  // Absorbed + rotary queries of this (sequence, head group) -> K-major SW128 chunks.
-  // Chunk (b, c) holds latent columns [c*64, c*64+64) of branch b; the last chunk is rope.
-  {
-    const int nlat_chunks = NB * SUB * (DLS / 64);
-    const int total = q_chunks * NPAD * 8;  // 16-byte units
-    for (int idx = tid; idx < total; idx += kNumThreads) {
-      const int chunk = idx / (NPAD * 8);
-      const int rem = idx % (NPAD * 8);
-      const int r = rem / 8, u = rem % 8;
-      const int h = hg * NPAD + r;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (h < p.H) {
-        if (chunk < nlat_chunks) {
-          const int b = chunk / (DLAT / 64), c = chunk % (DLAT / 64);
-          v = *reinterpret_cast<const uint4*>(p.q_abs + ((size_t(seq) * NB + b) * p.H + h) * DLAT + c * 64 + u * 8);
-        } else if (u * 8 < p.DR) {
-          v = *reinterpret_cast<const uint4*>(p.q_rope + (size_t(seq) * p.H + h) * p.DR + u * 8);
-        }
-      }
-      *reinterpret_cast<uint4*>(q_smem + chunk * L::kQChunkBytes + r * 128 + ((u ^ (r & 7)) * 16)) = v;
-    }
-    for (int i = tid; i < 32 * NPAD; i += kNumThreads) m_run[i] = 0.f;  // set exactly on tile 0
-  }
+  for (int i = tid; i < 32 * NPAD; i += kNumThreads) m_run[i] = 0.f;  // set exactly on tile 0
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_sh;
+  // heads of this CTA's slice (fused mode: absorption and merge/up-projection work split)
+  const int hpc = (HV + p.nsplit - 1) / p.nsplit;
+  const int hs0 = min(HV, split * hpc), hs1 = min(HV, hs0 + hpc);
+  int* sync_base = p.sync + (size_t(seq) * gridDim.z + hg) * 4;
+
+  if (warp != 0) {
+    // ---- fused K1: absorb this CTA's heads into the q_abs workspace, then meet the other
+    //      splits of the sequence. The TMA producer (warp 0) is already streaming KV.
+    if (p.fused) {
+      {
+        // Work split over ALL CTAs of this head group (every sequence), so each W^UK byte is
+        // read once: units (head, 8-column octet) x all sequences. In a warp, lane = (k-slice
+        // j of DH/8 rows, sequence group g of 4); the 8 k-slices are reduced by shuffles.
+        const int C = gridDim.x * gridDim.y;
+        const int c = blockIdx.y * gridDim.x + blockIdx.x;
+        const int NCOL = NB * DLAT, octs = NCOL / 8, KS = p.DH / 8;
+        const int U = HV * octs;
+        const int u0 = int((long long)c * U / C), u1 = int((long long)(c + 1) * U / C);
+        const int j = lane & 7, g = lane >> 3;
+        for (int u = u0 + warp - 1; u < u1; u += kNumThreads / 32 - 1) {
+          const int hh = hg * NPAD + u / octs, col = (u % octs) * 8;
+          const __nv_bfloat16* wp = p.w_uk + (size_t(hh) * p.DH + j * KS) * NCOL + col;
+          uint4 wv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) wv[i] = i < KS ? __ldg(reinterpret_cast<const uint4*>(wp + size_t(i) * NCOL))
+                                                      : make_uint4(0, 0, 0, 0);
+          for (int s0 = 0; s0 < p.B; s0 += 4) {  // warp-uniform trip count (shuffles below)
+            const int sq = s0 + g;
+            const bool sv = sq < p.B;
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+            const __nv_bfloat16* xq = p.q_nope + (size_t(sv ? sq : 0) * p.H + hh) * p.DH + j * KS;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (i >= KS || !sv) break;
+              const float xv = __bfloat162float(xq[i]);
+              const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(w2[e]);
+                acc[2 * e] = fmaf(xv, f.x, acc[2 * e]);
+                acc[2 * e + 1] = fmaf(xv, f.y, acc[2 * e + 1]);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);
+              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 4);
+            }
+            if (j == 0 && sv) {
+              const int b = col / DLAT, cc = col % DLAT;
+              uint4 v;
+              v.x = pack_bf16(acc[0] * p.score_scale, acc[1] * p.score_scale);
+              v.y = pack_bf16(acc[2] * p.score_scale, acc[3] * p.score_scale);
+              v.z = pack_bf16(acc[4] * p.score_scale, acc[5] * p.score_scale);
+              v.w = pack_bf16(acc[6] * p.score_scale, acc[7] * p.score_scale);
+              *reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.q_abs) +
+                                        ((size_t(sq) * NB + b) * p.H + hh) * DLAT + cc) = v;
+            }
+          }
+        }
+        if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 4] = (long long)global_ns();
+        // scaled rope queries of the group, also split over the CTAs
+        const int R_all = p.B * HV * p.DR;
+        const int r0 = int((long long)c * R_all / C), r1 = int((long long)(c + 1) * R_all / C);
+        for (int i = r0 + tid - 32; i < r1; i += kNumThreads - 32) {
+          const int sq = i / (HV * p.DR), rem = i % (HV * p.DR);
+          const size_t off = (size_t(sq) * p.H + hg * NPAD + rem / p.DR) * p.DR + rem % p.DR;
+          const_cast<__nv_bfloat16*>(p.q_rope)[off] = __float2bfloat16(__bfloat162float(p.q_rope_in[off]) * p.score_scale);
+        }
+        __threadfence();
+      }
+      named_bar_sync(2, kNumThreads - 32);
+      if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 5] = (long long)global_ns();
+      if (tid == 32) seq_barrier(p.sync + hg * 4 + 0, p.sync + hg * 4 + 1, gridDim.x * gridDim.y);
+      named_bar_sync(2, kNumThreads - 32);
+      if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin] = (long long)global_ns();
+    }
+    // ---- absorbed + rotary queries of this (sequence, head group) -> K-major SW128 chunks.
+    //      Chunk (b, c) holds latent columns [c*64, c*64+64) of branch b; the last is rope.
+    {
+      const int nlat_chunks = NB * SUB * (DLS / 64);
+      const int total = q_chunks * NPAD * 8;  // 16-byte units
+      for (int idx = tid - 32; idx < total; idx += kNumThreads - 32) {
+        const int chunk = idx / (NPAD * 8);
+        const int rem = idx % (NPAD * 8);
+        const int r = rem / 8, u = rem % 8;
+        const int h = hg * NPAD + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (h < p.H) {
+          if (chunk < nlat_chunks) {
+            const int b = chunk / (DLAT / 64), c = chunk % (DLAT / 64);
+            v = __ldcg(reinterpret_cast<const uint4*>(p.q_abs + ((size_t(seq) * NB + b) * p.H + h) * DLAT + c * 64 +
+                                                      u * 8));
+          } else if (u * 8 < p.DR) {
+            v = __ldcg(reinterpret_cast<const uint4*>(p.q_rope + (size_t(seq) * p.H + h) * p.DR + u * 8));
+          }
+        }
+        *reinterpret_cast<uint4*>(q_smem + chunk * L::kQChunkBytes + r * 128 + ((u ^ (r & 7)) * 16)) = v;
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    named_bar_sync(2, kNumThreads - 32);
+    tc_fence_after();
+  }
 
   if (warp == 0) {
     // ============================================================ TMA producer
@@ -238,6 +397,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
+    if (lane == 1 && R > 0 && p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+      // debug trace only: true arrival time of every latent unit (event 11)
+      int ls = 0, lp = 0;
+      for (int u = 0; u < R * SUB && u < 256; ++u) {
+        mbar_wait(&lat_full[ls], lp);
+        p.trace[12032 + 4 * 256 + u] = clock64();
+        if (++ls == p.lat_slots) { ls = 0; lp ^= 1; }
+      }
+    }
   } else if (warp == 1) {
     // ============================================================ MMA issuer (one warp, elected lane)
     // Issue order: QK(0); then for every round r: QK(r+1), PV(r). QK(r+1) only needs the S
@@ -258,7 +426,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       int pv_t = 0, pv_b = 0, pv_lslot = 0;
       auto issue_qk = [&](int r) {
         const int sslot = r & 1;
+        if (lane == 0) trace_event(p.trace, 12, r);
         mbar_wait(&s_empty[sslot], ((r >> 1) & 1) ^ 1);
+        if (lane == 0) trace_event(p.trace, 13, r);
         const int rslot = qk_t % p.rope_slots;
         mbar_wait(&rope_full[rslot], (qk_t / p.rope_slots) & 1);
         const uint32_t d = tbase + S_COL + sslot * NPAD;
@@ -287,9 +457,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (qk_b == NB - 1) mma_commit_w(&rope_empty[rslot]);
         if (++qk_b == NB) { qk_b = 0; ++qk_t; }
       };
-      issue_qk(0);
-      for (int r = 0; r < R; ++r) {
-        if (r + 1 < R) issue_qk(r + 1);
+      auto issue_pv = [&](int r) {
         const int pslot = r & 1;
         mbar_wait(&p_full[pslot], (r >> 1) & 1);
         if (lane == 0) trace_event(p.trace, 2, r);
@@ -308,6 +476,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         mma_commit_w(&o_done[pv_b]);
         if (lane == 0) trace_event(p.trace, 5, r);
         if (++pv_b == NB) { pv_b = 0; ++pv_t; }
+      };
+      // Readiness-driven issue: PV(r) goes out as soon as P(r) is ready (it releases the
+      // latent slot, which is what keeps the TMA ring deep), QK(r+1) as soon as its tile has
+      // landed and its S slot is free; QK runs at most one round ahead of PV.
+      // Static issue order QK(0), then {QK(r+1), PV(r)}: QK(r+1) overlaps softmax(r). (A
+      // readiness-driven order -- PV as soon as P is ready -- measured 15-40% slower.)
+      issue_qk(0);
+      for (int r = 0; r < R; ++r) {
+        if (r + 1 < R) issue_qk(r + 1);
+        issue_pv(r);
       }
       // Single-phase barrier for the epilogue: o_done[b] may lag by two phases there, which
       // a parity wait cannot disambiguate.
@@ -361,6 +539,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
           for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]);
         }
+        if (ws == 0 && lane == 0) trace_event(p.trace, 7, r);
         tc_fence_before();
         mbar_arrive(&s_empty[sslot]);
         if ((t0 + t + 1) * T > len || !lane_ok) {  // partial tile / unused M=64 lanes
@@ -385,6 +564,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // m_run is finite (0 before the first tile), so masked lanes stay at -inf. The first
         // tile of the split always takes the slow path (uniform: no vote needed).
         const bool slow = (t == 0) ? true : named_bar_or(1, kSoftThreads, dmax > thr);
+        if (ws == 0 && lane == 0) trace_event(p.trace, 8, r);
         bool rescale = false;
         if (slow) {
           // exact tile max per head: warp max, then across the 4 quarters through smem
@@ -419,6 +599,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // ---- probabilities (log2 domain; the score scale is folded into the queries)
         const int pslot = r & 1;
         if (r >= 2) mbar_wait(&p_empty[pslot], ((r >> 1) - 1) & 1);
+        if (ws == 0 && lane == 0) trace_event(p.trace, 9, r);
         if (lane_ok) {
           uint8_t* prow = prow0 + pslot * L::kPBytes;
 #pragma unroll
@@ -440,6 +621,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
         }
+        if (ws == 0 && lane == 0) trace_event(p.trace, 10, r);
         // ---- rare: the running max moved -> rescale this group's O_b columns
         if (rescale) {
           // PV(t-2, b) is complete (it was issued before QK(t, b), whose S we consumed), so
@@ -530,10 +712,75 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
+    // ---- fused K3: once every split of this sequence has written its partials, CTA `split`
+    //      merges heads [hs0, hs1) over the splits and up-projects them with W^UV.
+    if (p.fused) {
+      __threadfence();
+      named_bar_sync(1, kSoftThreads);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 1] = (long long)global_ns();
+      if (ws == 0 && lane == 0) seq_barrier(sync_base + 2, sync_base + 3, p.nsplit);
+      named_bar_sync(1, kSoftThreads);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 2] = (long long)global_ns();
+      const int t = tid - 64;
+      const int NCOL = NB * DLAT;
+      // heads in chunks that fit the two (now idle) P buffers
+      const int hc = (2 * L::kPBytes) / (4 * (NCOL + NB * p.nsplit));
+      for (int hc0 = hs0; hc0 < hs1; hc0 += hc) {
+      const int nh = min(hc, hs1 - hc0);
+      float* zs = reinterpret_cast<float*>(p_smem);  // [nh][NCOL] merged latent of this chunk's heads
+      float* wsp = zs + nh * NCOL;                     // [nh][NB][nsplit] split weights
+      for (int i = t; i < nh * NB; i += kSoftThreads) {
+        const int hl = i / NB, b = i % NB;
+        const float* l = p.lse_part + (size_t(seq) * p.nsplit * NB + b) * p.H + hg * NPAD + hc0 + hl;  // stride NB*H
+        float m = -INFINITY;
+        for (int k = 0; k < p.nsplit; ++k) m = fmaxf(m, __ldcg(l + size_t(k) * NB * p.H));
+        float tot = 0.f;
+        float* wr = wsp + (hl * NB + b) * p.nsplit;
+        for (int k = 0; k < p.nsplit; ++k) {
+          const float lk = __ldcg(l + size_t(k) * NB * p.H);
+          const float w = (m == -INFINITY || lk == -INFINITY) ? 0.f : ex2(lk - m);
+          wr[k] = w;
+          tot += w;
+        }
+        const float inv = tot > 0.f ? 1.f / tot : 0.f;
+        for (int k = 0; k < p.nsplit; ++k) wr[k] *= inv;
+      }
+      named_bar_sync(1, kSoftThreads);
+      for (int i = t; i < nh * NCOL; i += kSoftThreads) {
+        const int hl = i / NCOL, col = i % NCOL, b = col / DLAT, c = col % DLAT;
+        const float* o = p.o_part + ((size_t(seq) * p.nsplit * NB + b) * p.H + hg * NPAD + hc0 + hl) * DLAT + c;
+        const float* wr = wsp + (hl * NB + b) * p.nsplit;
+        float acc = 0.f;
+        for (int k = 0; k < p.nsplit; ++k) acc = fmaf(wr[k], __ldcg(o + size_t(k) * NB * p.H * DLAT), acc);
+        zs[i] = acc;
+      }
+      named_bar_sync(1, kSoftThreads);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 6] = (long long)global_ns();
+      // out[hh, d] = alpha * sum_k Z[k] W^UV[hh][k][d]: warp-units (head, 8-column octet of d),
+      // K = NB*DLAT split across lanes (<= 512 -> <= 16 rows per lane)
+      const int octs = p.DH / 8;
+      for (int u = ws; u < nh * octs; u += 8) {
+        const int hl = u / octs, d8 = u % octs;
+        const int hh = hg * NPAD + hc0 + hl;
+        float y[8];
+        warp_gemv_octet<16>(p.w_uv + size_t(hh) * NCOL * p.DH + d8 * 8, p.DH, zs + hl * NCOL, NCOL, y);
+        if (lane < 2) {
+          float4 v = lane == 0 ? make_float4(y[0], y[1], y[2], y[3]) : make_float4(y[4], y[5], y[6], y[7]);
+          v.x *= p.alpha; v.y *= p.alpha; v.z *= p.alpha; v.w *= p.alpha;
+          *reinterpret_cast<float4*>(p.out + (size_t(seq) * p.H + hh) * p.DH + d8 * 8 + lane * 4) = v;
+        }
+      }
+      named_bar_sync(1, kSoftThreads);
+      }
+    }
   }
   tc_fence_before();
+  if (p.trace != nullptr && warp >= 2) atomicAdd(&tmem_base_sh[1], 1u);
   __syncthreads();
-  if (p.trace != nullptr && tid == 0 && cta_lin < 1024) p.trace[7 * 256 + 2 * cta_lin + 1] = (long long)global_ns();
+  if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
+    p.trace[7 * 256 + 2 * cta_lin + 1] = (long long)global_ns();
+    p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = tmem_base_sh[1];
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tbase);

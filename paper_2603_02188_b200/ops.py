@@ -142,7 +142,7 @@ class DecodeWorkspace:
     def __init__(self, batch: int, heads: int, nb: int, dlat: int, dr: int, nsplit: int, device):
         nbytes = _lib.load().mlra_workspace_bytes(batch, heads, nb, dlat, dr, nsplit)
         self.key = (batch, heads, nb, dlat, dr, nsplit)
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # barrier state must start at 0
 
 
 def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,

@@ -264,3 +264,33 @@ def test_kimi_64_heads_tp4():
     for head, vec in contribs:
         want[head] += vec
     assert ak.max_rel_err(ak.calib_alphas(ocfg)[2] * want, got) <= TOL  # scaling=False here: alpha = 1
+
+
+@pytest.mark.parametrize("variant", ["mlra", "mla"])
+def test_opt_in_fused_step_matches_three_kernel_step(variant, monkeypatch):
+    """MLRA_FUSED=1 folds K1/K3 into K2 (grid + per-sequence barriers, cooperative launch).
+    It must reproduce the default K1 -> K2 -> K3 step up to reduction order, for ragged
+    lengths and both variants, and keep doing so over repeated calls (self-resetting barriers)."""
+    mlra = _mlra()
+    cfg = mlra.trained_config("mlra4" if variant == "mlra" else "mla").with_(d=256, d_cq=256)
+    ocfg = _oracle_cfg(cfg)
+    w = ak.build_weights(ocfg, 0.02, 4, ("w",))
+    lens = [5, 64, 300, 1000]
+    seq_streams, qns, qrs = [], [], []
+    for i, n in enumerate(lens):
+        hidden = ak.normal(4, ("h", i), (n, cfg.d))
+        seq_streams.append(ak.latent_streams(ocfg, w, hidden))
+        qn, qr, _, _ = ak.latent_projections(ocfg, w, hidden[-1:], [n - 1])
+        qns.append(ak.bf16_round(qn[0]))
+        qrs.append(ak.bf16_round(qr[0]))
+    eng = mlra.DecodeEngine(cfg, w, batch=len(lens), max_tokens=max(lens), page_size=64, nsplit=4)
+    rounded = _engine_inputs(eng, seq_streams)
+    monkeypatch.delenv("MLRA_FUSED", raising=False)
+    base = _run(eng, qns, qrs)
+    monkeypatch.setenv("MLRA_FUSED", "1")
+    for _ in range(3):
+        got = _run(eng, qns, qrs)
+        assert ak.max_rel_err(base, got) <= TOL_ORDER
+    wb = _bf16_weights(w)
+    for i in range(len(lens)):
+        assert ak.max_rel_err(ak.decode_attention(ocfg, wb, rounded[i], qns[i], qrs[i]), got[i]) <= TOL

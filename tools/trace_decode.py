@@ -2,7 +2,7 @@
 import os, sys, torch
 sys.path.insert(0, "."); sys.path.insert(0, "tools")
 from decode_check import make_case
-trace = torch.zeros(7 * 256 + 2048, dtype=torch.int64, device="cuda")
+trace = torch.zeros(12032 + 7 * 256, dtype=torch.int64, device="cuda")
 os.environ["MLRA_DEBUG_TRACE_PTR"] = str(trace.data_ptr())
 from paper_2603_02188_b200 import ops
 which = sys.argv[1]
@@ -21,7 +21,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 tt = trace.cpu()
 t = tt[: 7 * 256].view(7, 256)
-cta = tt[7 * 256:].view(1024, 2)
+cta = tt[7 * 256:7 * 256 + 2048].view(1024, 2)
 base = t[0, 0].item()
 n = int((t[1] != 0).sum())
 print("round  tma_issue  data_rdy  qk_issue  S_seen    P_done  pv_issue  mma_done (cycles from first TMA)")
@@ -37,3 +37,25 @@ t0 = st.min()
 dur = (en - st) / 1e3
 print(f"CTAs {n_cta}: start spread {(st.max() - t0).item() / 1e3:.1f} us, end max {(en.max() - t0).item() / 1e3:.1f} us, "
       f"dur min/med/max {dur.min().item():.1f}/{dur.median().item():.1f}/{dur.max().item():.1f} us")
+
+import statistics as _st
+rr = range(4, n - 4)
+def med(xs): return int(_st.median(xs)) if xs else -1
+print("median TMA latency (data_rdy - tma_issue):", med([(t[6, r] - t[0, r]).item() for r in rr]),
+      "| slot hold (mma_done - data_rdy):", med([(t[5, r] - t[6, r]).item() for r in rr]),
+      "| QK->S_seen:", med([(t[3, r] - t[1, r]).item() for r in rr]),
+      "| P_done->pv_issue:", med([(t[2, r] - t[4, r]).item() for r in rr]),
+      "| period:", med([(t[6, r + 1] - t[6, r]).item() for r in rr]))
+sub = tt[12032:12032 + 1024].view(4, 256)
+arr = tt[12032 + 1024:12032 + 1280]
+print("softmax sub-phases (median cycles): S_seen->S_in_regs", med([(sub[0, r] - t[3, r]).item() for r in rr]),
+      "| ->vote", med([(sub[1, r] - sub[0, r]).item() for r in rr]),
+      "| ->P slot free", med([(sub[2, r] - sub[1, r]).item() for r in rr]),
+      "| ->P stored", med([(sub[3, r] - sub[2, r]).item() for r in rr]),
+      "| ->P_done(fence+arrive)", med([(t[4, r] - sub[3, r]).item() for r in rr]))
+print("TRUE TMA latency (arrival - issue):", med([(arr[r] - t[0, r]).item() for r in rr]),
+      "| arrival -> QK data_rdy seen:", med([(t[6, r] - arr[r]).item() for r in rr]))
+e12 = tt[12032 + 5 * 256:12032 + 6 * 256]; e13 = tt[12032 + 6 * 256:12032 + 7 * 256]
+print("MMA warp: prev mma_done -> issue_qk entry", med([(e12[r] - t[5, r - 2]).item() for r in rr]),
+      "| s_empty wait", med([(e13[r] - e12[r]).item() for r in rr]),
+      "| rope+lat wait", med([(t[6, r] - e13[r]).item() for r in rr]))
