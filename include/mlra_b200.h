@@ -105,9 +105,12 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.
  * Replaces decode.py:304-305 (attend_local + reduce_contributions inside
  * absorbed_decode_step) for every unit a device owns.
- * When B * nsplit * head_groups <= SM count, this is ONE cooperative kernel launch: the
- * query absorption and the split merge + up-projection run inside the decode kernel around
- * two self-resetting per-sequence barriers; otherwise K1, K2, K3 are launched in turn.
+ * Default: K1, K2, K3 launched in turn on `stream`. Opt-in (environment MLRA_FUSED=1, and
+ * B * nsplit * head_groups <= SM count): ONE cooperative launch in which the query
+ * absorption (split over all CTAs of a head group, behind a group barrier) and the split
+ * merge + up-projection (behind a per-sequence barrier) run inside the decode kernel; the
+ * barriers are self-resetting, so the workspace is zeroed once. Same results up to
+ * reduction order; slower on B200 for MLRA-4 (profiles/ROUND1.md).
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  */
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
