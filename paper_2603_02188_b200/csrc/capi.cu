@@ -43,6 +43,36 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// Launch with (pdl = true) programmatic stream serialization: the kernel may start before its
+// predecessor on the stream finishes and must griddepcontrol.wait before consuming its output.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                      Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+template <typename K>
+int set_smem_once(K kern, unsigned& done_mask, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 32 && (done_mask & (1u << dev))) return MLRA_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return cuda_check("cudaFuncSetAttribute");
+  if (dev < 32) done_mask |= 1u << dev;
+  return MLRA_OK;
+}
+
 constexpr int kSmemBudget = 232448;  // 227 KB opt-in dynamic smem (the kernel has no static smem)
 
 template <int T, int NPAD, int DLS, int NB>
@@ -81,11 +111,13 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
   cfg.blockDim = dim3(mlra::kNumThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // fused mode spins on per-sequence barriers
   attr[0].val.cooperative = p.fused ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (p.pdl && !p.fused) ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (cudaLaunchKernelEx(&cfg, kern, lat_map, rope_map, p) != cudaSuccess)
     return cuda_check("mlra_decode_kernel launch");
   return cuda_check("mlra_decode_kernel launch");
@@ -133,25 +165,35 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
   if (B <= 0) return MLRA_OK;
   if (H <= 0 || DH <= 0 || NB <= 0 || DLAT <= 0 || DLAT % 2 != 0 || DR < 0)
     return fail(MLRA_ERR_SHAPE, "absorb_query: bad dims H=%d DH=%d NB=%d DLAT=%d DR=%d", H, DH, NB, DLAT, DR);
-  const int NCOL = NB * DLAT;
-  if (NCOL % 8 != 0) return fail(MLRA_ERR_SHAPE, "absorb_query: NB*DLAT=%d not a multiple of 8", NCOL);
+  if (DLAT % 8 != 0) return fail(MLRA_ERR_SHAPE, "absorb_query: DLAT=%d not a multiple of 8", DLAT);
+  if (DH > 1024) return fail(MLRA_ERR_SHAPE, "absorb_query: DH=%d too large", DH);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  constexpr int NT = 32;  // narrow column tiles: enough CTAs to cover the SMs at TP4
-  const size_t smem = mlra::head_gemm_smem<NT>(DH);
-  if (smem > 200 * 1024) return fail(MLRA_ERR_SHAPE, "absorb_query: DH=%d too large", DH);
-  auto kern = mlra::head_gemm_kernel<__nv_bfloat16, true, NT>;  // NOLINT
-  static unsigned attr_done = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 32 || !(attr_done & (1u << dev))) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (dev < 32) attr_done |= 1u << dev;
+  if (DH % 32 != 0) {
+    // small/odd head widths (the reference's test dims): per-head GEMM, whole K in smem
+    constexpr int NT = 32;
+    const size_t smem = mlra::head_gemm_smem<NT>(DH);
+    auto kern = mlra::head_gemm_kernel<__nv_bfloat16, true, NT>;
+    static unsigned hg_done = 0;
+    if (int rc = set_smem_once(kern, hg_done, 200 * 1024)) return rc;
+    const int NCOL = NB * DLAT;
+    dim3 grid((NCOL + NT - 1) / NT, H, (B + mlra::kHG_S - 1) / mlra::kHG_S);
+    kern<<<grid, mlra::kHG_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(q_nope),
+                                                static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
+                                                score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
+                                                DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
+    return cuda_check("absorb_query launch");
   }
-  dim3 grid((NCOL + NT - 1) / NT, H, (B + mlra::kHG_S - 1) / mlra::kHG_S);
-  kern<<<grid, mlra::kHG_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(q_nope),
-                                              static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
-                                              score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
-                                              DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
+  const size_t smem = mlra::absorb_smem(DH);
+  static unsigned attr_done = 0;
+  if (int rc = set_smem_once(mlra::absorb_kernel, attr_done, int(mlra::absorb_smem(1024)))) return rc;
+  const int NCOL = NB * DLAT;
+  dim3 grid((NCOL + mlra::kAbsCols - 1) / mlra::kAbsCols, H);
+  if (launch_ex(mlra::absorb_kernel, grid, dim3(mlra::kAbsThreads), smem, st, false,
+                static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(w_uk),
+                static_cast<__nv_bfloat16*>(q_abs), B, H, DH, NB, DLAT, score_scale,
+                static_cast<const __nv_bfloat16*>(q_rope), DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr,
+                DR) != cudaSuccess)
+    return cuda_check("absorb_query launch");
   return cuda_check("absorb_query launch");
 }
 
@@ -188,7 +230,7 @@ struct FusedArgs {
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       const FusedArgs* fa);
+                       const FusedArgs* fa, bool pdl = false);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
@@ -200,7 +242,7 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       const FusedArgs* fa) {
+                       const FusedArgs* fa, bool pdl) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -273,6 +315,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.lse_part = lse_part;
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
+  p.pdl = pdl ? 1 : 0;
   if (fa != nullptr) {
     p.fused = 1;
     p.q_nope = static_cast<const __nv_bfloat16*>(fa->q_nope);
@@ -319,9 +362,26 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
 // standalone entry point allocates it from a per-thread cache (mlra_decode_step passes the
 // workspace slice instead).
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
-                        int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st) {
+                        int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
+                        bool pdl = false) {
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
+  // partials staged in smem by bulk copies when they fit next to W^UV (the common case)
+  const int staged = (mlra::combine_smem(NB, DLAT, DH, nsplit, 1) <= size_t(kSmemBudget) && (DLAT * 4) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(o_part) & 15) == 0) ? 1 : 0;
+  const size_t csmem = mlra::combine_smem(NB, DLAT, DH, nsplit, staged);
+  if (upproj != 0 && DH % 4 == 0 && DH <= 128 && NB <= 4 && csmem <= size_t(kSmemBudget) &&
+      (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0 && (size_t(NB) * DLAT * DH * 2) % 16 == 0) {
+    // one kernel: merge + up-projection, W^UV staged by bulk copy (common case)
+    static unsigned attr_done = 0;
+    if (int rc = set_smem_once(mlra::combine_upproj_kernel, attr_done, kSmemBudget)) return rc;
+    dim3 grid(H, (B + mlra::kCmbSeqs - 1) / mlra::kCmbSeqs);
+    if (launch_ex(mlra::combine_upproj_kernel, grid, dim3(mlra::kCmbThreads), csmem, st, pdl, o_part, lse_part,
+                  static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT, DH, nsplit, alpha,
+                  upproj == 2 ? 1 : 0, staged) != cudaSuccess)
+      return cuda_check("combine launch");
+    return cuda_check("combine launch");
+  }
   if (upproj == 0) {
     mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
         o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1);
@@ -397,11 +457,15 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   }
   int rc = mlra_absorb_query(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
   if (rc) return rc;
-  rc = mlra_decode_partials(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
-                            page_size, max_pages, num_pages, nsplit, stream);
+  // K2 and K3 are chained with programmatic dependent launch: K2's TMA producer streams the
+  // cache while K1 drains (the cache was written before K1 started), K3 bulk-loads W^UV while
+  // K2 drains; both wait on their predecessor before touching its output.
+  const bool pdl = getenv("MLRA_NO_PDL") == nullptr;
+  rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
+                   max_pages, num_pages, nsplit, stream, nullptr, pdl);
   if (rc) return rc;
   return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream), pdl);
 }
 
 }  // extern "C"

@@ -60,6 +60,7 @@ struct DecodeParams {
   const __nv_bfloat16* w_uv;    // [H][NB*DLAT][DH]
   float* out;                   // [B, H, DH] = alpha * sum_b Z_b W^UV_b
   int* sync;                    // [B * head_groups * 4] self-resetting barrier state (zeroed once)
+  int pdl;                      // host side: launch with programmatic stream serialization
 };
 
 constexpr int kNumThreads = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  griddep_launch_dependents();  // K3 (PDL) may launch; it waits for this grid before reading
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
   // TMEM columns: S slots [0, 2*NPAD); O_{b,s} at O_COL + (b*SUB+s)*NPAD
   constexpr uint32_t kTmemCols = 512;
@@ -324,6 +326,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       named_bar_sync(2, kNumThreads - 32);
       if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin] = (long long)global_ns();
     }
+    // Under PDL this kernel overlaps K1's tail: the TMA producer is already streaming the
+    // cache (written before K1 started); the queries are K1's output.
+    griddep_wait();
     // ---- absorbed + rotary queries of this (sequence, head group) -> K-major SW128 chunks.
     //      Chunk (b, c) holds latent columns [c*64, c*64+64) of branch b; the last is rope.
     {

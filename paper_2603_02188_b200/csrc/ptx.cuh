@@ -106,6 +106,22 @@ __device__ __forceinline__ void tma_load_3d_hint(const void* desc, uint64_t* bar
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// Programmatic dependent launch (PDL). launch_dependents lets the next kernel on the stream
+// (launched with the programmatic-serialization attribute) start its prologue; wait blocks
+// until every kernel this one depends on has completed and its writes are visible. Both
+// are no-ops when the kernel was not launched that way.
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// 1-D bulk copy global -> this CTA's shared memory, completion counted on bar (tx bytes).
+// 16-byte aligned addresses, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Bulk L2 prefetch of [src, src+bytes) (16-byte aligned, bytes % 16 == 0); fire and forget.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
