@@ -123,14 +123,16 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
   return cuda_check("mlra_decode_kernel launch");
 }
 
-// TMEM columns used: 2 S slots + NB*SUB O blocks, NPAD each (<= 512).
+// TMEM columns used: 2 S slots (+ 2 rope-logit slots when NB > 1) + NB*SUB O blocks, NPAD each (<= 512).
 int pick_npad(int H, int NB, int SUB) {
   // registers: the softmax keeps NB x NPAD/2 sum partials per thread; cap NB = 4 at NPAD = 32
   if (NB == 4) return H <= 16 ? 16 : 32;
+  // S slots (2) + shared rope-logit slots (2, NB > 1) + one O block per sub-block
+  const int slots = 2 + (NB > 1 ? 2 : 0) + NB * SUB;
   for (int npad : {16, 32, 64}) {
-    if (H <= npad && (2 + NB * SUB) * npad <= 512) return npad;
+    if (H <= npad && slots * npad <= 512) return npad;
   }
-  return (2 + NB * SUB) * 64 <= 512 ? 64 : 32;  // more head groups, each re-reading the tile
+  return slots * 64 <= 512 ? 64 : 32;  // more head groups, each re-reading the tile
 }
 
 }  // namespace
@@ -331,6 +333,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
   if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
+  if (const char* e = getenv("MLRA_DEBUG_TRACE_CTA")) p.trace_cta = atoi(e);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool t128 = (T == 128);
   const int npad = pick_npad(H, NB, SUB);

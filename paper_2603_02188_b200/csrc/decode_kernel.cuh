@@ -21,9 +21,13 @@
 // Pool row layout (width W): [branch 0 latent | ... | branch NB-1 latent | rope]; each
 // branch latent = SUB sub-blocks of DLS columns (MLA: SUB = 4).
 //
-// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
+// Warp roles (352 threads): warp 0 = TMA producer, warp 1 = TMEM owner + QK issuer,
 // warps 2..9 = softmax / rescale / epilogue in two groups of four (one warp per TMEM lane
-// quarter each); the groups split the heads of every round.
+// quarter each; the groups split the heads of every round), warp 10 = PV issuer. QK and PV
+// are issued by different warps so that neither waits behind the other's dependencies
+// (a QK waiting for its tile no longer holds back the PV that frees a ring slot).
+// With NB > 1 branches per tile the rope logits (identical in every branch, Eq. 5) are
+// computed once per tile into their own TMEM slot and added by the softmax warps.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -45,7 +49,8 @@ struct DecodeParams {
   int lat_slots, rope_slots;    // ring depths (set by the host from the smem budget)
   int box_rows;                 // token rows per TMA box: T when pages hold whole tiles, else 64
   float rescale_threshold;      // lazy-rescale threshold (log2 units)
-  long long* trace;             // debug: per-round clock64 events of CTA (0,0,0), or null
+  long long* trace;             // debug: per-round clock64 events of CTA `trace_cta`, or null
+  int trace_cta;                // debug: linear CTA index traced (x fastest)
   // ---- fused mode (fused = 1): K1 and K3 folded into this kernel ---------------------------
   // The nsplit CTAs of one (sequence, head group) each absorb a slice of the heads into q_abs
   // (used as an L2-resident workspace), meet at a per-sequence barrier, run the split-KV
@@ -63,7 +68,8 @@ struct DecodeParams {
   int pdl;                      // host side: launch with programmatic stream serialization
 };
 
-constexpr int kNumThreads = 320;  // TMA warp, MMA warp, 2 x 4 softmax warps
+constexpr int kNumThreads = 352;  // TMA warp, QK warp, 2 x 4 softmax warps, PV warp
+constexpr int kPvWarp = 10;
 constexpr int kSoftThreads = 256;
 
 constexpr float kRescaleThreshold = 8.0f;  // P stays <= 2^8 between rescales
@@ -80,7 +86,7 @@ struct DecodeLayout {
   // red[2][4][NPAD] + aw[8][NPAD] + m_run[8][4][NPAD] + lred[4][4][NPAD] + invl[4][NPAD]
   static constexpr int kScratchFloats = 8 * NPAD + 8 * NPAD + 32 * NPAD + 16 * NPAD + 4 * NPAD;
   static constexpr int kBarOff = ((kScratchFloats * 4 + 127) / 128) * 128;
-  static constexpr int kNumBars = 2 * kMaxLat + 2 * kMaxRope + 8 + 4 + 1;
+  static constexpr int kNumBars = 2 * kMaxLat + 2 * kMaxRope + 8 + 4 + 1 + 2;
   static constexpr int kScratchBytes = kBarOff + kNumBars * 8 + 8;
   static int smem_bytes(int NB, int SUB, int lat_slots, int rope_slots) {
     const int q_chunks = NB * SUB * (DLS / 64) + 1;
@@ -89,11 +95,15 @@ struct DecodeLayout {
   }
 };
 
-__device__ __forceinline__ void trace_event(long long* trace, int ev, int r) {
+__device__ __forceinline__ bool is_trace_cta(int trace_cta) {
+  return int((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) == trace_cta;
+}
+
+__device__ __forceinline__ void trace_event(long long* trace, int trace_cta, int ev, int r) {
   // events: 0 TMA issue of unit r, 1 QK(r) issue, 2 PV(r) issue, 3 S(r) seen, 4 P(r) done,
   //         5 MMA iteration r done, 6 QK(r) data ready (lat_full observed)
   //         (softmax sub-phases) 7 S in registers, 8 vote done, 9 P slot free, 10 P stored
-  if (trace != nullptr && r < 256 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+  if (trace != nullptr && r < 256 && is_trace_cta(trace_cta))
     trace[(ev < 7 ? ev * 256 : 12032 + (ev - 7) * 256) + r] = clock64();
 }
 
@@ -214,15 +224,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* p_empty = p_full + 2;            // [2]
   uint64_t* o_done = p_empty + 2;            // [4]
   uint64_t* o_final = o_done + 4;
-  uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(o_final + 1);
+  uint64_t* sr_empty = o_final + 1;          // [2] shared rope logits slot consumed (NB > 1)
+  uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(sr_empty + 2);
 
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   griddep_launch_dependents();  // K3 (PDL) may launch; it waits for this grid before reading
-  if (p.trace != nullptr && tid == 0 && cta_lin < 1024) p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
-  // TMEM columns: S slots [0, 2*NPAD); O_{b,s} at O_COL + (b*SUB+s)*NPAD
+  if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
+    p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
+    p.trace[13824 + 2 * cta_lin] = clock64();
+  }
+  // TMEM columns: S slots [0, 2*NPAD); (NB > 1) rope-logit slots [2*NPAD, 4*NPAD);
+  // O_{b,s} at O_COL + (b*SUB+s)*NPAD
   constexpr uint32_t kTmemCols = 512;
-  const uint32_t S_COL = 0, O_COL = 2 * NPAD;
+  constexpr bool kSharedRope = NB > 1;
+  const uint32_t S_COL = 0, SR_COL = 2 * NPAD, O_COL = (kSharedRope ? 4 : 2) * NPAD;
 
   if (tid == 0) {
     for (int i = 0; i < p.lat_slots; ++i) { mbar_init(&lat_full[i], 1); mbar_init(&lat_empty[i], 1); }
@@ -233,6 +249,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int i = 0; i < 4; ++i) mbar_init(&o_done[i], 1);
     mbar_init(o_final, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&sr_empty[i], kSoftThreads);
     tmem_base_sh[1] = 0;  // debug-trace check of the final CTA barrier
     fence_barrier_init();
     tma_prefetch_desc(&lat_map);
@@ -359,142 +376,163 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
 
   if (warp == 0) {
-    // ============================================================ TMA producer
-    if (lane == 0 && R > 0) {
-      // lat_map: 3-D view {64 cols, rows, latent chunk} of the pool, so one box brings a whole
-      // DLS-wide sub-block of a T-token tile; rope_map: 2-D {64 cols, box_rows rows} view.
+    // ============================================================ TMA producer (whole warp)
+    // lat_map: 3-D view {64 cols, rows, latent chunk} of the pool, so one box brings a whole
+    // DLS-wide sub-block of a T-token tile; rope_map: 2-D {64 cols, box_rows rows} view.
+    // The page ids of the next 32/nbox tiles are fetched by the 32 lanes in one round trip
+    // (no dependent block-table load per tile), then lane 0 issues the boxes.
+    if (R > 0) {
       const uint64_t policy = l2_policy_evict_first();
       const int rope_col = NB * DLAT;
       const int nbox = T / p.box_rows;
       const int box_bytes = p.box_rows * 128;
-      int lslot = 0, lphase = 0;
+      const int tiles_per_fetch = 32 / nbox;
+      int lslot = 0, lphase = 0, my_row = 0;
       for (int t = 0; t < ntiles; ++t) {
-        int rows[T / 64];
-        for (int i = 0; i < nbox; ++i) {
-          const int tok0 = (t0 + t) * T + p.box_rows * i;
-          const int page = min(tok0 / p.page_size, n_valid_pages - 1);
-          rows[i] = p.block_table[size_t(seq) * p.max_pages + page] * p.page_size + (tok0 % p.page_size);
+        const int tf = t % tiles_per_fetch;
+        if (tf == 0) {
+          const int tt = t + lane / nbox;
+          my_row = 0;
+          if (tt < ntiles) {
+            const int tok0 = (t0 + tt) * T + p.box_rows * (lane % nbox);
+            const int page = min(tok0 / p.page_size, n_valid_pages - 1);
+            my_row = __ldg(p.block_table + size_t(seq) * p.max_pages + page) * p.page_size + (tok0 % p.page_size);
+          }
         }
+        int rows[T / 64];
+#pragma unroll
+        for (int i = 0; i < T / 64; ++i) rows[i] = __shfl_sync(0xffffffffu, my_row, tf * nbox + (i < nbox ? i : 0));
         {
           const int slot = t % p.rope_slots;
           mbar_wait(&rope_empty[slot], ((t / p.rope_slots) & 1) ^ 1);
-          mbar_arrive_expect_tx(&rope_full[slot], L::kRopeBytes);
-          for (int i = 0; i < nbox; ++i)
-            tma_load_2d_hint(&rope_map, &rope_full[slot], rope_ring + slot * L::kRopeBytes + i * box_bytes, rope_col,
-                             rows[i], policy);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&rope_full[slot], L::kRopeBytes);
+            for (int i = 0; i < nbox; ++i)
+              tma_load_2d_hint(&rope_map, &rope_full[slot], rope_ring + slot * L::kRopeBytes + i * box_bytes, rope_col,
+                               rows[i], policy);
+          }
         }
         for (int u = 0; u < NB * SUB; ++u) {
           mbar_wait(&lat_empty[lslot], lphase ^ 1);
-          mbar_arrive_expect_tx(&lat_full[lslot], L::kLatBytes);
-          uint8_t* dst = lat_ring + lslot * L::kLatBytes;
-          if (nbox == 1) {
-            // one box = [DLS/64 chunks][T rows][128 B]: exactly the chunk-major smem layout
-            tma_load_3d_hint(&lat_map, &lat_full[lslot], dst, 0, rows[0], u * (DLS / 64), policy);
-          } else {
-            // pages of 64 tokens: per chunk, per 64-row page box (2-D view)
-            for (int c = 0; c < DLS / 64; ++c)
-              for (int i = 0; i < nbox; ++i)
-                tma_load_2d_hint(&rope_map, &lat_full[lslot], dst + c * L::kChunkBytes + i * box_bytes,
-                                 u * DLS + c * 64, rows[i], policy);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&lat_full[lslot], L::kLatBytes);
+            uint8_t* dst = lat_ring + lslot * L::kLatBytes;
+            if (nbox == 1) {
+              // one box = [DLS/64 chunks][T rows][128 B]: exactly the chunk-major smem layout
+              tma_load_3d_hint(&lat_map, &lat_full[lslot], dst, 0, rows[0], u * (DLS / 64), policy);
+            } else {
+              // pages of 64 tokens: per chunk, per 64-row page box (2-D view)
+              for (int c = 0; c < DLS / 64; ++c)
+                for (int i = 0; i < nbox; ++i)
+                  tma_load_2d_hint(&rope_map, &lat_full[lslot], dst + c * L::kChunkBytes + i * box_bytes,
+                                   u * DLS + c * 64, rows[i], policy);
+            }
+            trace_event(p.trace, p.trace_cta, 0, t * NB * SUB + u);
           }
-          trace_event(p.trace, 0, t * NB * SUB + u);
+          __syncwarp();
           if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
         }
       }
     }
-    if (lane == 1 && R > 0 && p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-      // debug trace only: true arrival time of every latent unit (event 11)
-      int ls = 0, lp = 0;
-      for (int u = 0; u < R * SUB && u < 256; ++u) {
-        mbar_wait(&lat_full[ls], lp);
-        p.trace[12032 + 4 * 256 + u] = clock64();
-        if (++ls == p.lat_slots) { ls = 0; lp ^= 1; }
-      }
-    }
-  } else if (warp == 1) {
-    // ============================================================ MMA issuer (one warp, elected lane)
-    // Issue order: QK(0); then for every round r: QK(r+1), PV(r). QK(r+1) only needs the S
-    // slot freed by softmax(r-1), so it overlaps softmax(r). The whole warp runs this loop
-    // (converged, descriptors in uniform registers); elect.sync picks the issuing lane.
+  } else if (warp == 1 || warp == kPvWarp) {
+    // ============================================================ MMA issuers (one warp each, elected lane)
+    // Warp 1 issues every QK in round order; QK(r) needs its tile and the S slot freed by
+    // softmax(r-2), so it runs up to two rounds ahead of the softmax. Warp 10 issues every
+    // PV(r) as soon as P(r) is ready. Each warp runs its loop converged (descriptors in
+    // uniform registers); elect.sync picks the issuing lane. tcgen05.commit tracks the
+    // issuing thread's own MMAs: QK(r) is complete before P(r) exists, so the PV warp's
+    // commit after PV(r) is a valid release of the latent slot both used.
     if (R > 0) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(T, NPAD, false, false);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(DLS, NPAD, true, true);
-      const int kq_rope = (p.DR + 15) / 16;
       // descriptor templates (start address 0); per use: + (smem byte address >> 4)
       const uint64_t kdesc_sw128 = make_sdesc(0, 16, 1024, kSw128);              // K-major, 128B swizzle
       const uint64_t vdesc_sw128 = make_sdesc(0, L::kChunkBytes, 1024, kSw128);  // MN-major V (LBO = chunk)
       const uint64_t pdesc = make_sdesc(0, 128, L::kPSbo, kSwNone);               // MN-major P, interleaved
       const uint32_t lat_base = smem_u32(lat_ring), rope_base = smem_u32(rope_ring);
       const uint32_t q_base = smem_u32(q_smem), p_base = smem_u32(p_smem);
-      const uint32_t q_rope_addr = q_base + (NB * SUB * (DLS / 64)) * L::kQChunkBytes;
-      int qk_t = 0, qk_b = 0, qk_lslot = 0, qk_lphase = 0;
-      int pv_t = 0, pv_b = 0, pv_lslot = 0;
-      auto issue_qk = [&](int r) {
-        const int sslot = r & 1;
-        if (lane == 0) trace_event(p.trace, 12, r);
-        mbar_wait(&s_empty[sslot], ((r >> 1) & 1) ^ 1);
-        if (lane == 0) trace_event(p.trace, 13, r);
-        const int rslot = qk_t % p.rope_slots;
-        mbar_wait(&rope_full[rslot], (qk_t / p.rope_slots) & 1);
-        const uint32_t d = tbase + S_COL + sslot * NPAD;
-        uint32_t acc = 0;
-        for (int s = 0; s < SUB; ++s) {
-          mbar_wait(&lat_full[qk_lslot], qk_lphase);
-          if (lane == 0 && s == 0) trace_event(p.trace, 6, r);
-          tc_fence_after();
-          const uint64_t a0 = kdesc_sw128 + ((lat_base + qk_lslot * L::kLatBytes) >> 4);
-          const uint64_t b0 = kdesc_sw128 + ((q_base + (qk_b * SUB + s) * (DLS / 64) * L::kQChunkBytes) >> 4);
+      if (warp == 1) {
+        constexpr uint32_t idesc_qk = make_idesc_bf16(T, NPAD, false, false);
+        const int kq_rope = (p.DR + 15) / 16;
+        const uint32_t q_rope_addr = q_base + (NB * SUB * (DLS / 64)) * L::kQChunkBytes;
+        int lslot = 0, lphase = 0;
+        for (int t = 0; t < ntiles; ++t) {
+          const int rslot = t % p.rope_slots;
+          const uint64_t ra0 = kdesc_sw128 + ((rope_base + rslot * L::kRopeBytes) >> 4);
+          const uint64_t rb0 = kdesc_sw128 + (q_rope_addr >> 4);
+          if (lane == 0) trace_event(p.trace, p.trace_cta, 12, t * NB);
+          mbar_wait(&rope_full[rslot], (t / p.rope_slots) & 1);
+          if constexpr (kSharedRope) {
+            // rope logits of the tile, once for all branches
+            mbar_wait(&sr_empty[t & 1], ((t >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tbase + SR_COL + (t & 1) * NPAD;
+            for (int kk = 0; kk < kq_rope; ++kk) mma_bf16_ss_w(d, ra0 + kk * 2, rb0 + kk * 2, idesc_qk, kk > 0 ? 1u : 0u);
+            mma_commit_w(&rope_empty[rslot]);
+          }
+#pragma unroll 1
+          for (int b = 0; b < NB; ++b) {
+            const int r = t * NB + b;
+            const int sslot = r & 1;
+            mbar_wait(&s_empty[sslot], ((r >> 1) & 1) ^ 1);
+            if (lane == 0) trace_event(p.trace, p.trace_cta, 13, r);
+            const uint32_t d = tbase + S_COL + sslot * NPAD;
+            uint32_t acc = 0;
+            for (int s = 0; s < SUB; ++s) {
+              mbar_wait(&lat_full[lslot], lphase);
+              if (lane == 0 && s == 0) trace_event(p.trace, p.trace_cta, 6, r);
+              tc_fence_after();
+              const uint64_t a0 = kdesc_sw128 + ((lat_base + lslot * L::kLatBytes) >> 4);
+              const uint64_t b0 = kdesc_sw128 + ((q_base + (b * SUB + s) * (DLS / 64) * L::kQChunkBytes) >> 4);
 #pragma unroll
-          for (int c = 0; c < DLS / 64; ++c)
+              for (int c = 0; c < DLS / 64; ++c)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              mma_bf16_ss_w(d, a0 + ((c * L::kChunkBytes + kk * 32) >> 4), b0 + ((c * L::kQChunkBytes + kk * 32) >> 4),
-                            idesc_qk, acc);
-              acc = 1;
+                for (int kk = 0; kk < 4; ++kk) {
+                  mma_bf16_ss_w(d, a0 + ((c * L::kChunkBytes + kk * 32) >> 4),
+                                b0 + ((c * L::kQChunkBytes + kk * 32) >> 4), idesc_qk, acc);
+                  acc = 1;
+                }
+              if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
             }
-          if (++qk_lslot == p.lat_slots) { qk_lslot = 0; qk_lphase ^= 1; }
+            if (lane == 0) trace_event(p.trace, p.trace_cta, 1, r);
+            if constexpr (!kSharedRope) {
+              for (int kk = 0; kk < kq_rope; ++kk) mma_bf16_ss_w(d, ra0 + kk * 2, rb0 + kk * 2, idesc_qk, 1);
+              mma_commit_w(&s_full[sslot]);
+              mma_commit_w(&rope_empty[rslot]);
+            } else {
+              mma_commit_w(&s_full[sslot]);  // also covers the tile's rope logits (issued earlier)
+            }
+          }
         }
-        if (lane == 0) trace_event(p.trace, 1, r);
-        const uint64_t a0 = kdesc_sw128 + ((rope_base + rslot * L::kRopeBytes) >> 4);
-        const uint64_t b0 = kdesc_sw128 + (q_rope_addr >> 4);
-        for (int kk = 0; kk < kq_rope; ++kk) mma_bf16_ss_w(d, a0 + kk * 2, b0 + kk * 2, idesc_qk, 1);
-        mma_commit_w(&s_full[sslot]);
-        if (qk_b == NB - 1) mma_commit_w(&rope_empty[rslot]);
-        if (++qk_b == NB) { qk_b = 0; ++qk_t; }
-      };
-      auto issue_pv = [&](int r) {
-        const int pslot = r & 1;
-        mbar_wait(&p_full[pslot], (r >> 1) & 1);
-        if (lane == 0) trace_event(p.trace, 2, r);
-        tc_fence_after();
-        const uint64_t pb = pdesc + ((p_base + pslot * L::kPBytes) >> 4);
-        const uint32_t acc0 = pv_t > 0 ? 1u : 0u;
-        for (int s = 0; s < SUB; ++s) {
-          const uint64_t a0 = vdesc_sw128 + ((lat_base + pv_lslot * L::kLatBytes) >> 4);
-          const uint32_t d = tbase + O_COL + (pv_b * SUB + s) * NPAD;
+      } else {
+        constexpr uint32_t idesc_pv = make_idesc_bf16(DLS, NPAD, true, true);
+        int lslot = 0;
+        for (int t = 0; t < ntiles; ++t) {
+#pragma unroll 1
+          for (int b = 0; b < NB; ++b) {
+            const int r = t * NB + b;
+            const int pslot = r & 1;
+            mbar_wait(&p_full[pslot], (r >> 1) & 1);
+            if (lane == 0) trace_event(p.trace, p.trace_cta, 2, r);
+            tc_fence_after();
+            const uint64_t pb = pdesc + ((p_base + pslot * L::kPBytes) >> 4);
+            const uint32_t acc0 = t > 0 ? 1u : 0u;
+            for (int s = 0; s < SUB; ++s) {
+              const uint64_t a0 = vdesc_sw128 + ((lat_base + lslot * L::kLatBytes) >> 4);
+              const uint32_t d = tbase + O_COL + (b * SUB + s) * NPAD;
 #pragma unroll
-          for (int k = 0; k < T / 16; ++k) mma_bf16_ss_w(d, a0 + k * (2048 >> 4), pb + k * (256 >> 4), idesc_pv, acc0 | k);
-          mma_commit_w(&lat_empty[pv_lslot]);
-          if (++pv_lslot == p.lat_slots) pv_lslot = 0;
+              for (int k = 0; k < T / 16; ++k)
+                mma_bf16_ss_w(d, a0 + k * (2048 >> 4), pb + k * (256 >> 4), idesc_pv, acc0 | k);
+              mma_commit_w(&lat_empty[lslot]);
+              if (++lslot == p.lat_slots) lslot = 0;
+            }
+            mma_commit_w(&p_empty[pslot]);
+            mma_commit_w(&o_done[b]);
+            if (lane == 0) trace_event(p.trace, p.trace_cta, 5, r);
+          }
         }
-        mma_commit_w(&p_empty[pslot]);
-        mma_commit_w(&o_done[pv_b]);
-        if (lane == 0) trace_event(p.trace, 5, r);
-        if (++pv_b == NB) { pv_b = 0; ++pv_t; }
-      };
-      // Readiness-driven issue: PV(r) goes out as soon as P(r) is ready (it releases the
-      // latent slot, which is what keeps the TMA ring deep), QK(r+1) as soon as its tile has
-      // landed and its S slot is free; QK runs at most one round ahead of PV.
-      // Static issue order QK(0), then {QK(r+1), PV(r)}: QK(r+1) overlaps softmax(r). (A
-      // readiness-driven order -- PV as soon as P is ready -- measured 15-40% slower.)
-      issue_qk(0);
-      for (int r = 0; r < R; ++r) {
-        if (r + 1 < R) issue_qk(r + 1);
-        issue_pv(r);
+        // Single-phase barrier for the epilogue: o_done[b] may lag by two phases there, which
+        // a parity wait cannot disambiguate.
+        mma_commit_w(o_final);
       }
-      // Single-phase barrier for the epilogue: o_done[b] may lag by two phases there, which
-      // a parity wait cannot disambiguate.
-      mma_commit_w(o_final);
     }
   } else {
     // ============================================================ softmax / rescale / epilogue
@@ -528,7 +566,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const int r = t * NB + b;
         const int sslot = r & 1;
         mbar_wait(&s_full[sslot], (r >> 1) & 1);
-        if (ws == 0 && lane == 0) trace_event(p.trace, 3, r);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 3, r);
         tc_fence_after();
         float s[kHG];
         {
@@ -540,13 +578,29 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int c = 0; c < kHG; c += 16) tmem_ld16(taddr + c, raw + c);
           }
-          tmem_ld_wait();
+          if constexpr (kSharedRope) {
+            // + the tile's rope logits (complete: s_full of this round covers them)
+            uint32_t rr[kHG];
+            const uint32_t raddr = tbase + lane_off + SR_COL + (t & 1) * NPAD + h_lo;
+            if constexpr (kHG == 8) {
+              tmem_ld8(raddr, rr);
+            } else {
 #pragma unroll
-          for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]);
+              for (int c = 0; c < kHG; c += 16) tmem_ld16(raddr + c, rr + c);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]) + __uint_as_float(rr[c]);
+          } else {
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]);
+          }
         }
-        if (ws == 0 && lane == 0) trace_event(p.trace, 7, r);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 7, r);
         tc_fence_before();
         mbar_arrive(&s_empty[sslot]);
+        if (kSharedRope && b == NB - 1) mbar_arrive(&sr_empty[t & 1]);
         if ((t0 + t + 1) * T > len || !lane_ok) {  // partial tile / unused M=64 lanes
           const int tok = (t0 + t) * T + tok_in_tile;
           if (!(lane_ok && tok < len)) {
@@ -568,8 +622,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         // m_run is finite (0 before the first tile), so masked lanes stay at -inf. The first
         // tile of the split always takes the slow path (uniform: no vote needed).
-        const bool slow = (t == 0) ? true : named_bar_or(1, kSoftThreads, dmax > thr);
-        if (ws == 0 && lane == 0) trace_event(p.trace, 8, r);
+        // (per group: the groups own disjoint heads, so their rescale decisions are independent)
+        const bool slow = (t == 0) ? true : named_bar_or(3 + grp, kSoftThreads / 2, dmax > thr);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 8, r);
         bool rescale = false;
         if (slow) {
           // exact tile max per head: warp max, then across the 4 quarters through smem
@@ -584,7 +639,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             for (int c = 0; c < kHG; c += 4)
               *reinterpret_cast<float4*>(red_r + q * NPAD + c) = make_float4(wm[c], wm[c + 1], wm[c + 2], wm[c + 3]);
           }
-          named_bar_sync(1, kSoftThreads);
+          named_bar_sync(3 + grp, kSoftThreads / 2);
           if (lane < h_cnt) {
             const float m_tile =
                 fmaxf(fmaxf(red_r[lane], red_r[NPAD + lane]), fmaxf(red_r[2 * NPAD + lane], red_r[3 * NPAD + lane]));
@@ -604,7 +659,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // ---- probabilities (log2 domain; the score scale is folded into the queries)
         const int pslot = r & 1;
         if (r >= 2) mbar_wait(&p_empty[pslot], ((r >> 1) - 1) & 1);
-        if (ws == 0 && lane == 0) trace_event(p.trace, 9, r);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 9, r);
         if (lane_ok) {
           uint8_t* prow = prow0 + pslot * L::kPBytes;
 #pragma unroll
@@ -626,7 +681,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
         }
-        if (ws == 0 && lane == 0) trace_event(p.trace, 10, r);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 10, r);
         // ---- rare: the running max moved -> rescale this group's O_b columns
         if (rescale) {
           // PV(t-2, b) is complete (it was issued before QK(t, b), whose S we consumed), so
@@ -654,7 +709,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[pslot]);
-        if (ws == 0 && lane == 0) trace_event(p.trace, 4, r);
+        if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 4, r);
       }
     }
 
@@ -784,6 +839,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   __syncthreads();
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin + 1] = (long long)global_ns();
+    p.trace[13824 + 2 * cta_lin + 1] = clock64();
     p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = tmem_base_sh[1];
   }
   if (warp == 1) {

@@ -2,7 +2,7 @@
 import os, sys, torch
 sys.path.insert(0, "."); sys.path.insert(0, "tools")
 from decode_check import make_case
-trace = torch.zeros(12032 + 7 * 256, dtype=torch.int64, device="cuda")
+trace = torch.zeros(13824 + 2048, dtype=torch.int64, device="cuda")
 os.environ["MLRA_DEBUG_TRACE_PTR"] = str(trace.data_ptr())
 from paper_2603_02188_b200 import ops
 which = sys.argv[1]
