@@ -8,6 +8,23 @@
 
 namespace mlra {
 
+// Dev-only phase stamps for the small kernels (tools/small_trace.cu defines MLRA_SMALL_TRACE).
+#ifdef MLRA_SMALL_TRACE
+__device__ unsigned long long g_small_trace[4096 * 8];
+#define MLRA_STAMP(k)                                                                                   \
+  do {                                                                                                  \
+    if (threadIdx.x == 0) {                                                                             \
+      unsigned long long t_;                                                                            \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)::"memory");                                  \
+      g_small_trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (k)] = t_;   \
+    }                                                                                                   \
+  } while (0)
+#else
+#define MLRA_STAMP(k) \
+  do {                \
+  } while (0)
+#endif
+
 // ----------------------------------------------------------------------------- K0
 // attnkit/decode.py:129-150 (append_owned) + cache.py:44-57: write one token row per
 // sequence into its page. rows [B, W] bf16; positions [B] = slot index of the new token.
@@ -179,263 +196,271 @@ __global__ void merge_splits_kernel(const float* __restrict__ o_part, const floa
 }
 
 
-// acc[0..8) += x * (8 bf16 of w)
-__device__ __forceinline__ void fma8(float (&acc)[8], float x, const uint4& w) {
-  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2 f = __bfloat1622float2(w2[j]);
-    acc[2 * j] = fmaf(x, f.x, acc[2 * j]);
-    acc[2 * j + 1] = fmaf(x, f.y, acc[2 * j + 1]);
-  }
+// ----------------------------------------------------------------------------- K1 / K3 (v2)
+// Both small GEMMs of the step are "4 sequences x 128 output columns per CTA" kernels with
+// the weight tile staged in smem. 512 threads = 128 columns x 4 quarters of the
+// contraction: a thread's loop reads a conflict-free bf16 of the weight row and a
+// broadcast float4 of the 4 sequences (4 FMAs per 2 shared loads), 16 warps per SM hide
+// the shared-load latency, and the 4 quarters are added through smem at the end.
+// Spreading a head's columns x sequence groups (x branches) over 100s of CTAs keeps every
+// SM's share of the weights at 32 KB: the kernels cost about one round trip to L2/HBM.
+constexpr int kG4Seqs = 4, kG4Threads = 512, kG4Cols = 128, kG4KChunk = 128, kG4Q = kG4Threads / kG4Cols;
+
+// K1: q_abs[s, b, h, c] = scale * sum_p q_nope[s, h, p] * W^UK[h][p][b*DLAT + c]
+// (attnkit/decode.py:155-167, per branch at :224). Grid (ceil(NCOL/128), H, ceil(B/4)).
+// The W^UK tile does not depend on the previous kernel: its loads are issued before
+// griddepcontrol.wait. CTAs of column block 0 also write q_rope * scale.
+inline size_t absorb4_smem() {
+  return size_t(kG4KChunk) * kG4Cols * 2 + size_t(kG4KChunk) * kG4Seqs * 4 + size_t(kG4Q) * kG4Seqs * kG4Cols * 4;
 }
 
-// ----------------------------------------------------------------------------- K1
-// Query absorption (attnkit/decode.py:155-167, used per branch at :224):
-//   q_abs[s, b, h, c] = scale * sum_p q_nope[s, h, p] * W^UK_b[c, h, p]
-// with W^UK packed [H][DH][NB*DLAT] (column n -> branch n / DLAT, latent n % DLAT) and
-// scale = tau * log2(e) folded in for K2's log2-domain softmax; CTAs of column block 0
-// also write q_rope * scale. One CTA per (32-column block, head), 16 sequences per pass:
-// the W^UK tile [DH x 32] and the queries are staged in smem with one round trip of
-// independent 16-byte loads; thread = (sequence, 8-column octet, quarter of DH) runs
-// DH/4 x 8 FMAs and the quarters are summed with two shuffles.
-// Triggers the dependent launch at entry so K2 (PDL) can start streaming the cache.
-constexpr int kAbsCols = 32, kAbsThreads = 256, kAbsSeqs = 16;
-__global__ void __launch_bounds__(kAbsThreads)
-absorb_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __restrict__ w_uk,
-              __nv_bfloat16* __restrict__ q_abs, int B, int H, int DH, int NB, int DLAT, float scale,
-              const __nv_bfloat16* __restrict__ rope_in, __nv_bfloat16* __restrict__ rope_out, int DR) {
+__global__ void __launch_bounds__(kG4Threads)
+absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __restrict__ w_uk,
+               __nv_bfloat16* __restrict__ q_abs, int B, int H, int DH, int NB, int DLAT, float scale,
+               const __nv_bfloat16* __restrict__ rope_in, __nv_bfloat16* __restrict__ rope_out, int DR,
+               int* __restrict__ zero, int nzero) {
   griddep_launch_dependents();
-  griddep_wait();  // q_nope comes from the previous kernel on the stream
-  extern __shared__ __align__(16) uint4 abs_smem[];
-  uint4* ws = abs_smem;            // [DH][4]: W^UK[h][p][c0 .. c0+32)
-  uint4* xs = abs_smem + DH * 4;   // [kAbsSeqs][DH/8]: q_nope rows of this pass
+  extern __shared__ __align__(16) uint8_t g4_smem[];
+  if (zero != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    for (int i = threadIdx.x; i < nzero; i += kG4Threads) zero[i] = 0;  // the step's K2 completion counters
+  __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(g4_smem);                      // [KC][128]
+  float4* xs = reinterpret_cast<float4*>(g4_smem + size_t(kG4KChunk) * kG4Cols * 2);  // [KC] x 4 seqs
+  float* red = reinterpret_cast<float*>(xs + kG4KChunk);                              // [Q][4][128]
   const int NCOL = NB * DLAT;
-  const int h = blockIdx.y, c0 = blockIdx.x * kAbsCols, tid = threadIdx.x;
-  const int o = tid & 3, qk = (tid >> 2) & 3, sl = tid >> 4;
-  const int col = c0 + o * 8;
-  for (int i = tid; i < DH * 4; i += kAbsThreads) {
-    const int k = i >> 2, oo = i & 3;
-    ws[i] = (c0 + oo * 8 < NCOL) ? __ldg(reinterpret_cast<const uint4*>(w_uk + (size_t(h) * DH + k) * NCOL + c0 + oo * 8))
-                                  : make_uint4(0, 0, 0, 0);
+  const int c0 = blockIdx.x * kG4Cols, h = blockIdx.y, s0 = blockIdx.z * kG4Seqs, tid = threadIdx.x;
+  const int ncols = min(kG4Cols, NCOL - c0);
+  const int oct = ncols / 8;  // 16-byte chunks per weight row (NCOL % 8 == 0, host-checked)
+  const int col = tid % kG4Cols, kq = tid / kG4Cols;
+  MLRA_STAMP(0);
+  float acc[kG4Seqs] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < DH; k0 += kG4KChunk) {
+    const int kc = min(kG4KChunk, DH - k0);
+    if (k0 > 0) __syncthreads();
+    {
+      // weight tile: kc rows x ncols in 16-byte chunks, and this thread's query element;
+      // every load is in flight before the first store
+      constexpr int kPer = kG4KChunk * kG4Cols / 8 / kG4Threads;  // 4
+      uint4 v[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int i = tid + j * kG4Threads;
+        const int r = i / (kG4Cols / 8), c8 = i % (kG4Cols / 8);
+        v[j] = (r < kc && c8 < oct) ? __ldg(reinterpret_cast<const uint4*>(w_uk + (size_t(h) * DH + k0 + r) * NCOL + c0) + c8)
+                                   : make_uint4(0, 0, 0, 0);
+      }
+      if (k0 == 0) griddep_wait();  // q_nope comes from the previous kernel on the stream
+      // x: thread (row r = tid / 4, sequence tid % 4)
+      const int xr = tid / kG4Seqs, xsq = tid % kG4Seqs;
+      float xv = 0.f;
+      if (xr < kc && s0 + xsq < B) xv = __bfloat162float(q_nope[(size_t(s0 + xsq) * H + h) * DH + k0 + xr]);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) reinterpret_cast<uint4*>(ws)[tid + j * kG4Threads] = v[j];
+      if (xr < kG4KChunk) reinterpret_cast<float*>(xs)[tid] = xv;
+    }
+    __syncthreads();
+    MLRA_STAMP(1);
+    const int q_len = (kc + kG4Q - 1) / kG4Q, r0 = kq * q_len, r1 = min(kc, r0 + q_len);
+    const __nv_bfloat16* wc = ws + col;
+#pragma unroll 8
+    for (int r = r0; r < r1; ++r) {
+      const float w = __bfloat162float(wc[r * kG4Cols]);
+      const float4 x = xs[r];
+      acc[0] = fmaf(x.x, w, acc[0]);
+      acc[1] = fmaf(x.y, w, acc[1]);
+      acc[2] = fmaf(x.z, w, acc[2]);
+      acc[3] = fmaf(x.w, w, acc[3]);
+    }
+  }
+  MLRA_STAMP(2);
+  if (kq > 0) {
+#pragma unroll
+    for (int s = 0; s < kG4Seqs; ++s) red[((kq - 1) * kG4Seqs + s) * kG4Cols + col] = acc[s];
+  }
+  __syncthreads();
+  if (kq == 0 && col < ncols) {
+    const int cc = c0 + col, b = cc / DLAT, c = cc % DLAT;
+#pragma unroll
+    for (int s = 0; s < kG4Seqs; ++s) {
+      float v = acc[s];
+#pragma unroll
+      for (int q = 1; q < kG4Q; ++q) v += red[((q - 1) * kG4Seqs + s) * kG4Cols + col];
+      if (s0 + s < B) q_abs[((size_t(s0 + s) * NB + b) * H + h) * DLAT + c] = __float2bfloat16(v * scale);
+    }
   }
   if (blockIdx.x == 0 && rope_out != nullptr) {
-    for (int i = tid; i < B * DR; i += kAbsThreads) {
-      const size_t off = (size_t(i / DR) * H + h) * DR + i % DR;
-      rope_out[off] = __float2bfloat16(__bfloat162float(rope_in[off]) * scale);
-    }
-  }
-  const int xw = DH / 8, kq = xw / 4;  // 16-byte words per row, per quarter (DH % 32 == 0)
-  for (int s0 = 0; s0 < B; s0 += kAbsSeqs) {
-    const int ns = min(kAbsSeqs, B - s0);
-    if (s0 > 0) __syncthreads();
-    for (int i = tid; i < ns * xw; i += kAbsThreads)
-      xs[i] = __ldg(reinterpret_cast<const uint4*>(q_nope + (size_t(s0 + i / xw) * H + h) * DH) + i % xw);
-    __syncthreads();
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (sl < ns) {
-      const uint4* xr = xs + sl * xw + qk * kq;
-      const uint4* wq = ws + qk * kq * 8 * 4;
-      for (int k8 = 0; k8 < kq; ++k8) {
-        const uint4 xv = xr[k8];
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xv);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 xf = __bfloat1622float2(x2[j]);
-          fma8(acc, xf.x, wq[(k8 * 8 + 2 * j) * 4 + o]);
-          fma8(acc, xf.y, wq[(k8 * 8 + 2 * j + 1) * 4 + o]);
-        }
+    for (int i = tid; i < kG4Seqs * DR; i += kG4Threads) {
+      const int s = s0 + i / DR;
+      if (s < B) {
+        const size_t off = (size_t(s) * H + h) * DR + i % DR;
+        rope_out[off] = __float2bfloat16(__bfloat162float(rope_in[off]) * scale);
       }
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 4);
-      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
-    }
-    if (qk == 0 && sl < ns && col < NCOL) {
-      const int b = col / DLAT, cc = col % DLAT;
-      uint4 v;
-      v.x = pack_bf16(acc[0] * scale, acc[1] * scale);
-      v.y = pack_bf16(acc[2] * scale, acc[3] * scale);
-      v.z = pack_bf16(acc[4] * scale, acc[5] * scale);
-      v.w = pack_bf16(acc[6] * scale, acc[7] * scale);
-      *reinterpret_cast<uint4*>(q_abs + ((size_t(s0 + sl) * NB + b) * H + h) * DLAT + cc) = v;
-    }
   }
+  MLRA_STAMP(3);
 }
 
-inline size_t absorb_smem(int DH) { return size_t(DH) * 4 * 16 + size_t(kAbsSeqs) * (DH / 8) * 16; }
-
-// ----------------------------------------------------------------------------- K3
-// Split merge + value up-projection in one kernel (attnkit/decode.py:228 per branch, then
-// reduce_contributions :264-285 summing the branches in ascending order):
-//   w_k = 2^(lse_k - max) / sum_j 2^(lse_j - max)         (per sequence, branch, head)
-//   Z_b = sum_k w_k O_k                                      (merged latent, fp32)
-//   out[s, h, :] = alpha * sum_b Z_b . W^UV_b[h]            (per_branch = 0)
-//   out[s, b, h, :] = alpha * Z_b . W^UV_b[h]               (per_branch = 1)
-// One CTA per (head, 4 sequences). W^UV[h] ([NB*DLAT][DH] bf16, <= 128 KB) does not depend
-// on K2, so its bulk copy into smem is issued before griddepcontrol.wait; then the split
-// weights and merged latents (smem), then thread (sequence, 4-column quad of d, half of the
-// latent rows) accumulates per branch and the two halves are added through smem.
-constexpr int kCmbSeqs = 4, kCmbThreads = 256;
-// smem: W^UV [NCOL][DH] bf16 | Z [4][NCOL] | weights [4][NB][nsplit] | red [4][4][DH] | mbarriers
-//       | (staged = 1) partials [4][nsplit][NB][DLAT] fp32
-inline size_t combine_smem(int NB, int DLAT, int DH, int nsplit, int staged) {
-  const size_t w = size_t(NB) * DLAT * DH * 2;
-  const size_t z = size_t(kCmbSeqs) * NB * DLAT * 4;
-  const size_t wt = size_t(kCmbSeqs) * NB * nsplit * 4;
-  const size_t red = size_t(kCmbSeqs) * 4 * DH * 4;
-  const size_t parts = staged ? size_t(kCmbSeqs) * nsplit * NB * DLAT * 4 : 0;
-  return ((w + z + wt + red + 15) / 16) * 16 + 16 + parts;
+// K3: split merge + W^UV up-projection + ascending branch sum + alpha
+// (attnkit/decode.py:228 per branch, then reduce_contributions :264-285).
+// Grid (ceil(B/SEQS), H, NB), SEQS in {4, 8} sequences per CTA (8 when 4 would need more
+// than one wave); with NB > 1 and a summed output the NB CTAs of a (sequence group, head)
+// form a cluster: each up-projects its branch, rank 0 adds the NB results through
+// distributed shared memory in ascending branch order (deterministic, the reference's
+// order) and writes the head. Per CTA:
+//   W^UV_b[h]  [DLAT][DH] bf16 bulk-copied into smem before griddepcontrol.wait (PDL);
+//   w_k  = 2^(lse_k - max) / sum_j 2^(lse_j - max)  per (sequence, split);
+//   Z[c] = sum_k w_k O_k[c], thread = (latent c, sequence), all split loads in flight;
+//   y[d] = alpha * sum_c Z[c] W[c][d], thread = (column d, quarter of c), quarters added in smem.
+template <int SEQS>
+inline size_t combine4_smem(int DLAT, int DH, int nsplit) {
+  return ((size_t(DLAT) * DH * 2 + 15) / 16) * 16 + size_t(DLAT) * SEQS * 4 + size_t(kG4Q) * SEQS * DH * 4 + 16;
 }
 
-__global__ void __launch_bounds__(kCmbThreads)
-combine_upproj_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
-                      const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT,
-                      int DH, int nsplit, float alpha, int per_branch, int staged) {
-  extern __shared__ __align__(128) uint8_t cmb_smem[];
-  const int NCOL = NB * DLAT;
-  const __nv_bfloat16* wsm = reinterpret_cast<const __nv_bfloat16*>(cmb_smem);      // [NCOL][DH]
-  float* zs = reinterpret_cast<float*>(cmb_smem + size_t(NCOL) * DH * 2);          // [kCmbSeqs][NCOL]
-  float* wts = zs + kCmbSeqs * NCOL;                                               // [kCmbSeqs][NB][nsplit]
-  float* red = wts + kCmbSeqs * NB * nsplit;                                       // [kCmbSeqs][4][DH]
-  const size_t head_bytes =
-      ((size_t(NCOL) * DH * 2 + (kCmbSeqs * NCOL + kCmbSeqs * NB * nsplit + kCmbSeqs * 4 * DH) * 4 + 15) / 16) * 16;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(cmb_smem + head_bytes);  // [0] W^UV, [1] partials
-  float* parts = reinterpret_cast<float*>(cmb_smem + head_bytes + 16);  // [4][nsplit][NB][DLAT]
-  const int h = blockIdx.x, s0 = blockIdx.y * kCmbSeqs, tid = threadIdx.x;
-  const int ns = min(kCmbSeqs, B - s0);
+constexpr int kMergeChunk = 12;  // split loads in flight per thread (B = 16 -> 9 splits: one pass)
+
+template <int SEQS>
+__global__ void __launch_bounds__(kG4Threads, 2)
+combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
+                const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
+                int nsplit, float alpha, int per_branch, const int* __restrict__ done, int target) {
+  static_assert(SEQS == 4 || SEQS == 8, "4 or 8 sequences per CTA");
+  extern __shared__ __align__(128) uint8_t c4_smem[];
+  const size_t wbytes = size_t(DLAT) * DH * 2;
+  const __nv_bfloat16* wsm = reinterpret_cast<const __nv_bfloat16*>(c4_smem);  // [DLAT][DH]
+  float* zs = reinterpret_cast<float*>(c4_smem + ((wbytes + 15) / 16) * 16);    // [DLAT][SEQS]
+  float* ys = zs + DLAT * SEQS;                                                 // [Q][SEQS][DH]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ys + kG4Q * SEQS * DH);
+  const int s0 = blockIdx.x * SEQS, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
+  MLRA_STAMP(0);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(bar, 1);
     fence_barrier_init();
   }
   __syncthreads();
-  const uint32_t wbytes = uint32_t(NCOL) * DH * 2;
   if (tid == 0) {
-    mbar_arrive_expect_tx(&bar[0], wbytes);
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(w_uv + size_t(h) * NCOL * DH);
-    for (uint32_t off = 0; off < wbytes; off += 65536)
-      bulk_copy_g2s(cmb_smem + off, src + off, min(65536u, wbytes - off), &bar[0]);
+    mbar_arrive_expect_tx(bar, uint32_t(wbytes));
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(w_uv + (size_t(h) * NB + b) * DLAT * DH);
+    for (size_t off = 0; off < wbytes; off += 32768)
+      bulk_copy_g2s(c4_smem + off, src + off, uint32_t(wbytes - off < 32768 ? wbytes - off : 32768), bar);
   }
-  griddep_wait();  // partials of K2
-  if (staged && tid < 32) {
-    // every (sequence, split, branch) row of this head: DLAT contiguous floats
-    const int nrows = ns * nsplit * NB;
-    if (tid == 0) mbar_arrive_expect_tx(&bar[1], uint32_t(nrows) * DLAT * 4);
-    __syncwarp();
-    for (int i = tid; i < nrows; i += 32) {
-      const int s = i / (nsplit * NB), kb = i % (nsplit * NB);  // kb = k * NB + b
-      bulk_copy_g2s(parts + size_t(i) * DLAT, o_part + ((size_t(s0 + s) * nsplit * NB + kb) * H + h) * DLAT,
-                    uint32_t(DLAT) * 4, &bar[1]);
-    }
-  }
-  // split weights, one thread per (sequence, branch)
-  for (int i = tid; i < ns * NB; i += kCmbThreads) {
-    const int s = i / NB, b = i % NB;
-    const float* l = lse_part + (size_t(s0 + s) * nsplit * NB + b) * H + h;  // split stride NB*H
-    float m = -INFINITY;
-    for (int k = 0; k < nsplit; ++k) m = fmaxf(m, l[size_t(k) * NB * H]);
-    float tot = 0.f;
-    float* wr = wts + i * nsplit;
-    for (int k = 0; k < nsplit; ++k) {
-      const float lk = l[size_t(k) * NB * H];
-      const float w = (m == -INFINITY || lk == -INFINITY) ? 0.f : ex2(lk - m);
-      wr[k] = w;
-      tot += w;
-    }
-    const float inv = tot > 0.f ? 1.f / tot : 0.f;
-    for (int k = 0; k < nsplit; ++k) wr[k] *= inv;
-  }
-  __syncthreads();
-  // merged latents
-  if (staged) {
-    mbar_wait(&bar[1], 0);
-    for (int i = tid; i < ns * NCOL; i += kCmbThreads) {
-      const int s = i / NCOL, col = i % NCOL, b = col / DLAT, c = col % DLAT;
-      const float* wr = wts + (s * NB + b) * nsplit;
-      const float* pr = parts + (size_t(s) * nsplit * NB + b) * DLAT + c;
-      float acc = 0.f;
-      for (int k = 0; k < nsplit; ++k) acc = fmaf(wr[k], pr[size_t(k) * NB * DLAT], acc);
-      zs[i] = acc;
-    }
-  }
-  const size_t kstride = size_t(NB) * H * DLAT;
-  for (int i = staged ? ns * NCOL : tid; i < ns * NCOL; i += kCmbThreads) {
-    const int s = i / NCOL, col = i % NCOL, b = col / DLAT, c = col % DLAT;
-    const float* o = o_part + ((size_t(s0 + s) * nsplit * NB + b) * H + h) * DLAT + c;
-    const float* wr = wts + (s * NB + b) * nsplit;
-    // up to 16 split loads in flight per pass (independent addresses, one round trip)
-    float acc = 0.f;
-    for (int k0 = 0; k0 < nsplit; k0 += 16) {
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = (k0 + j < nsplit) ? __ldcg(o + size_t(k0 + j) * kstride) : 0.f;
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (k0 + j < nsplit) acc = fmaf(wr[k0 + j], v[j], acc);
-    }
-    zs[i] = acc;
-  }
-  __syncthreads();
-  mbar_wait(&bar[0], 0);
-  // up-projection: thread = (half of the latent rows, sequence, quad of d); 2 * 4 * DH/4 <= 256
-  // items for DH <= 128 (host-checked), so one uniform pass around the __syncthreads below
-  const int nq = DH / 4;
-  {
-    const int item = tid;
-    const bool valid = item < 2 * kCmbSeqs * nq;
-    const int half = valid ? item / (kCmbSeqs * nq) : 2, s = (item / nq) % kCmbSeqs, dq = item % nq;
-    float acc[4][4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[b][j] = 0.f;
-    if (valid && s < ns) {
-      const int rows = (DLAT + 1) / 2;
-      const int r0 = half * rows, r1 = min(DLAT, r0 + rows);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (b >= NB) break;
-        const float* z = zs + s * NCOL + b * DLAT;
-        const __nv_bfloat16* wb = wsm + size_t(b) * DLAT * DH + dq * 4;
-#pragma unroll 4
-        for (int r = r0; r < r1; ++r) {
-          const float zv = z[r];
-          const uint2 wv = *reinterpret_cast<const uint2*>(wb + size_t(r) * DH);
-          const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.x));
-          const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.y));
-          acc[b][0] = fmaf(zv, w01.x, acc[b][0]);
-          acc[b][1] = fmaf(zv, w01.y, acc[b][1]);
-          acc[b][2] = fmaf(zv, w23.x, acc[b][2]);
-          acc[b][3] = fmaf(zv, w23.y, acc[b][3]);
-        }
-      }
-    }
-    if (half == 1) {
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (b < NB) *reinterpret_cast<float4*>(red + (s * 4 + b) * DH + dq * 4) = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
+  if (done == nullptr) {
+    griddep_wait();  // partials of K2 (the whole grid)
+  } else {
+    // only this CTA's sequences: every K2 CTA of sequence s adds 1 to done[s] once its
+    // partials are globally visible (fence + atomic); acquire loads pair with it
+    if (tid < SEQS && s0 + tid < B) {
+      const int* f = done + s0 + tid;
+      while (ld_acquire_gpu(f) < target) __nanosleep(128);
     }
     __syncthreads();
-    if (half == 0 && s < ns) {
-      float tot[4] = {0.f, 0.f, 0.f, 0.f};
+  }
+  MLRA_STAMP(1);
+  const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
+  // merge: thread = (latent column c, sequence); the split weights are computed by every
+  // thread of a sequence redundantly (L2-resident lse loads) -- no extra barrier
+  for (int i = tid; i < DLAT * SEQS; i += kG4Threads) {
+    const int c = i / SEQS, sq = i % SEQS, s = s0 + sq;
+    float z = 0.f;
+    if (s < B) {
+      const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
+      const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
+      float m = -INFINITY, tot = 0.f;
+      for (int k0 = 0; k0 < nsplit; k0 += kMergeChunk) {
+        float lk[kMergeChunk], v[kMergeChunk];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (b >= NB) break;
-        const float4 o1 = *reinterpret_cast<const float4*>(red + (s * 4 + b) * DH + dq * 4);
-        const float v0 = (acc[b][0] + o1.x) * alpha, v1 = (acc[b][1] + o1.y) * alpha;
-        const float v2 = (acc[b][2] + o1.z) * alpha, v3 = (acc[b][3] + o1.w) * alpha;
-        if (per_branch) {
-          *reinterpret_cast<float4*>(out + ((size_t(s0 + s) * NB + b) * H + h) * DH + dq * 4) = make_float4(v0, v1, v2, v3);
-        } else {
-          tot[0] += v0; tot[1] += v1; tot[2] += v2; tot[3] += v3;
+        for (int j = 0; j < kMergeChunk; ++j) {
+          const int k = min(k0 + j, nsplit - 1);
+          lk[j] = __ldcg(l + size_t(k) * NB * H);
+          v[j] = __ldcg(o + size_t(k) * kstride);
+        }
+        // online rescale across chunks of splits (one chunk for nsplit <= kMergeChunk)
+        float mc = m;
+#pragma unroll
+        for (int j = 0; j < kMergeChunk; ++j) mc = (k0 + j < nsplit) ? fmaxf(mc, lk[j]) : mc;
+        if (mc != -INFINITY) {
+          const float a = (m == -INFINITY) ? 0.f : ex2(m - mc);
+          z *= a;
+          tot *= a;
+#pragma unroll
+          for (int j = 0; j < kMergeChunk; ++j) {
+            const float w = (k0 + j >= nsplit || lk[j] == -INFINITY) ? 0.f : ex2(lk[j] - mc);
+            tot += w;
+            z = fmaf(w, v[j], z);
+          }
+          m = mc;
         }
       }
-      if (!per_branch)
-        *reinterpret_cast<float4*>(out + (size_t(s0 + s) * H + h) * DH + dq * 4) = make_float4(tot[0], tot[1], tot[2], tot[3]);
+      z = tot > 0.f ? z / tot : 0.f;
+    }
+    zs[i] = z;
+  }
+  __syncthreads();
+  MLRA_STAMP(2);
+  mbar_wait(bar, 0);
+  MLRA_STAMP(3);
+  const bool cluster_sum = NB > 1 && !per_branch;
+  const int cq = tid / kG4Cols;
+  const int q_len = (DLAT + kG4Q - 1) / kG4Q, cr0 = cq * q_len, cr1 = min(DLAT, cr0 + q_len);
+  for (int d0 = 0; d0 < DH; d0 += kG4Cols) {
+    const int d = d0 + tid % kG4Cols;
+    float acc[SEQS];
+#pragma unroll
+    for (int s = 0; s < SEQS; ++s) acc[s] = 0.f;
+    if (d < DH) {
+      const __nv_bfloat16* wc = wsm + d;
+#pragma unroll 4
+      for (int c = cr0; c < cr1; ++c) {
+        const float w = __bfloat162float(wc[size_t(c) * DH]);
+#pragma unroll
+        for (int s4 = 0; s4 < SEQS; s4 += 4) {
+          const float4 z = *reinterpret_cast<const float4*>(zs + c * SEQS + s4);
+          acc[s4 + 0] = fmaf(z.x, w, acc[s4 + 0]);
+          acc[s4 + 1] = fmaf(z.y, w, acc[s4 + 1]);
+          acc[s4 + 2] = fmaf(z.z, w, acc[s4 + 2]);
+          acc[s4 + 3] = fmaf(z.w, w, acc[s4 + 3]);
+        }
+      }
+    }
+    if (d0 > 0) __syncthreads();
+    if (d < DH) {
+#pragma unroll
+      for (int s = 0; s < SEQS; ++s) ys[(cq * SEQS + s) * DH + d] = acc[s];
     }
   }
+  __syncthreads();
+  // quarters -> ys[0] (scaled); thread = (sequence, column)
+  for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+    float v = ys[i];
+#pragma unroll
+    for (int q = 1; q < kG4Q; ++q) v += ys[q * SEQS * DH + i];
+    ys[i] = v * alpha;
+  }
+  MLRA_STAMP(4);
+  if (!cluster_sum) {
+    __syncthreads();
+    for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+      const int s = s0 + i / DH, d = i % DH;
+      if (s >= B) continue;
+      if (per_branch) out[((size_t(s) * NB + b) * H + h) * DH + d] = ys[i];
+      else out[(size_t(s) * H + h) * DH + d] = ys[i];
+    }
+  } else {
+    // branch sum over the cluster (ranks = branches along z), ascending order
+    cluster_arrive_release();
+    cluster_wait_acquire();
+    if (b == 0) {
+      const uint32_t ys_addr = smem_u32(ys);
+      for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+        const int s = s0 + i / DH, d = i % DH;
+        float tot = ys[i];
+        for (int r = 1; r < NB; ++r) tot += ld_shared_cluster_f32(mapa_shared(ys_addr + i * 4, r));
+        if (s < B) out[(size_t(s) * H + h) * DH + d] = tot;
+      }
+    }
+    // keep every rank's smem alive until rank 0 has read it
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
+  MLRA_STAMP(5);
 }
 
 }  // namespace mlra

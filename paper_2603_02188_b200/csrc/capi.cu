@@ -111,13 +111,11 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
   cfg.blockDim = dim3(mlra::kNumThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;  // fused mode spins on per-sequence barriers
-  attr[0].val.cooperative = p.fused ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = (p.pdl && !p.fused) ? 1 : 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, kern, lat_map, rope_map, p) != cudaSuccess)
     return cuda_check("mlra_decode_kernel launch");
   return cuda_check("mlra_decode_kernel launch");
@@ -162,8 +160,9 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_
   return cuda_check("cache_append launch");
 }
 
-int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
-                      int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
+// K1; `zero` (nullable) = nzero per-sequence completion counters of the step to reset.
+static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
+                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream, int* zero, int nzero) {
   if (B <= 0) return MLRA_OK;
   if (H <= 0 || DH <= 0 || NB <= 0 || DLAT <= 0 || DLAT % 2 != 0 || DR < 0)
     return fail(MLRA_ERR_SHAPE, "absorb_query: bad dims H=%d DH=%d NB=%d DLAT=%d DR=%d", H, DH, NB, DLAT, DR);
@@ -183,27 +182,35 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
                                                 static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
                                                 score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
                                                 DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
+    if (zero != nullptr && cudaMemsetAsync(zero, 0, size_t(nzero) * sizeof(int), st) != cudaSuccess)
+      return cuda_check("absorb_query counter reset");
     return cuda_check("absorb_query launch");
   }
-  const size_t smem = mlra::absorb_smem(DH);
-  static unsigned attr_done = 0;
-  if (int rc = set_smem_once(mlra::absorb_kernel, attr_done, int(mlra::absorb_smem(1024)))) return rc;
+  if ((reinterpret_cast<uintptr_t>(w_uk) & 15) != 0)
+    return fail(MLRA_ERR_CONFIG, "absorb_query: w_uk must be 16-byte aligned");
+  // CTA = (128 latent columns, head, 4 sequences): W^UK tile staged in smem, one column per thread
+  const size_t smem = mlra::absorb4_smem();
   const int NCOL = NB * DLAT;
-  dim3 grid((NCOL + mlra::kAbsCols - 1) / mlra::kAbsCols, H);
-  if (launch_ex(mlra::absorb_kernel, grid, dim3(mlra::kAbsThreads), smem, st, false,
+  dim3 grid((NCOL + mlra::kG4Cols - 1) / mlra::kG4Cols, H, (B + mlra::kG4Seqs - 1) / mlra::kG4Seqs);
+  if (launch_ex(mlra::absorb4_kernel, grid, dim3(mlra::kG4Threads), smem, st, false,
                 static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(w_uk),
                 static_cast<__nv_bfloat16*>(q_abs), B, H, DH, NB, DLAT, score_scale,
                 static_cast<const __nv_bfloat16*>(q_rope), DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr,
-                DR) != cudaSuccess)
+                DR, zero, nzero) != cudaSuccess)
     return cuda_check("absorb_query launch");
   return cuda_check("absorb_query launch");
+}
+
+int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
+                      int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
+  return absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_out, B, H, DH, NB, DLAT, DR, score_scale, stream, nullptr, 0);
 }
 
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
          al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4) +
-         al(size_t(B) * NB * H * DLAT * 4) + al(size_t(B) * ((H + 15) / 16) * 4 * sizeof(int));
+         al(size_t(B) * NB * H * DLAT * 4) + al(size_t(B) * sizeof(int));
 }
 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
@@ -218,33 +225,22 @@ int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
   return s < 1 ? 1 : s;
 }
 
-struct FusedArgs {
-  const void* q_nope;
-  const void* q_rope_in;
-  const void* w_uk;
-  const void* w_uv;
-  float* out;
-  int* sync;
-  int DH;
-  float score_scale, alpha;
-};
-
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       const FusedArgs* fa, bool pdl = false);
+                       int* done, bool pdl = false);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
                          int DLS, int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream) {
   return decode_impl(q_abs, q_rope, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
-                     max_pages, num_pages, nsplit, stream, nullptr);
+                     max_pages, num_pages, nsplit, stream, nullptr, false);
 }
 
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       const FusedArgs* fa, bool pdl) {
+                       int* done, bool pdl) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -318,18 +314,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
   p.pdl = pdl ? 1 : 0;
-  if (fa != nullptr) {
-    p.fused = 1;
-    p.q_nope = static_cast<const __nv_bfloat16*>(fa->q_nope);
-    p.q_rope_in = static_cast<const __nv_bfloat16*>(fa->q_rope_in);
-    p.w_uk = static_cast<const __nv_bfloat16*>(fa->w_uk);
-    p.w_uv = static_cast<const __nv_bfloat16*>(fa->w_uv);
-    p.out = fa->out;
-    p.sync = fa->sync;
-    p.DH = fa->DH;
-    p.score_scale = fa->score_scale;
-    p.alpha = fa->alpha;
-  }
+  p.done = done;
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
   if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
@@ -364,24 +349,47 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
 // K3 needs a [B, H, NB*DLAT] fp32 scratch for the merged latent when it up-projects; the
 // standalone entry point allocates it from a per-thread cache (mlra_decode_step passes the
 // workspace slice instead).
+// K3. With `done` (mlra_decode_step) each CTA waits for the completion counters of its own
+// sequences (target = K2 CTAs per sequence) instead of for the whole K2 grid.
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
                         int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                        bool pdl = false) {
+                        bool pdl = false, const int* done = nullptr, int target = 0) {
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
-  // partials staged in smem by bulk copies when they fit next to W^UV (the common case)
-  const int staged = (mlra::combine_smem(NB, DLAT, DH, nsplit, 1) <= size_t(kSmemBudget) && (DLAT * 4) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(o_part) & 15) == 0) ? 1 : 0;
-  const size_t csmem = mlra::combine_smem(NB, DLAT, DH, nsplit, staged);
-  if (upproj != 0 && DH % 4 == 0 && DH <= 128 && NB <= 4 && csmem <= size_t(kSmemBudget) &&
-      (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0 && (size_t(NB) * DLAT * DH * 2) % 16 == 0) {
-    // one kernel: merge + up-projection, W^UV staged by bulk copy (common case)
-    static unsigned attr_done = 0;
-    if (int rc = set_smem_once(mlra::combine_upproj_kernel, attr_done, kSmemBudget)) return rc;
-    dim3 grid(H, (B + mlra::kCmbSeqs - 1) / mlra::kCmbSeqs);
-    if (launch_ex(mlra::combine_upproj_kernel, grid, dim3(mlra::kCmbThreads), csmem, st, pdl, o_part, lse_part,
-                  static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT, DH, nsplit, alpha,
-                  upproj == 2 ? 1 : 0, staged) != cudaSuccess)
+  // sequences per CTA: 4, or 8 when 4 would need more than one wave (2 CTAs per SM)
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool seq8 = long((B + 3) / 4) * H * NB > 2L * sms;
+  const size_t c4smem = seq8 ? mlra::combine4_smem<8>(DLAT, DH, nsplit) : mlra::combine4_smem<4>(DLAT, DH, nsplit);
+  if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
+    // CTA = (4 or 8 sequences, head, branch); with a summed output the NB branch CTAs of a
+    // (sequence group, head) form a cluster and add their results through DSMEM.
+    auto kern = seq8 ? mlra::combine4_kernel<8> : mlra::combine4_kernel<4>;
+    static unsigned attr_done4 = 0, attr_done8 = 0;
+    if (int rc = set_smem_once(kern, seq8 ? attr_done8 : attr_done4, kSmemBudget)) return rc;
+    const int per_branch = upproj == 2 ? 1 : 0;
+    const int seqs = seq8 ? 8 : 4;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
+    cfg.blockDim = dim3(mlra::kG4Threads);
+    cfg.dynamicSmemBytes = c4smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = (NB > 1 && !per_branch) ? NB : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
+                           DH, nsplit, alpha, per_branch, done, target) != cudaSuccess)
       return cuda_check("combine launch");
     return cuda_check("combine launch");
   }
@@ -440,35 +448,24 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   ws += al(size_t(B) * nsplit * NB * H * 4);
   float* zbuf = reinterpret_cast<float*>(ws);
   ws += al(size_t(B) * NB * H * DLAT * 4);
-  int* sync = reinterpret_cast<int*>(ws);
-  // Fused single-kernel step when every split of every (sequence, head group) can be
-  // co-resident (1 CTA per SM): K1 and K3 run inside K2 around two per-sequence barriers.
+  int* done = reinterpret_cast<int*>(ws);  // [B] per-sequence K2 completion counters
+  // K2 CTAs per sequence (every head group counts)
   const int npad = pick_npad(H, NB, SUB);
   const int hgroups = (H + npad - 1) / npad;
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // The fused single-kernel step (K1/K3 folded into K2 behind grid/sequence barriers) is
-  // opt-in: it measured slower than K1 -> K2 -> K3 for MLRA-4 (cross-CTA barriers cost 2-4 us
-  // each on B200 and its W^UV pass is latency-bound), see profiles/ROUND1.md.
-  const bool fused_ok = getenv("MLRA_FUSED") != nullptr && (DH % 8) == 0 && DH <= 128 && NB * DLAT <= 512 &&
-                        nsplit <= 64 && long(B) * nsplit * hgroups <= sms;
-  if (fused_ok) {
-    FusedArgs fa{q_nope, q_rope, w_uk, w_uv, out, sync, DH, score_scale, alpha};
-    return decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
-                       page_size, max_pages, num_pages, nsplit, stream, &fa);
-  }
-  int rc = mlra_absorb_query(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
-  if (rc) return rc;
-  // K2 and K3 are chained with programmatic dependent launch: K2's TMA producer streams the
-  // cache while K1 drains (the cache was written before K1 started), K3 bulk-loads W^UV while
-  // K2 drains; both wait on their predecessor before touching its output.
+  // K1 resets the counters; K2 and K3 are chained with programmatic dependent launch: K2's
+  // TMA producer streams the cache while K1 drains (the cache was written before K1 started)
+  // and waits on K1 only before reading the queries; K3's CTAs load W^UV as soon as they are
+  // resident and then wait only for the K2 CTAs of their own sequences (the counters), so
+  // the merge of early-finishing sequences overlaps K2's tail.
   const bool pdl = getenv("MLRA_NO_PDL") == nullptr;
+  int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream,
+                       pdl ? done : nullptr, B);
+  if (rc) return rc;
   rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
-                   max_pages, num_pages, nsplit, stream, nullptr, pdl);
+                   max_pages, num_pages, nsplit, stream, pdl ? done : nullptr, pdl);
   if (rc) return rc;
   return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
-                      static_cast<cudaStream_t>(stream), pdl);
+                      static_cast<cudaStream_t>(stream), pdl, pdl ? done : nullptr, nsplit * hgroups);
 }
 
 }  // extern "C"

@@ -51,20 +51,8 @@ struct DecodeParams {
   float rescale_threshold;      // lazy-rescale threshold (log2 units)
   long long* trace;             // debug: per-round clock64 events of CTA `trace_cta`, or null
   int trace_cta;                // debug: linear CTA index traced (x fastest)
-  // ---- fused mode (fused = 1): K1 and K3 folded into this kernel ---------------------------
-  // The nsplit CTAs of one (sequence, head group) each absorb a slice of the heads into q_abs
-  // (used as an L2-resident workspace), meet at a per-sequence barrier, run the split-KV
-  // attention, meet again after writing their partials, and each merges + up-projects its
-  // slice of heads into `out`. Needs every CTA of a sequence co-resident (cooperative launch).
-  int fused;
-  int DH;                       // query/output head width
-  float score_scale, alpha;     // tau*log2(e), alpha_attn
-  const __nv_bfloat16* q_nope;  // [B, H, DH]
-  const __nv_bfloat16* q_rope_in;  // [B, H, DR] (unscaled)
-  const __nv_bfloat16* w_uk;    // [H][DH][NB*DLAT]
-  const __nv_bfloat16* w_uv;    // [H][NB*DLAT][DH]
-  float* out;                   // [B, H, DH] = alpha * sum_b Z_b W^UV_b
-  int* sync;                    // [B * head_groups * 4] self-resetting barrier state (zeroed once)
+  int* done;                    // [B] per-sequence completion counters (or null): every CTA adds 1
+                                // after its partials are globally visible; K3 waits on them
   int pdl;                      // host side: launch with programmatic stream serialization
 };
 
@@ -111,62 +99,6 @@ __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
   return t;
-}
-
-// Sense-reversing barrier across the `n` CTAs of one sequence (called by ONE thread per CTA).
-// Self-resetting: the last arriver zeroes the counter and flips the flag, so the state can be
-// reused by the next launch (and inside CUDA graphs) without host resets.
-__device__ __forceinline__ void seq_barrier(int* cnt, int* flag, int n) {
-  volatile int* vflag = flag;
-  const int old = *vflag;  // read before arriving: the flip needs our arrival
-  __threadfence();
-  if (atomicAdd(cnt, 1) == n - 1) {
-    atomicExch(cnt, 0);
-    __threadfence();
-    atomicExch(flag, old ^ 1);
-  } else {
-    while (*vflag == old) __nanosleep(64);
-  }
-  __threadfence();
-}
-
-// y[c] = scale * sum_k x[k] * W[k][c] for c in one 8-column octet, W bf16 row-major with row
-// stride ldw, x either bf16 (absorb: query row) or fp32 in smem (up-projection: merged latent).
-// Warp-cooperative: lane j accumulates rows k = j, j+32, ... with 16-byte loads (all issued
-// before use), then a butterfly over the 32 lanes; every lane returns the 8 sums.
-template <int K_PER_LANE_MAX, typename Tx>
-__device__ __forceinline__ void warp_gemv_octet(const __nv_bfloat16* __restrict__ W, size_t ldw, const Tx* x, int K,
-                                                float (&y)[8]) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int j = 0; j < 8; ++j) y[j] = 0.f;
-  uint4 wv[K_PER_LANE_MAX];
-#pragma unroll
-  for (int i = 0; i < K_PER_LANE_MAX; ++i) {
-    const int k = lane + 32 * i;
-    wv[i] = (k < K) ? __ldg(reinterpret_cast<const uint4*>(W + size_t(k) * ldw)) : make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int i = 0; i < K_PER_LANE_MAX; ++i) {
-    const int k = lane + 32 * i;
-    float xv = 0.f;
-    if (k < K) {
-      if constexpr (sizeof(Tx) == 2) xv = __bfloat162float(x[k]);
-      else xv = x[k];
-    }
-    const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(w2[j]);
-      y[2 * j] = fmaf(xv, f.x, y[2 * j]);
-      y[2 * j + 1] = fmaf(xv, f.y, y[2 * j + 1]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) y[j] += __shfl_xor_sync(0xffffffffu, y[j], off);
-  }
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -263,86 +195,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_sh;
-  // heads of this CTA's slice (fused mode: absorption and merge/up-projection work split)
-  const int hpc = (HV + p.nsplit - 1) / p.nsplit;
-  const int hs0 = min(HV, split * hpc), hs1 = min(HV, hs0 + hpc);
-  int* sync_base = p.sync + (size_t(seq) * gridDim.z + hg) * 4;
-
   if (warp != 0) {
-    // ---- fused K1: absorb this CTA's heads into the q_abs workspace, then meet the other
-    //      splits of the sequence. The TMA producer (warp 0) is already streaming KV.
-    if (p.fused) {
-      {
-        // Work split over ALL CTAs of this head group (every sequence), so each W^UK byte is
-        // read once: units (head, 8-column octet) x all sequences. In a warp, lane = (k-slice
-        // j of DH/8 rows, sequence group g of 4); the 8 k-slices are reduced by shuffles.
-        const int C = gridDim.x * gridDim.y;
-        const int c = blockIdx.y * gridDim.x + blockIdx.x;
-        const int NCOL = NB * DLAT, octs = NCOL / 8, KS = p.DH / 8;
-        const int U = HV * octs;
-        const int u0 = int((long long)c * U / C), u1 = int((long long)(c + 1) * U / C);
-        const int j = lane & 7, g = lane >> 3;
-        for (int u = u0 + warp - 1; u < u1; u += kNumThreads / 32 - 1) {
-          const int hh = hg * NPAD + u / octs, col = (u % octs) * 8;
-          const __nv_bfloat16* wp = p.w_uk + (size_t(hh) * p.DH + j * KS) * NCOL + col;
-          uint4 wv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) wv[i] = i < KS ? __ldg(reinterpret_cast<const uint4*>(wp + size_t(i) * NCOL))
-                                                      : make_uint4(0, 0, 0, 0);
-          for (int s0 = 0; s0 < p.B; s0 += 4) {  // warp-uniform trip count (shuffles below)
-            const int sq = s0 + g;
-            const bool sv = sq < p.B;
-            float acc[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-            const __nv_bfloat16* xq = p.q_nope + (size_t(sv ? sq : 0) * p.H + hh) * p.DH + j * KS;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              if (i >= KS || !sv) break;
-              const float xv = __bfloat162float(xq[i]);
-              const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(w2[e]);
-                acc[2 * e] = fmaf(xv, f.x, acc[2 * e]);
-                acc[2 * e + 1] = fmaf(xv, f.y, acc[2 * e + 1]);
-              }
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
-              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);
-              acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 4);
-            }
-            if (j == 0 && sv) {
-              const int b = col / DLAT, cc = col % DLAT;
-              uint4 v;
-              v.x = pack_bf16(acc[0] * p.score_scale, acc[1] * p.score_scale);
-              v.y = pack_bf16(acc[2] * p.score_scale, acc[3] * p.score_scale);
-              v.z = pack_bf16(acc[4] * p.score_scale, acc[5] * p.score_scale);
-              v.w = pack_bf16(acc[6] * p.score_scale, acc[7] * p.score_scale);
-              *reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(p.q_abs) +
-                                        ((size_t(sq) * NB + b) * p.H + hh) * DLAT + cc) = v;
-            }
-          }
-        }
-        if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 4] = (long long)global_ns();
-        // scaled rope queries of the group, also split over the CTAs
-        const int R_all = p.B * HV * p.DR;
-        const int r0 = int((long long)c * R_all / C), r1 = int((long long)(c + 1) * R_all / C);
-        for (int i = r0 + tid - 32; i < r1; i += kNumThreads - 32) {
-          const int sq = i / (HV * p.DR), rem = i % (HV * p.DR);
-          const size_t off = (size_t(sq) * p.H + hg * NPAD + rem / p.DR) * p.DR + rem % p.DR;
-          const_cast<__nv_bfloat16*>(p.q_rope)[off] = __float2bfloat16(__bfloat162float(p.q_rope_in[off]) * p.score_scale);
-        }
-        __threadfence();
-      }
-      named_bar_sync(2, kNumThreads - 32);
-      if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 5] = (long long)global_ns();
-      if (tid == 32) seq_barrier(p.sync + hg * 4 + 0, p.sync + hg * 4 + 1, gridDim.x * gridDim.y);
-      named_bar_sync(2, kNumThreads - 32);
-      if (p.trace != nullptr && tid == 32 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin] = (long long)global_ns();
-    }
     // Under PDL this kernel overlaps K1's tail: the TMA producer is already streaming the
     // cache (written before K1 started); the queries are K1's output.
     griddep_wait();
@@ -725,11 +578,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (lane == 0) lred[(bb * 4 + q) * NPAD + h_lo + c] = v;
       }
     }
+    if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = clock64();
     if (ntiles > 0) {
       mbar_wait(o_final, 0);
       tc_fence_after();
     }
     named_bar_sync(1, kSoftThreads);
+    if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 4] = clock64();
     const size_t part_row0 = (size_t(seq) * p.nsplit + split) * NB;  // (seq, split, b) row index
     if (q == 0 && lane < h_cnt) {
       const int h = h_lo + lane;
@@ -772,66 +627,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-    // ---- fused K3: once every split of this sequence has written its partials, CTA `split`
-    //      merges heads [hs0, hs1) over the splits and up-projects them with W^UV.
-    if (p.fused) {
+    if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 5] = clock64();
+    // ---- completion: partials of this CTA globally visible -> count it for its sequence
+    if (p.done != nullptr) {
       __threadfence();
       named_bar_sync(1, kSoftThreads);
-      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 1] = (long long)global_ns();
-      if (ws == 0 && lane == 0) seq_barrier(sync_base + 2, sync_base + 3, p.nsplit);
-      named_bar_sync(1, kSoftThreads);
-      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 2] = (long long)global_ns();
-      const int t = tid - 64;
-      const int NCOL = NB * DLAT;
-      // heads in chunks that fit the two (now idle) P buffers
-      const int hc = (2 * L::kPBytes) / (4 * (NCOL + NB * p.nsplit));
-      for (int hc0 = hs0; hc0 < hs1; hc0 += hc) {
-      const int nh = min(hc, hs1 - hc0);
-      float* zs = reinterpret_cast<float*>(p_smem);  // [nh][NCOL] merged latent of this chunk's heads
-      float* wsp = zs + nh * NCOL;                     // [nh][NB][nsplit] split weights
-      for (int i = t; i < nh * NB; i += kSoftThreads) {
-        const int hl = i / NB, b = i % NB;
-        const float* l = p.lse_part + (size_t(seq) * p.nsplit * NB + b) * p.H + hg * NPAD + hc0 + hl;  // stride NB*H
-        float m = -INFINITY;
-        for (int k = 0; k < p.nsplit; ++k) m = fmaxf(m, __ldcg(l + size_t(k) * NB * p.H));
-        float tot = 0.f;
-        float* wr = wsp + (hl * NB + b) * p.nsplit;
-        for (int k = 0; k < p.nsplit; ++k) {
-          const float lk = __ldcg(l + size_t(k) * NB * p.H);
-          const float w = (m == -INFINITY || lk == -INFINITY) ? 0.f : ex2(lk - m);
-          wr[k] = w;
-          tot += w;
-        }
-        const float inv = tot > 0.f ? 1.f / tot : 0.f;
-        for (int k = 0; k < p.nsplit; ++k) wr[k] *= inv;
-      }
-      named_bar_sync(1, kSoftThreads);
-      for (int i = t; i < nh * NCOL; i += kSoftThreads) {
-        const int hl = i / NCOL, col = i % NCOL, b = col / DLAT, c = col % DLAT;
-        const float* o = p.o_part + ((size_t(seq) * p.nsplit * NB + b) * p.H + hg * NPAD + hc0 + hl) * DLAT + c;
-        const float* wr = wsp + (hl * NB + b) * p.nsplit;
-        float acc = 0.f;
-        for (int k = 0; k < p.nsplit; ++k) acc = fmaf(wr[k], __ldcg(o + size_t(k) * NB * p.H * DLAT), acc);
-        zs[i] = acc;
-      }
-      named_bar_sync(1, kSoftThreads);
-      if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 6] = (long long)global_ns();
-      // out[hh, d] = alpha * sum_k Z[k] W^UV[hh][k][d]: warp-units (head, 8-column octet of d),
-      // K = NB*DLAT split across lanes (<= 512 -> <= 16 rows per lane)
-      const int octs = p.DH / 8;
-      for (int u = ws; u < nh * octs; u += 8) {
-        const int hl = u / octs, d8 = u % octs;
-        const int hh = hg * NPAD + hc0 + hl;
-        float y[8];
-        warp_gemv_octet<16>(p.w_uv + size_t(hh) * NCOL * p.DH + d8 * 8, p.DH, zs + hl * NCOL, NCOL, y);
-        if (lane < 2) {
-          float4 v = lane == 0 ? make_float4(y[0], y[1], y[2], y[3]) : make_float4(y[4], y[5], y[6], y[7]);
-          v.x *= p.alpha; v.y *= p.alpha; v.z *= p.alpha; v.w *= p.alpha;
-          *reinterpret_cast<float4*>(p.out + (size_t(seq) * p.H + hh) * p.DH + d8 * 8 + lane * 4) = v;
-        }
-      }
-      named_bar_sync(1, kSoftThreads);
-      }
+      if (ws == 0 && lane == 0) atomicAdd(p.done + seq, 1);
     }
   }
   tc_fence_before();
@@ -840,7 +641,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin + 1] = (long long)global_ns();
     p.trace[13824 + 2 * cta_lin + 1] = clock64();
-    p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = tmem_base_sh[1];
   }
   if (warp == 1) {
     tc_fence_after();

@@ -267,10 +267,13 @@ def test_kimi_64_heads_tp4():
 
 
 @pytest.mark.parametrize("variant", ["mlra", "mla"])
-def test_opt_in_fused_step_matches_three_kernel_step(variant, monkeypatch):
-    """MLRA_FUSED=1 folds K1/K3 into K2 (grid + per-sequence barriers, cooperative launch).
-    It must reproduce the default K1 -> K2 -> K3 step up to reduction order, for ragged
-    lengths and both variants, and keep doing so over repeated calls (self-resetting barriers)."""
+def test_counter_chained_step_matches_stream_ordered_step(variant, monkeypatch):
+    """By default K3's CTAs wait on per-sequence K2 completion counters (reset by K1) instead
+    of on the whole K2 grid. Repeated steps and CUDA-graph replays must reproduce the plain
+    stream-ordered step (MLRA_NO_PDL=1) exactly -- same kernels, same reduction order --
+    for ragged lengths and both variants."""
+    import torch
+
     mlra = _mlra()
     cfg = mlra.trained_config("mlra4" if variant == "mlra" else "mla").with_(d=256, d_cq=256)
     ocfg = _oracle_cfg(cfg)
@@ -285,12 +288,25 @@ def test_opt_in_fused_step_matches_three_kernel_step(variant, monkeypatch):
         qrs.append(ak.bf16_round(qr[0]))
     eng = mlra.DecodeEngine(cfg, w, batch=len(lens), max_tokens=max(lens), page_size=64, nsplit=4)
     rounded = _engine_inputs(eng, seq_streams)
-    monkeypatch.delenv("MLRA_FUSED", raising=False)
+    monkeypatch.setenv("MLRA_NO_PDL", "1")
     base = _run(eng, qns, qrs)
-    monkeypatch.setenv("MLRA_FUSED", "1")
+    monkeypatch.delenv("MLRA_NO_PDL", raising=False)
     for _ in range(3):
         got = _run(eng, qns, qrs)
-        assert ak.max_rel_err(base, got) <= TOL_ORDER
+        assert np.array_equal(base, got)
+    # graph replay: the counter reset and the waits live inside the captured step
+    qn_t, qr_t = eng.prepare_queries(torch.tensor(np.stack(qns)), torch.tensor(np.stack(qrs)))
+    out = eng.decode_attention(qn_t, qr_t)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=s):
+        eng.decode_attention(qn_t, qr_t, out=out)
+    for _ in range(4):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(base, out.double().cpu().numpy())
     wb = _bf16_weights(w)
     for i in range(len(lens)):
         assert ak.max_rel_err(ak.decode_attention(ocfg, wb, rounded[i], qns[i], qrs[i]), got[i]) <= TOL

@@ -19,7 +19,7 @@ o = ops.decode_partials(*args)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 def med(xs): return int(st.median(xs)) if xs else -1
 ctas = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 8, 40, 77, 100, 135, 143]
-print("cta  dur_us  rounds period tma_lat arr->seen hold  soft  Pdone->PV  QK->S | start->TMA0 TMA0->data0 data0->Pdone0 lastPV->end (cycles)")
+print("cta  dur_us  rounds period tma_lat  hold  soft  Pdone->PV  QK->S | start->TMA0 TMA0->data0 data0->Pdone0 lastPV->softdone ->ofinal ->stored ->end (cycles)")
 for cta in ctas:
     os.environ["MLRA_DEBUG_TRACE_CTA"] = str(cta)
     for _ in range(3):
@@ -29,15 +29,16 @@ for cta in ctas:
     t = tt[: 7 * 256].view(7, 256)
     ce = tt[7 * 256:7 * 256 + 2048].view(1024, 2)
     n = int((t[1] != 0).sum())
-    arr = tt[12032 + 1024:12032 + 1280]
+    arr = t[6]
+    ep = tt[7 * 256 + 2048 + 8 * cta: 7 * 256 + 2048 + 8 * cta + 8]
     rr = range(3, n - 2)
     dur = (ce[cta, 1] - ce[cta, 0]).item() / 1e3
     print(f"{cta:3d} {dur:7.1f} {n:6d} {med([(t[6, r + 1] - t[6, r]).item() for r in rr]):6d} "
-          f"{med([(arr[r] - t[0, r]).item() for r in rr]):7d} {med([(t[6, r] - arr[r]).item() for r in rr]):9d} "
+          f"{med([(arr[r] - t[0, r]).item() for r in rr]):7d} "
           f"{med([(t[5, r] - t[6, r]).item() for r in rr]):5d} {med([(t[4, r] - t[3, r]).item() for r in rr]):5d} "
           f"{med([(t[2, r] - t[4, r]).item() for r in rr]):10d} {med([(t[3, r] - t[1, r]).item() for r in rr]):6d} | "
           f"{(t[0, 0] - tt[13824 + 2 * cta]).item():10d} {(arr[0] - t[0, 0]).item():11d} {(t[4, 0] - arr[0]).item():13d} "
-          f"{(tt[13824 + 2 * cta + 1] - t[5, n - 1]).item():11d}")
+          f"{(ep[3] - t[5, n - 1]).item():16d} {(ep[4] - ep[3]).item():7d} {(ep[5] - ep[4]).item():7d} {(tt[13824 + 2 * cta + 1] - ep[5]).item():5d}")
 n_cta = int((ce[:, 1] != 0).sum())
 s0 = ce[:n_cta, 0].double(); e0 = ce[:n_cta, 1].double()
 d = ((e0 - s0) / 1e3)
