@@ -118,6 +118,27 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
                      int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
                      int nsplit, float score_scale, float alpha, void* stream);
 
+/*
+ * GQA comparison variant (attnkit/decode.py:232-240 attend_local's non-latent branch,
+ * :258-261; kv_map zoo.py:35-38: query head i reads KV slot i // (h/g)) on the same split-KV
+ * kernel machinery: per KV head one K and one V sub-block per 128-token tile, no rope part.
+ *   q     [B, G, R, DH] bf16: query head b*R + j of this device (R = h/g per KV head),
+ *         post-RoPE, unscaled, zero-padded to DH in {64, 128}
+ *   pool  [num_pages*page_size, 2*G*DH] bf16 rows [K_0 | ... | K_{G-1} | V_0 | ... | V_{G-1}]
+ *         (post-RoPE keys, plain values, each zero-padded to DH)
+ *   score_scale = tau * log2(e), tau = 1/sqrt(d_h) (config.py:112), applied in fp32
+ *   o_part [B, nsplit, G, R, DH] fp32, lse_part [B, nsplit, G, R] fp32
+ *   out    [B, G*R, DH] fp32 (mlra_gqa_decode_step: K2 + split merge)
+ */
+int mlra_gqa_default_splits(int B, int G, int max_seqlen);
+size_t mlra_gqa_workspace_bytes(int B, int G, int R, int DH, int nsplit);
+int mlra_gqa_decode_partials(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                             float* o_part, float* lse_part, int B, int G, int R, int DH, int page_size, int max_pages,
+                             int num_pages, int nsplit, float score_scale, void* stream);
+int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                         float* out, void* workspace, int B, int G, int R, int DH, int page_size, int max_pages,
+                         int num_pages, int nsplit, float score_scale, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

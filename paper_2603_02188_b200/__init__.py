@@ -1,5 +1,5 @@
-"""B200-native decode attention for Multi-Head Low-Rank Attention (MLRA-4), with the MLA
-comparison variant, behind the reference kit's decode API (arXiv 2603.02188, "attnkit").
+"""B200-native decode attention for Multi-Head Low-Rank Attention (MLRA-4), with the MLA and
+GQA comparison variants, behind the reference kit's decode API (arXiv 2603.02188, "attnkit").
 
 Drop-in names (attnkit/__init__.py:25-53 subset for the decode path):
 ``AttnConfig``, ``trained_config``, ``table_context``, ``Rng``, ``WeightSet``,
@@ -39,7 +39,8 @@ def __getattr__(name):
         "sim_decode": ("tp", "sim_decode"), "ShardSet": ("tp", "ShardSet"), "DeviceShard": ("tp", "DeviceShard"),
         "TrafficLedger": ("tp", "TrafficLedger"), "TPDecodeGroup": ("tp", "TPDecodeGroup"),
         "PagedCache": ("cache", "PagedCache"), "PagedLatentCache": ("cache", "PagedLatentCache"),
-        "RowLayout": ("cache", "RowLayout"),
+        "RowLayout": ("cache", "RowLayout"), "GqaLayout": ("cache", "GqaLayout"),
+        "gqa": ("gqa", None), "GqaDecodeEngine": ("gqa", "GqaDecodeEngine"),
     }
     if name in lazy:
         import importlib

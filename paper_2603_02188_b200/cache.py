@@ -83,6 +83,10 @@ class RowLayout:
         i = self.units.index(name)
         return slice(i * self.dlp, i * self.dlp + self.dl)
 
+    def extract(self, name: str, rows: torch.Tensor) -> torch.Tensor:
+        """[..., W] pool rows -> [..., *row_shape] of one stream."""
+        return rows[..., self.column(name)]
+
     def pack_rows(self, rows: dict, device=None) -> torch.Tensor:
         """{stream: [..., width]} (numpy or torch, any float) -> [..., W] bf16 padded rows."""
         first = next(iter(rows.values()))
@@ -93,6 +97,51 @@ class RowLayout:
             v = torch.as_tensor(np.asarray(v) if not torch.is_tensor(v) else v, dtype=torch.float32, device=device)
             out[..., self.column(name)] = v
         return out.to(torch.bfloat16)
+
+
+@dataclass(frozen=True)
+class GqaLayout:
+    """Token-row layout of a GQA pool (the comparison variant, attnkit/zoo.py:47-58 streams
+    ``k`` and ``v`` of shape (g, d_h), cache.py:105-144): ``[K_0 | ... | K_{g-1} | V_0 | ... |
+    V_{g-1}]``, each KV head zero-padded to ``dhp`` in {64, 128} columns (zero key columns
+    leave the logits unchanged, zero value columns are sliced off the output)."""
+
+    g: int   # KV heads held by this device
+    dh: int  # head width
+
+    @property
+    def dhp(self) -> int:
+        if self.dh > 128:
+            raise ConfigError(f"gqa head width {self.dh} exceeds the kernel's 128-column sub-block")
+        return 64 if self.dh <= 64 else 128
+
+    @property
+    def units(self) -> tuple:
+        return ("k", "v")
+
+    @property
+    def width(self) -> int:
+        return 2 * self.g * self.dhp
+
+    def row_shapes(self) -> dict:
+        return {"k": (self.g, self.dh), "v": (self.g, self.dh)}
+
+    def extract(self, name: str, rows: torch.Tensor) -> torch.Tensor:
+        if name not in ("k", "v"):
+            raise ConfigError(f"gqa cache has no stream {name!r}")
+        o = 0 if name == "k" else self.g * self.dhp
+        part = rows[..., o:o + self.g * self.dhp]
+        return part.reshape(*part.shape[:-1], self.g, self.dhp)[..., :self.dh]
+
+    def pack_rows(self, rows: dict, device=None) -> torch.Tensor:
+        """{"k": [..., g, d_h], "v": [..., g, d_h]} -> [..., W] bf16 padded rows."""
+        k, v = (torch.as_tensor(np.asarray(rows[n]) if not torch.is_tensor(rows[n]) else rows[n],
+                                dtype=torch.float32, device=device) for n in ("k", "v"))
+        lead = tuple(k.shape[:-2])
+        out = torch.zeros(lead + (2, self.g, self.dhp), dtype=torch.float32, device=device)
+        out[..., 0, :, :self.dh] = k
+        out[..., 1, :, :self.dh] = v
+        return out.reshape(lead + (self.width,)).to(torch.bfloat16)
 
 
 class PagedCache:
@@ -158,8 +207,8 @@ class PagedCache:
         return self.block_table[s].long()[tok // self.page_size] * self.page_size + tok % self.page_size
 
     def stream(self, s: int, name: str) -> torch.Tensor:
-        """Device view (copy) of one stream of sequence s: [n, width] bf16."""
-        return self.pool[self.token_slots(s)][:, self.layout.column(name)]
+        """Device view (copy) of one stream of sequence s: [n, *row_shape] bf16."""
+        return self.layout.extract(name, self.pool[self.token_slots(s)])
 
 
 class PagedLatentCache:
@@ -229,7 +278,7 @@ class PagedLatentCache:
         if not 0 <= t < self.n:
             raise IndexError(t)
         slot = self.paged.token_slots(0)[t]
-        out = self.paged.pool[slot, self.layout.column(name)].float().cpu().numpy().astype(np.float64)
+        out = self.layout.extract(name, self.paged.pool[slot]).float().cpu().numpy().astype(np.float64)
         out.setflags(write=False)
         return out
 

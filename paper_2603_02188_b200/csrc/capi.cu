@@ -75,29 +75,35 @@ int set_smem_once(K kern, unsigned& done_mask, int bytes) {
 
 constexpr int kSmemBudget = 232448;  // 227 KB opt-in dynamic smem (the kernel has no static smem)
 
-template <int T, int NPAD, int DLS, int NB>
+template <int T, int NPAD, int DLS, int NB, bool GQA = false>
 int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra::DecodeParams p, int head_groups,
                   cudaStream_t stream) {
   using L = mlra::DecodeLayout<T, NPAD, DLS>;
   const int q_chunks = NB * p.SUB * (DLS / 64) + 1;
   const int fixed = q_chunks * L::kQChunkBytes + 2 * L::kPBytes + L::kScratchBytes;
-  // Rope ring: up to 4 tiles deep for one-branch configs; shrink it before the latent ring.
-  int rope_slots = (NB == 1 && p.SUB == 1) ? 4 : (T == 64 ? 3 : 2);
-  int lat_slots = 0;
-  for (;; --rope_slots) {
-    lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
-    if (lat_slots >= 2 * p.SUB + 2 || rope_slots == 2) break;
+  int rope_slots = 0, lat_slots = 0;
+  if (GQA) {
+    // K and V sub-blocks share one ring; no rope part
+    lat_slots = (kSmemBudget - fixed) / L::kLatBytes;
+    if (lat_slots < 3) return fail(MLRA_ERR_CONFIG, "gqa decode: ring of %d slots < 3", lat_slots);
+  } else {
+    // Rope ring: up to 4 tiles deep for one-branch configs; shrink it before the latent ring.
+    rope_slots = (NB == 1 && p.SUB == 1) ? 4 : (T == 64 ? 3 : 2);
+    for (;; --rope_slots) {
+      lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
+      if (lat_slots >= 2 * p.SUB + 2 || rope_slots == 2) break;
+    }
+    // QK(r+1) is issued while PV(r) still holds its sub-blocks: 2*SUB resident + 1 in flight
+    if (lat_slots < 2 * p.SUB + 1)
+      return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
+                  2 * p.SUB + 1);
   }
   if (lat_slots > mlra::kMaxLat) lat_slots = mlra::kMaxLat;
-  // QK(r+1) is issued while PV(r) still holds its sub-blocks: 2*SUB resident + 1 in flight
-  if (lat_slots < 2 * p.SUB + 1)
-    return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
-                2 * p.SUB + 1);
   p.lat_slots = lat_slots;
   p.rope_slots = rope_slots;
   const int smem = L::smem_bytes(NB, p.SUB, lat_slots, rope_slots);
   if (smem > kSmemBudget) return fail(MLRA_ERR_CONFIG, "decode: smem %d exceeds budget", smem);
-  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS, NB>;
+  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS, NB, GQA>;
   static unsigned attr_done = 0;  // per instantiation, one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -119,6 +125,57 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
   if (cudaLaunchKernelEx(&cfg, kern, lat_map, rope_map, p) != cudaSuccess)
     return cuda_check("mlra_decode_kernel launch");
   return cuda_check("mlra_decode_kernel launch");
+}
+
+// TMA views of a pool [rows, W] bf16 (pure host descriptors, cached per thread so a decode
+// loop over the same pool does not re-encode them every step):
+//   lat  = 3-D {64 columns, rows, nlat 64-column chunks} (chunk stride 128 B), box
+//          {64, T, DLS/64}: one box brings a DLS-wide sub-block of a T-token tile;
+//   rope = 2-D {W, rows}, box {64, box_rows} (rope tiles, and sub-blocks of 64-token pages).
+struct PoolMaps {
+  const void* pool;
+  cuuint64_t rows;
+  int W, T, box_rows, DLS, nlat;
+  CUtensorMap lat, rope;
+};
+
+int get_pool_maps(const void* pool, cuuint64_t total_rows, int W, int T, int box_rows, int DLS, int nlat,
+                  const PoolMaps** out) {
+  auto encode = get_encode();
+  if (!encode) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  thread_local PoolMaps cache[8];
+  thread_local int cache_next = 0;
+  for (auto& e : cache)
+    if (e.pool == pool && e.rows == total_rows && e.W == W && e.T == T && e.box_rows == box_rows && e.DLS == DLS &&
+        e.nlat == nlat) {
+      *out = &e;
+      return MLRA_OK;
+    }
+  PoolMaps e{pool, total_rows, W, T, box_rows, DLS, nlat, {}, {}};
+  {
+    cuuint64_t dims[2] = {cuuint64_t(W), total_rows};
+    cuuint64_t strides[1] = {cuuint64_t(W) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&e.rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(2d) failed (%d): W=%d", int(cr), W);
+  }
+  {
+    cuuint64_t dims[3] = {64, total_rows, cuuint64_t(nlat)};
+    cuuint64_t strides[2] = {cuuint64_t(W) * 2, 128};
+    cuuint32_t box[3] = {64, cuuint32_t(T), cuuint32_t(DLS / 64)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = encode(&e.lat, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d): W=%d", int(cr), W);
+  }
+  cache[cache_next] = e;
+  *out = &cache[cache_next];
+  cache_next = (cache_next + 1) % 8;
+  return MLRA_OK;
 }
 
 // TMEM columns used: 2 S slots (+ 2 rope-logit slots when NB > 1) + NB*SUB O blocks, NPAD each (<= 512).
@@ -253,54 +310,11 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   if (SUB > 1 && NB != 1) return fail(MLRA_ERR_CONFIG, "decode: multi-block latents (SUB>1) need NB=1");
   const int DLAT = SUB * DLS;
   const int W = NB * DLAT + DR;
-  auto encode = get_encode();
-  if (!encode) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int T = (SUB == 1) ? 128 : 64;  // SUB > 1 (MLA) keeps 2*SUB sub-blocks resident: 64-token tiles
   const int box_rows = (page_size % T == 0) ? T : 64;
   const cuuint64_t total_rows = cuuint64_t(num_pages) * cuuint64_t(page_size);
-  // Tensor maps are pure host descriptors; cache the last few per thread so a decode loop
-  // over the same pool does not re-encode them every step.
-  struct MapEntry {
-    const void* pool;
-    cuuint64_t rows;
-    int W, T, box_rows, DLS, nlat;
-    CUtensorMap lat, rope;
-  };
-  thread_local MapEntry cache[8];
-  thread_local int cache_next = 0;
-  const int nlat = NB * DLAT / 64;
-  MapEntry* hit = nullptr;
-  for (auto& e : cache)
-    if (e.pool == pool && e.rows == total_rows && e.W == W && e.T == T && e.box_rows == box_rows && e.DLS == DLS &&
-        e.nlat == nlat)
-      hit = &e;
-  if (!hit) {
-    MapEntry e{pool, total_rows, W, T, box_rows, DLS, nlat, {}, {}};
-    {
-      cuuint64_t dims[2] = {cuuint64_t(W), total_rows};
-      cuuint64_t strides[1] = {cuuint64_t(W) * 2};
-      cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
-      cuuint32_t estr[2] = {1, 1};
-      CUresult cr = encode(&e.rope, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(2d) failed (%d): W=%d", int(cr), W);
-    }
-    {
-      // {64 columns, rows, latent chunk}: chunk stride 128 B, row stride W*2 B
-      cuuint64_t dims[3] = {64, total_rows, cuuint64_t(nlat)};
-      cuuint64_t strides[2] = {cuuint64_t(W) * 2, 128};
-      cuuint32_t box[3] = {64, cuuint32_t(T), cuuint32_t(DLS / 64)};
-      cuuint32_t estr[3] = {1, 1, 1};
-      CUresult cr = encode(&e.lat, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d): W=%d", int(cr), W);
-    }
-    cache[cache_next] = e;
-    hit = &cache[cache_next];
-    cache_next = (cache_next + 1) % 8;
-  }
+  const PoolMaps* hit = nullptr;
+  if (int rc = get_pool_maps(pool, total_rows, W, T, box_rows, DLS, NB * DLAT / 64, &hit)) return rc;
   const CUtensorMap& lat_map = hit->lat;
   const CUtensorMap& rope_map = hit->rope;
 
@@ -344,6 +358,52 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   MLRA_NPAD(64, 64, 1);
 #undef MLRA_DISPATCH
 #undef MLRA_NPAD
+}
+
+// ----------------------------------------------------------------------------- GQA variant
+// KV heads per CTA: the largest of {4, 2, 1} dividing the device's KV-head count.
+static int gqa_nbc(int G) { return G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1); }
+
+static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                           float* o_part, float* lse_part, int B, int G, int R, int DH, int page_size, int max_pages,
+                           int num_pages, int nsplit, float score_scale, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (G < 1) return fail(MLRA_ERR_CONFIG, "gqa decode: G=%d KV heads", G);
+  if (R < 1 || R > 16) return fail(MLRA_ERR_CONFIG, "gqa decode: %d query heads per KV head not in [1,16]", R);
+  if (DH != 64 && DH != 128) return fail(MLRA_ERR_CONFIG, "gqa decode: padded head width %d not in {64,128}", DH);
+  if (page_size <= 0 || page_size % 64 != 0) return fail(MLRA_ERR_CONFIG, "gqa decode: page_size %d not a multiple of 64", page_size);
+  if (nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "gqa decode: nsplit %d not in [1,64]", nsplit);
+  const int W = 2 * G * DH;
+  const int T = 128;
+  const int box_rows = (page_size % T == 0) ? T : 64;
+  const cuuint64_t total_rows = cuuint64_t(num_pages) * cuuint64_t(page_size);
+  const PoolMaps* maps = nullptr;
+  if (int rc = get_pool_maps(pool, total_rows, W, T, box_rows, DH, W / 64, &maps)) return rc;
+  mlra::DecodeParams p{};
+  p.q_abs = static_cast<const __nv_bfloat16*>(q);
+  p.q_rope = nullptr;
+  p.block_table = block_table;
+  p.seqlens = seqlens;
+  p.o_part = o_part;
+  p.lse_part = lse_part;
+  p.B = B; p.H = R; p.SUB = 1; p.DR = 0; p.W = W;
+  p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
+  p.nb_total = G;
+  p.qk_scale = score_scale;
+  p.rescale_threshold = mlra::kRescaleThreshold;
+  if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
+  if (const char* e = getenv("MLRA_DEBUG_TRACE_CTA")) p.trace_cta = atoi(e);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nbc = gqa_nbc(G), z = G / nbc;
+#define MLRA_GQA(DD)                                                                      \
+  do {                                                                                    \
+    if (nbc == 4) return launch_decode<128, 16, DD, 4, true>(maps->lat, maps->rope, p, z, st); \
+    if (nbc == 2) return launch_decode<128, 16, DD, 2, true>(maps->lat, maps->rope, p, z, st); \
+    return launch_decode<128, 16, DD, 1, true>(maps->lat, maps->rope, p, z, st);          \
+  } while (0)
+  if (DH == 128) MLRA_GQA(128);
+  MLRA_GQA(64);
+#undef MLRA_GQA
 }
 
 // K3 needs a [B, H, NB*DLAT] fp32 scratch for the merged latent when it up-projects; the
@@ -466,6 +526,47 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   if (rc) return rc;
   return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
                       static_cast<cudaStream_t>(stream), pdl, pdl ? done : nullptr, nsplit * hgroups);
+}
+
+int mlra_gqa_default_splits(int B, int G, int max_seqlen) {
+  int sms = mlra_num_sms();
+  if (sms <= 0) sms = 148;
+  if (B < 1 || G < 1) return 1;
+  const int z = G / gqa_nbc(G);
+  const int tiles = (max_seqlen + 127) / 128;
+  int s = sms / (B * z);
+  if (s > tiles) s = tiles;
+  if (s > 64) s = 64;
+  return s < 1 ? 1 : s;
+}
+
+int mlra_gqa_decode_partials(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                             float* o_part, float* lse_part, int B, int G, int R, int DH, int page_size, int max_pages,
+                             int num_pages, int nsplit, float score_scale, void* stream) {
+  return gqa_decode_impl(q, pool, block_table, seqlens, o_part, lse_part, B, G, R, DH, page_size, max_pages, num_pages,
+                         nsplit, score_scale, stream);
+}
+
+size_t mlra_gqa_workspace_bytes(int B, int G, int R, int DH, int nsplit) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return al(size_t(B) * nsplit * G * R * DH * 4) + al(size_t(B) * nsplit * G * R * 4);
+}
+
+int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                         float* out, void* workspace, int B, int G, int R, int DH, int page_size, int max_pages,
+                         int num_pages, int nsplit, float score_scale, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* o_part = reinterpret_cast<float*>(ws);
+  ws += al(size_t(B) * nsplit * G * R * DH * 4);
+  float* lse_part = reinterpret_cast<float*>(ws);
+  int rc = gqa_decode_impl(q, pool, block_table, seqlens, o_part, lse_part, B, G, R, DH, page_size, max_pages,
+                           num_pages, nsplit, score_scale, stream);
+  if (rc) return rc;
+  // split merge; KV head b's query head j is output head b*R + j (out [B, G*R, DH])
+  return combine_impl(o_part, lse_part, nullptr, out, nullptr, B, R, G, DH, DH, nsplit, 1.f, 0,
+                      static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -53,6 +53,13 @@ struct DecodeParams {
   int trace_cta;                // debug: linear CTA index traced (x fastest)
   int* done;                    // [B] per-sequence completion counters (or null): every CTA adds 1
                                 // after its partials are globally visible; K3 waits on them
+  // ---- GQA comparison variant (template GQA = true) ------------------------------------------
+  // Pool row [K_0 | ... | K_{G-1} | V_0 | ... | V_{G-1}] (each DLS wide, post-RoPE keys), no
+  // rope part (DR = 0). "Branch" = KV head: blockIdx.z selects NB of the nb_total KV heads,
+  // H = query heads per KV head. q_abs holds the unscaled queries [B, nb_total, H, DLS]; the
+  // score scale tau*log2(e) is applied in fp32 by the softmax (qk_scale).
+  int nb_total;
+  float qk_scale;
   int pdl;                      // host side: launch with programmatic stream serialization
 };
 
@@ -107,7 +114,7 @@ __device__ __forceinline__ float warp_max(float v) {
   return r;
 }
 
-template <int T, int NPAD, int DLS, int NB>
+template <int T, int NPAD, int DLS, int NB, bool GQA = false>
 __global__ void __launch_bounds__(kNumThreads, 1)
     mlra_decode_kernel(const __grid_constant__ CUtensorMap lat_map, const __grid_constant__ CUtensorMap rope_map,
                        const DecodeParams p) {
@@ -118,9 +125,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   static_assert(NB >= 1 && NB <= 4, "1..4 branches per device");
   constexpr int kHG = NPAD / 2;  // heads (TMEM columns) per softmax group
 
-  const int SUB = p.SUB;
+  const int SUB = GQA ? 1 : p.SUB;
   const int DLAT = SUB * DLS;
-  const int seq = blockIdx.y, split = blockIdx.x, hg = blockIdx.z;
+  const int seq = blockIdx.y, split = blockIdx.x;
+  // MLRA/MLA: blockIdx.z = head group; GQA: blockIdx.z = group of NB KV heads (all its heads)
+  const int hg = GQA ? 0 : blockIdx.z;
+  const int branch0 = GQA ? blockIdx.z * NB : 0;  // first branch of this CTA in the q/partials layout
+  const int nbq = GQA ? p.nb_total : NB;           // branches in the q_abs / o_part / lse layouts
   const int len = p.seqlens[seq];
   const int ntiles_total = (len + T - 1) / T;
   const int per = (ntiles_total + p.nsplit - 1) / p.nsplit;
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // TMEM columns: S slots [0, 2*NPAD); (NB > 1) rope-logit slots [2*NPAD, 4*NPAD);
   // O_{b,s} at O_COL + (b*SUB+s)*NPAD
   constexpr uint32_t kTmemCols = 512;
-  constexpr bool kSharedRope = NB > 1;
+  constexpr bool kSharedRope = NB > 1 && !GQA;
   const uint32_t S_COL = 0, SR_COL = 2 * NPAD, O_COL = (kSharedRope ? 4 : 2) * NPAD;
 
   if (tid == 0) {
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (h < p.H) {
           if (chunk < nlat_chunks) {
             const int b = chunk / (DLAT / 64), c = chunk % (DLAT / 64);
-            v = __ldcg(reinterpret_cast<const uint4*>(p.q_abs + ((size_t(seq) * NB + b) * p.H + h) * DLAT + c * 64 +
+            v = __ldcg(reinterpret_cast<const uint4*>(p.q_abs + ((size_t(seq) * nbq + branch0 + b) * p.H + h) * DLAT + c * 64 +
                                                       u * 8));
           } else if (u * 8 < p.DR) {
             v = __ldcg(reinterpret_cast<const uint4*>(p.q_rope + (size_t(seq) * p.H + h) * p.DR + u * 8));
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         int rows[T / 64];
 #pragma unroll
         for (int i = 0; i < T / 64; ++i) rows[i] = __shfl_sync(0xffffffffu, my_row, tf * nbox + (i < nbox ? i : 0));
-        {
+        if (!GQA) {
           const int slot = t % p.rope_slots;
           mbar_wait(&rope_empty[slot], ((t / p.rope_slots) & 1) ^ 1);
           if (lane == 0) {
@@ -265,20 +276,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                rows[i], policy);
           }
         }
-        for (int u = 0; u < NB * SUB; ++u) {
+        // units of the tile: MLRA/MLA the NB*SUB latent sub-blocks; GQA K_b then V_b per KV head
+        for (int u = 0; u < (GQA ? 2 * NB : NB * SUB); ++u) {
+          const int ch0 = GQA ? ((u & 1) ? p.nb_total + branch0 + (u >> 1) : branch0 + (u >> 1)) * (DLS / 64)
+                              : u * (DLS / 64);  // first 64-column chunk of the unit in the row
           mbar_wait(&lat_empty[lslot], lphase ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&lat_full[lslot], L::kLatBytes);
             uint8_t* dst = lat_ring + lslot * L::kLatBytes;
             if (nbox == 1) {
               // one box = [DLS/64 chunks][T rows][128 B]: exactly the chunk-major smem layout
-              tma_load_3d_hint(&lat_map, &lat_full[lslot], dst, 0, rows[0], u * (DLS / 64), policy);
+              tma_load_3d_hint(&lat_map, &lat_full[lslot], dst, 0, rows[0], ch0, policy);
             } else {
               // pages of 64 tokens: per chunk, per 64-row page box (2-D view)
               for (int c = 0; c < DLS / 64; ++c)
                 for (int i = 0; i < nbox; ++i)
                   tma_load_2d_hint(&rope_map, &lat_full[lslot], dst + c * L::kChunkBytes + i * box_bytes,
-                                   u * DLS + c * 64, rows[i], policy);
+                                   (ch0 + c) * 64, rows[i], policy);
             }
             trace_event(p.trace, p.trace_cta, 0, t * NB * SUB + u);
           }
@@ -308,11 +322,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const uint32_t q_rope_addr = q_base + (NB * SUB * (DLS / 64)) * L::kQChunkBytes;
         int lslot = 0, lphase = 0;
         for (int t = 0; t < ntiles; ++t) {
-          const int rslot = t % p.rope_slots;
+          const int rslot = GQA ? 0 : t % p.rope_slots;
           const uint64_t ra0 = kdesc_sw128 + ((rope_base + rslot * L::kRopeBytes) >> 4);
           const uint64_t rb0 = kdesc_sw128 + (q_rope_addr >> 4);
           if (lane == 0) trace_event(p.trace, p.trace_cta, 12, t * NB);
-          mbar_wait(&rope_full[rslot], (t / p.rope_slots) & 1);
+          if (!GQA) mbar_wait(&rope_full[rslot], (t / p.rope_slots) & 1);
           if constexpr (kSharedRope) {
             // rope logits of the tile, once for all branches
             mbar_wait(&sr_empty[t & 1], ((t >> 1) & 1) ^ 1);
@@ -343,10 +357,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                 b0 + ((c * L::kQChunkBytes + kk * 32) >> 4), idesc_qk, acc);
                   acc = 1;
                 }
+              if constexpr (GQA) {
+                // K_b is QK's alone: release it here; then step over V_b (the PV warp's)
+                mma_commit_w(&lat_empty[lslot]);
+                if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
+              }
               if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
             }
             if (lane == 0) trace_event(p.trace, p.trace_cta, 1, r);
-            if constexpr (!kSharedRope) {
+            if constexpr (GQA) {
+              mma_commit_w(&s_full[sslot]);
+            } else if constexpr (!kSharedRope) {
               for (int kk = 0; kk < kq_rope; ++kk) mma_bf16_ss_w(d, ra0 + kk * 2, rb0 + kk * 2, idesc_qk, 1);
               mma_commit_w(&s_full[sslot]);
               mma_commit_w(&rope_empty[rslot]);
@@ -357,12 +378,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       } else {
         constexpr uint32_t idesc_pv = make_idesc_bf16(DLS, NPAD, true, true);
-        int lslot = 0;
+        int lslot = 0, lphase = 0;
         for (int t = 0; t < ntiles; ++t) {
 #pragma unroll 1
           for (int b = 0; b < NB; ++b) {
             const int r = t * NB + b;
             const int pslot = r & 1;
+            if constexpr (GQA) {
+              // step over K_b (the QK warp's) to V_b, and wait for V_b itself
+              if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
+              mbar_wait(&lat_full[lslot], lphase);
+            }
             mbar_wait(&p_full[pslot], (r >> 1) & 1);
             if (lane == 0) trace_event(p.trace, p.trace_cta, 2, r);
             tc_fence_after();
@@ -375,7 +401,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               for (int k = 0; k < T / 16; ++k)
                 mma_bf16_ss_w(d, a0 + k * (2048 >> 4), pb + k * (256 >> 4), idesc_pv, acc0 | k);
               mma_commit_w(&lat_empty[lslot]);
-              if (++lslot == p.lat_slots) lslot = 0;
+              if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
             }
             mma_commit_w(&p_empty[pslot]);
             mma_commit_w(&o_done[b]);
@@ -444,6 +470,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]) + __uint_as_float(rr[c]);
+          } else if constexpr (GQA) {
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < kHG; ++c) s[c] = __uint_as_float(raw[c]) * p.qk_scale;
           } else {
             tmem_ld_wait();
 #pragma unroll
@@ -585,7 +615,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     named_bar_sync(1, kSoftThreads);
     if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 4] = clock64();
-    const size_t part_row0 = (size_t(seq) * p.nsplit + split) * NB;  // (seq, split, b) row index
+    const size_t part_row0 = (size_t(seq) * p.nsplit + split) * nbq + branch0;  // (seq, split, b) row index
     if (q == 0 && lane < h_cnt) {
       const int h = h_lo + lane;
 #pragma unroll

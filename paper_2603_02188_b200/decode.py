@@ -26,13 +26,13 @@ import numpy as np
 import torch
 
 from . import ops
-from .cache import PagedCache, PagedLatentCache, RowLayout
+from .cache import GqaLayout, PagedCache, PagedLatentCache, RowLayout
 from .config import LATENT_VARIANTS, AttnConfig
 from .costs import calib_factors
 from .errors import ConfigError, IntegrityError, RoutingError
 from .projections import LatentProjector
 
-SERVED = ("mla", "mlra")
+SERVED = ("mla", "mlra", "gqa")
 
 
 @dataclass(frozen=True)
@@ -77,6 +77,8 @@ def _check_served(cfg: AttnConfig) -> None:
 def full_ownership(cfg: AttnConfig) -> Ownership:  # decode.py:53-76 (served variants)
     _check_served(cfg)
     all_heads = tuple(range(cfg.h))
+    if cfg.variant == "gqa":
+        return Ownership(all_heads, kv_slots=tuple(range(cfg.g)))
     if cfg.variant == "mla":
         return Ownership(all_heads, units=(LatentUnit(-1, -1, all_heads),))
     return Ownership(all_heads, units=tuple(LatentUnit(-1, b, all_heads) for b in range(4)))
@@ -86,7 +88,9 @@ def unit_width(cfg: AttnConfig) -> int:
     return cfg.d_c if cfg.variant == "mla" else cfg.block_dim
 
 
-def row_layout(cfg: AttnConfig, own: Ownership) -> RowLayout:
+def row_layout(cfg: AttnConfig, own: Ownership):
+    if cfg.variant == "gqa":
+        return GqaLayout(len(own.kv_slots), cfg.d_h)
     return RowLayout(tuple(u.stream for u in own.units), unit_width(cfg), cfg.d_h_rope)
 
 
@@ -204,6 +208,10 @@ def attend_local(cfg: AttnConfig, local_w, own: Ownership, cache: PagedLatentCac
     _check_served(cfg)
     if not isinstance(cache, PagedLatentCache):
         raise RoutingError("attend_local on the B200 path needs a PagedLatentCache (new_cache)")
+    if cfg.variant == "gqa":
+        from .gqa import attend_local_gqa
+
+        return attend_local_gqa(cfg, own, cache, queries)
     if cache.n == 0:
         raise ConfigError("cache read: stream 'rope' is empty")
     heads = list(own.units[0].heads)
@@ -242,7 +250,12 @@ class _StepState:
     """Per-(config, weights) device state for the single-sequence drop-in step."""
 
     def __init__(self, cfg: AttnConfig, w, device):
-        self.projector = LatentProjector(cfg, w, device)
+        if cfg.variant == "gqa":
+            from .projections import GqaProjector
+
+            self.projector = GqaProjector(cfg, w, device)
+        else:
+            self.projector = LatentProjector(cfg, w, device)
         self.own = full_ownership(cfg)
         self.lw = local_weights(cfg, w, self.own)
 
@@ -280,6 +293,14 @@ def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tu
     dev = cache.paged.device
     st = _state(cfg, w, dev)
     pos = cache.pos_offset + cache.n
+    if cfg.variant == "gqa":
+        # zoo projections (zoo.py:47-58): append k, v rows, attend on the cached heads
+        hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
+        q, k, v = st.projector(hidden, torch.tensor([pos], device=dev))
+        cache.append_packed(cache.layout.pack_rows({"k": k[0], "v": v[0]}, device=dev)[None])
+        contribs = attend_local(cfg, {}, st.own, cache, {"q": q[0]})
+        out, _ = reduce_contributions(cfg, contribs)
+        return out, cache
     rows, q_nope, q_rope = _project_rows(cfg, st, cache.layout, h_t, pos, dev)
     cache.append_packed(cache.layout.pack_rows(rows, device=dev)[None])
     qn, qr = _queries_to_device(cfg, cache.layout, q_nope, q_rope, list(range(cfg.h)), dev)
@@ -311,6 +332,8 @@ class DecodeEngine:
                  page_size: int = 128, device=None, nsplit: int | None = None, page_order=None,
                  alpha: float | None = None):
         _check_served(cfg)
+        if cfg.variant == "gqa":
+            raise RoutingError("DecodeEngine serves the latent family; use gqa.GqaDecodeEngine for gqa")
         self.cfg = cfg
         self.own = own or full_ownership(cfg)
         self.layout = row_layout(cfg, self.own)

@@ -165,6 +165,62 @@ def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seq
     return out
 
 
+# ----------------------------------------------------------------------------- GQA variant
+def gqa_default_splits(batch: int, kv_heads: int, max_seqlen: int) -> int:
+    return _lib.load().mlra_gqa_default_splits(batch, kv_heads, max_seqlen)
+
+
+def gqa_decode_partials(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor, seqlens: torch.Tensor,
+                        page_size: int, nsplit: int, score_scale: float, out=None):
+    """K2 (GQA): q [B, G, R, DH] bf16 (post-RoPE, unscaled, DH in {64, 128}) over a pool of rows
+    [K_0..K_{G-1} | V_0..V_{G-1}] -> o_part [B, nsplit, G, R, DH], lse_part [B, nsplit, G, R]."""
+    _need(q, torch.bfloat16, "q", 4)
+    _need(pool, torch.bfloat16, "pool", 2)
+    _need(block_table, torch.int32, "block_table", 2)
+    _need(seqlens, torch.int32, "seqlens", 1)
+    B, G, R, DH = q.shape
+    if pool.shape[1] != 2 * G * DH:
+        raise ShapeMismatchError(f"gqa pool width {pool.shape[1]} != 2*G*DH = {2 * G * DH}")
+    if out is None:
+        o_part = torch.empty((B, nsplit, G, R, DH), dtype=torch.float32, device=q.device)
+        lse_part = torch.empty((B, nsplit, G, R), dtype=torch.float32, device=q.device)
+    else:
+        o_part, lse_part = out
+    rc = _lib.load().mlra_gqa_decode_partials(q.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
+                                              seqlens.data_ptr(), o_part.data_ptr(), lse_part.data_ptr(), B, G, R,
+                                              DH, page_size, block_table.shape[1], pool.shape[0] // page_size, nsplit,
+                                              float(score_scale), _stream())
+    _lib.check(rc, "mlra_gqa_decode_partials")
+    return o_part, lse_part
+
+
+class GqaWorkspace:
+    """Device scratch (split partials) of one GQA decode step."""
+
+    def __init__(self, batch: int, kv_heads: int, reps: int, dh: int, nsplit: int, device):
+        nbytes = _lib.load().mlra_gqa_workspace_bytes(batch, kv_heads, reps, dh, nsplit)
+        self.key = (batch, kv_heads, reps, dh, nsplit)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def gqa_decode_step(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor, seqlens: torch.Tensor,
+                    page_size: int, nsplit: int, score_scale: float, workspace: GqaWorkspace,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+    """K2 (GQA) + split merge: q [B, G, R, DH] -> out [B, G*R, DH] fp32 (head b*R + j)."""
+    _need(q, torch.bfloat16, "q", 4)
+    B, G, R, DH = q.shape
+    if workspace.key != (B, G, R, DH, nsplit):
+        raise ConfigError(f"gqa workspace sized for {workspace.key}, call needs {(B, G, R, DH, nsplit)}")
+    if out is None:
+        out = torch.empty((B, G * R, DH), dtype=torch.float32, device=q.device)
+    rc = _lib.load().mlra_gqa_decode_step(q.data_ptr(), pool.data_ptr(), block_table.data_ptr(), seqlens.data_ptr(),
+                                          out.data_ptr(), workspace.buf.data_ptr(), B, G, R, DH, page_size,
+                                          block_table.shape[1], pool.shape[0] // page_size, nsplit, float(score_scale),
+                                          _stream())
+    _lib.check(rc, "mlra_gqa_decode_step")
+    return out
+
+
 def score_scale(tau: float) -> float:
     """Scale folded into the queries: scores are evaluated in the log2 domain."""
     return float(tau) * LOG2E

@@ -46,6 +46,18 @@ def shard_ownership(cfg: AttnConfig, phi: int, device_id: int) -> Ownership:  # 
     _check_served(cfg)
     h, k = cfg.h, device_id
     all_heads = tuple(range(h))
+    if cfg.variant == "gqa":
+        # KV-head axis first; beyond g devices, the query heads of one KV head are split
+        g, r = cfg.g, h // cfg.g
+        if phi <= g:
+            slots = _ranges(g, phi, "KV-head axis")[k]
+            return Ownership(tuple(range(slots[0] * r, (slots[-1] + 1) * r)), kv_slots=slots)
+        per_group = phi // g
+        if phi % g != 0 or r % per_group != 0:
+            raise ConfigError(f"gqa: cannot split {r} heads per KV head across {per_group} devices")
+        group = k // per_group
+        heads = tuple(i + group * r for i in _ranges(r, per_group, "query-head axis")[k % per_group])
+        return Ownership(heads, kv_slots=(group,))
     if cfg.variant == "mla":
         heads = _ranges(h, phi, "query-head axis")[k]
         return Ownership(heads, units=(LatentUnit(-1, -1, heads),))
@@ -57,7 +69,9 @@ def shard_ownership(cfg: AttnConfig, phi: int, device_id: int) -> Ownership:  # 
     return Ownership(heads, units=(LatentUnit(-1, block, heads),))
 
 
-def _resource_keys(own: Ownership) -> list[str]:  # tpsim.py:134-144 (latent family)
+def _resource_keys(own: Ownership) -> list[str]:  # tpsim.py:134-144 (latent family + gqa)
+    if not own.units:
+        return [f"k{s}" for s in own.kv_slots] + [f"v{s}" for s in own.kv_slots]
     return [unit.stream for unit in own.units] + ["rope"]
 
 
@@ -158,8 +172,20 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
     st = _state(cfg, w, dev)
     before = [s.cache.reads for s in shards.shards]
     by_device: dict = {}
+    if cfg.variant == "gqa":
+        import torch
+
+        hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
+        q, k, v = st.projector(hidden, torch.tensor([pos], device=dev))
     for idx in exec_order:
         shard = shards.shards[idx]
+        if cfg.variant == "gqa":
+            slots = list(shard.own.kv_slots)
+            rows = {"k": k[0][slots], "v": v[0][slots]}
+            shard.cache.append_packed(shard.cache.layout.pack_rows(rows, device=dev)[None])
+            by_device[shard.device_id] = attend_local(cfg, {}, shard.own, shard.cache,
+                                                      {"q": q[0].double().cpu().numpy()})
+            continue
         rows, q_nope, q_rope = _project_rows(cfg, st, shard.cache.layout, h_t, pos, dev)
         shard.cache.append_packed(shard.cache.layout.pack_rows(rows, device=dev)[None])
         queries = {"q_nope": q_nope.double().cpu().numpy(), "q_rope": q_rope.double().cpu().numpy()}

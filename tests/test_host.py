@@ -79,7 +79,42 @@ def test_shard_ownership_rules():
     with pytest.raises(ConfigError, match="TP degree"):
         shard_ownership(p, 16, 0)
     with pytest.raises(RoutingError):
-        shard_ownership(trained_config("gqa"), 2, 0)
+        shard_ownership(trained_config("mla").with_(variant="mha"), 2, 0)
+
+
+@pytest.mark.parametrize("shape,phi", [("2.9b", 1), ("2.9b", 2), ("kimi", 1), ("kimi", 4), ("kimi", 8)])
+def test_gqa_shard_ownership_matches_oracle(shape, phi):
+    """tpsim.py:58-131 for gqa (g=6 at the 2.9B shape, g=8 at the Kimi context shape):
+    KV-head axis, grouped heads."""
+    from oracle import attnkit_port as ak
+    from paper_2603_02188_b200.config import table_context
+    from paper_2603_02188_b200.tp import shard_ownership
+
+    cfg = trained_config("gqa") if shape == "2.9b" else table_context()["gqa"]
+    for k in range(phi):
+        own = shard_ownership(cfg, phi, k)
+        heads, slots = ak.shard_units(ak.cfg_from(cfg), phi, k)
+        assert own.heads == tuple(heads) and own.kv_slots == tuple(slots) and own.units == ()
+
+
+def test_gqa_layout_pack_and_extract():
+    import torch
+
+    from paper_2603_02188_b200.cache import GqaLayout
+
+    lay = GqaLayout(3, 8)
+    assert (lay.dhp, lay.width) == (64, 384) and lay.row_shapes() == {"k": (3, 8), "v": (3, 8)}
+    k = np.arange(24, dtype=np.float64).reshape(3, 8)
+    v = -np.arange(24, dtype=np.float64).reshape(3, 8) - 1
+    row = lay.pack_rows({"k": k, "v": v}, device=torch.device("cpu"))
+    assert row.shape == (384,)
+    r = row.float().numpy()
+    assert list(r[64:72]) == list(k[1]) and r[72:128].sum() == 0 and list(r[192 + 128:192 + 136]) == list(v[2])
+    np.testing.assert_array_equal(lay.extract("k", row[None]).float().numpy()[0], k)
+    np.testing.assert_array_equal(lay.extract("v", row[None]).float().numpy()[0], v)
+    assert GqaLayout(6, 128).width == 1536
+    with pytest.raises(ConfigError):
+        GqaLayout(1, 256).dhp
 
 
 def test_row_layout_padding():
@@ -131,8 +166,10 @@ def test_pack_rows_places_streams():
 def test_decode_routing_errors():
     from paper_2603_02188_b200.decode import decode_step, full_ownership
 
+    own = full_ownership(trained_config("gqa"))
+    assert own.kv_slots == tuple(range(6)) and own.heads == tuple(range(24))
     with pytest.raises(RoutingError):
-        full_ownership(trained_config("gqa"))
+        full_ownership(trained_config("mla").with_(variant="mha"))
     cfg = AttnConfig("mlra", branches=2, h=4, d=32, d_h=8, d_h_rope=4, d_c=32, d_cq=16)
     with pytest.raises(RoutingError):
         full_ownership(cfg)
