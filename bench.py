@@ -185,6 +185,42 @@ class StepRunner:
         self.graphs[i % 2].replay()
 
 
+class GqaStepRunner:
+    """GQA comparison variant (2.9B: h=24, g=6, d_h=128): two engines over distinct random
+    caches, alternated, one CUDA graph each (K2 GQA + split merge)."""
+
+    def __init__(self, cfg, own, batch, ctx, device):
+        import torch
+
+        from paper_2603_02188_b200.gqa import GqaDecodeEngine
+
+        self.engines, self.graphs = [], []
+        for i in range(2):
+            g = torch.Generator(device=device).manual_seed(2000 + i)
+            eng = GqaDecodeEngine(cfg, own, batch=batch, max_tokens=ctx + 64, page_size=128, device=device)
+            pool = eng.cache.pool
+            for s0 in range(0, pool.shape[0], 1 << 20):
+                e = min(pool.shape[0], s0 + (1 << 20))
+                pool[s0:e] = torch.randn((e - s0, pool.shape[1]), generator=g, device=device).to(torch.bfloat16)
+            eng.cache.seqlens.fill_(ctx)
+            eng.cache._host_lens = [ctx] * batch
+            q = eng.prepare_queries(torch.randn((batch, cfg.h, cfg.d_h), generator=g, device=device))
+            self.engines.append((eng, q))
+        stream = torch.cuda.Stream(device=device)
+        for eng, q in self.engines:
+            eng.decode_attention(q)
+        torch.cuda.synchronize()
+        for eng, q in self.engines:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                eng.decode_attention(q)
+            self.graphs.append(gr)
+        torch.cuda.synchronize()
+
+    def replay(self, i):
+        self.graphs[i % 2].replay()
+
+
 def time_graph_steps(runner, steps, warmup, rank_sync):
     import torch
 
@@ -481,6 +517,24 @@ def per_gpu_comparisons(cfg, device, args):
         "speedup_per_gpu_tp4": round(res["mla_tp4_rank"]["us_per_step"] / res["mlra4_tp4_rank"]["us_per_step"], 3),
         "mla_tp1_us": res["mla_tp1"]["us_per_step"], "mla_tp1_gbs": res["mla_tp1"]["gbs"],
         "paper_claim": "~2.8x (H100, FlashMLA vs FA3-based MLRA-4)", "traffic_ratio": 3.0,
+    }
+    # GQA baseline (2.9B, g=6: K and V heads, 3072 B/token at TP1, 1536 B/token per TP2 rank)
+    gqa = trained_config("gqa")
+    g_res = {}
+    for name, own, phi in (("gqa_tp1", None, 1), ("gqa_tp2_rank", shard_ownership(gqa, 2, 0), 2)):
+        r = GqaStepRunner(gqa, own, BATCH_PER_GROUP, CTX, device)
+        ms = time_graph_steps(r, args.steps, args.warmup, torch.cuda.synchronize)
+        nbytes = algorithmic_bytes(gqa, phi, [CTX] * BATCH_PER_GROUP)
+        g_res[name] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                       "algorithmic_bytes": nbytes}
+        del r
+        torch.cuda.empty_cache()
+    out["vs_gqa"] = {
+        "gqa_tp1": g_res["gqa_tp1"], "gqa_tp2_rank": g_res["gqa_tp2_rank"],
+        "mlra4_tp4_rank_us": res["mlra4_tp4_rank"]["us_per_step"],
+        "speedup_per_gpu_mlra4_tp4_vs_gqa_tp2": round(g_res["gqa_tp2_rank"]["us_per_step"] /
+                                                      res["mlra4_tp4_rank"]["us_per_step"], 3),
+        "traffic_ratio_gqa_tp2_rank_vs_mlra4_tp4_rank": 4.0,
     }
     return out
 

@@ -301,8 +301,7 @@ absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __
 
 // K3: split merge + W^UV up-projection + ascending branch sum + alpha
 // (attnkit/decode.py:228 per branch, then reduce_contributions :264-285).
-// Grid (ceil(B/SEQS), H, NB), SEQS in {4, 8} sequences per CTA (8 when 4 would need more
-// than one wave); with NB > 1 and a summed output the NB CTAs of a (sequence group, head)
+// Grid (ceil(B/SEQS), H, NB), SEQS (4) sequences per CTA; with NB > 1 and a summed output the NB CTAs of a (sequence group, head)
 // form a cluster: each up-projects its branch, rank 0 adds the NB results through
 // distributed shared memory in ascending branch order (deterministic, the reference's
 // order) and writes the head. Per CTA:

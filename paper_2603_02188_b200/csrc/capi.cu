@@ -416,24 +416,17 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
                         bool pdl = false, const int* done = nullptr, int target = 0) {
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
-  // sequences per CTA: 4, or 8 when 4 would need more than one wave (2 CTAs per SM)
-  int sms = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const bool seq8 = long((B + 3) / 4) * H * NB > 2L * sms;
-  const size_t c4smem = seq8 ? mlra::combine4_smem<8>(DLAT, DH, nsplit) : mlra::combine4_smem<4>(DLAT, DH, nsplit);
+  const size_t c4smem = mlra::combine4_smem<4>(DLAT, DH, nsplit);
   if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
-    // CTA = (4 or 8 sequences, head, branch); with a summed output the NB branch CTAs of a
+    // CTA = (4 sequences, head, branch); with a summed output the NB branch CTAs of a
     // (sequence group, head) form a cluster and add their results through DSMEM.
-    auto kern = seq8 ? mlra::combine4_kernel<8> : mlra::combine4_kernel<4>;
-    static unsigned attr_done4 = 0, attr_done8 = 0;
-    if (int rc = set_smem_once(kern, seq8 ? attr_done8 : attr_done4, kSmemBudget)) return rc;
+    // (8 sequences per CTA measured slower even where 4 needs 1.3 waves.)
+    auto kern = mlra::combine4_kernel<4>;
+    static unsigned attr_done4 = 0;
+    if (int rc = set_smem_once(kern, attr_done4, kSmemBudget)) return rc;
     const int per_branch = upproj == 2 ? 1 : 0;
-    const int seqs = seq8 ? 8 : 4;
+    const int seqs = 4;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
     cfg.blockDim = dim3(mlra::kG4Threads);

@@ -597,15 +597,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
 
     // ============================================================ epilogue: partials
-    // softmax sums: reduce this warp's 32 token lanes per head, then the 4 quarters in smem
+    // softmax sums: reduce this warp's 32 token lanes for all NB*kHG (branch, head) values at
+    // once by recursive halving (a lane keeps one half and receives the partner's other half:
+    // V/2 + V/4 + ... shuffles instead of 5*V), then the 4 quarters in smem.
+    {
+      constexpr int V = NB * kHG;
+      float vals[V];
 #pragma unroll
-    for (int bb = 0; bb < NB; ++bb) {
+      for (int i = 0; i < V; ++i) vals[i] = lsum[i / kHG][i % kHG];
+      int base = 0;  // original index of vals[0] on this lane
 #pragma unroll
-      for (int c = 0; c < kHG; ++c) {
-        float v = lsum[bb][c];
+      for (int k = 0; k < 5; ++k) {
+        const int o = 16 >> k;
+        const int live = V >> k;
+        if (live >= 2) {
+          const int half = live / 2;
+          const bool up = (lane & o) != 0;
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) lred[(bb * 4 + q) * NPAD + h_lo + c] = v;
+          for (int i = 0; i < half; ++i) {
+            const float send = up ? vals[i] : vals[i + half];
+            const float keep = up ? vals[i + half] : vals[i];
+            vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+          base += up ? half : 0;
+        } else {
+          vals[0] += __shfl_xor_sync(0xffffffffu, vals[0], o);
+        }
+      }
+      constexpr int kLive = (V >> 5) >= 1 ? (V >> 5) : 1;
+#pragma unroll
+      for (int i = 0; i < kLive; ++i) {
+        const int idx = base + i;
+        lred[((idx / kHG) * 4 + q) * NPAD + h_lo + idx % kHG] = vals[i];
       }
     }
     if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = clock64();
@@ -630,6 +653,32 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     named_bar_sync(1, kSoftThreads);
     const bool row_ok = (DLS == 128) || (lane < 16);
     const int row = (DLS == 128) ? q * 32 + lane : q * 16 + lane;
+    if constexpr (NB > 1) {
+      // one sub-block per branch (SUB = 1): every branch's TMEM load in flight, one wait
+      uint32_t raw[NB][kHG];
+      if (ntiles > 0) {
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          const uint32_t taddr = tbase + lane_off + O_COL + bb * NPAD + h_lo;
+          if constexpr (kHG == 8) {
+            tmem_ld8(taddr, raw[bb]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kHG; c += 16) tmem_ld16(taddr + c, raw[bb] + c);
+          }
+        }
+        tmem_ld_wait();
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          float* dst = p.o_part + ((part_row0 + bb) * p.H + hg * NPAD + h_lo) * size_t(DLAT) + row;
+#pragma unroll
+          for (int c = 0; c < kHG; ++c)
+            if (c < h_cnt) dst[size_t(c) * DLAT] = ntiles > 0 ? __uint_as_float(raw[bb][c]) * invl[bb * NPAD + h_lo + c] : 0.f;
+        }
+      }
+    } else
     for (int bb = 0; bb < NB; ++bb) {
       for (int sb = 0; sb < SUB; ++sb) {
         float o[kHG];

@@ -10,12 +10,15 @@ which = sys.argv[1]
 NB, DLAT = {"tp4": (1, 128), "tp1": (4, 128), "mla": (1, 512)}[which]
 B, H, DH, DR, L = 16, 24, 128, 64, 32768
 c = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128)
+c2 = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128, seed=1)  # the bench alternates two caches
 sub, dls = ops.latent_geometry(DLAT)
 nsplit = ops.default_splits(B, L, NB, sub)
 scale = ops.score_scale((DH + DR) ** -0.5)
 q_abs, q_rs = ops.absorb_query(c["q_nope"], c["q_rope"], c["w_uk"], NB, DLAT, scale)
 args = (q_abs, q_rs, c["pool"], c["bt"], c["seqlens"], c["page_size"], NB, sub, dls, nsplit)
 o = ops.decode_partials(*args)
+args2 = (q_abs, q_rs, c2["pool"], c2["bt"], c2["seqlens"], c2["page_size"], NB, sub, dls, nsplit)
+o2 = ops.decode_partials(*args2)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 def med(xs): return int(st.median(xs)) if xs else -1
 ctas = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 8, 40, 77, 100, 135, 143]
@@ -23,7 +26,7 @@ print("cta  dur_us  rounds period tma_lat  hold  soft  Pdone->PV  QK->S | start-
 for cta in ctas:
     os.environ["MLRA_DEBUG_TRACE_CTA"] = str(cta)
     for _ in range(3):
-        trace.zero_(); flush.zero_(); ops.decode_partials(*args, out=o)
+        trace.zero_(); ops.decode_partials(*args2, out=o2); ops.decode_partials(*args, out=o)
     torch.cuda.synchronize()
     tt = trace.cpu()
     t = tt[: 7 * 256].view(7, 256)
