@@ -80,28 +80,44 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
                   cudaStream_t stream) {
   using L = mlra::DecodeLayout<T, NPAD, DLS>;
   const int q_chunks = NB * p.SUB * (DLS / 64) + 1;
-  const int fixed = q_chunks * L::kQChunkBytes + 2 * L::kPBytes + L::kScratchBytes;
-  int rope_slots = 0, lat_slots = 0;
+  auto fixed = [&](int p_slots) { return q_chunks * L::kQChunkBytes + p_slots * L::kPBytes + L::kScratchBytes; };
+  auto fits = [&](int lat, int rope, int ps) { return L::smem_bytes(NB, p.SUB, lat, rope, ps) <= kSmemBudget; };
+  int rope_slots = 0, lat_slots = 0, p_slots = 2;
   if (GQA) {
     // K and V sub-blocks share one ring; no rope part
-    lat_slots = (kSmemBudget - fixed) / L::kLatBytes;
+    lat_slots = (kSmemBudget - fixed(2)) / L::kLatBytes;
     if (lat_slots < 3) return fail(MLRA_ERR_CONFIG, "gqa decode: ring of %d slots < 3", lat_slots);
+  } else if (NB > 1) {
+    // Several branches per tile share one rope tile (consumed by the tile's first QK): one
+    // rope slot suffices; latent depth is what keeps HBM busy (5 slots with a single P
+    // buffer beat 4 with two).
+    if (fits(5, 1, 1)) { lat_slots = 5; rope_slots = 1; p_slots = 1; }
+    else { rope_slots = 2; lat_slots = (kSmemBudget - fixed(2) - 2 * L::kRopeBytes) / L::kLatBytes; }
+  } else if (p.SUB == 1) {
+    // one branch: every round consumes a latent and a rope sub-block -> equal ring depths
+    for (int d = 6; d >= 2; --d)
+      if (fits(d, d, 2)) { lat_slots = rope_slots = d; break; }
   } else {
-    // Rope ring: up to 4 tiles deep for one-branch configs; shrink it before the latent ring.
-    rope_slots = (NB == 1 && p.SUB == 1) ? 4 : (T == 64 ? 3 : 2);
+    // multi-block latent (MLA, 64-token tiles): 2*SUB resident + 1 in flight at least
+    rope_slots = T == 64 ? 3 : 2;
     for (;; --rope_slots) {
-      lat_slots = (kSmemBudget - fixed - rope_slots * L::kRopeBytes) / L::kLatBytes;
+      lat_slots = (kSmemBudget - fixed(2) - rope_slots * L::kRopeBytes) / L::kLatBytes;
       if (lat_slots >= 2 * p.SUB + 2 || rope_slots == 2) break;
     }
-    // QK(r+1) is issued while PV(r) still holds its sub-blocks: 2*SUB resident + 1 in flight
-    if (lat_slots < 2 * p.SUB + 1)
-      return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
-                  2 * p.SUB + 1);
   }
+  if (!GQA && lat_slots < 2 * p.SUB + 1)
+    return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
+                2 * p.SUB + 1);
   if (lat_slots > mlra::kMaxLat) lat_slots = mlra::kMaxLat;
+  if (rope_slots > mlra::kMaxRope) rope_slots = mlra::kMaxRope;
+  if (const char* e = getenv("MLRA_DEBUG_RING")) {  // dev: "lat,rope,p"
+    int a = 0, b = 0, c = 0;
+    if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && fits(a, b, c)) { lat_slots = a; rope_slots = b; p_slots = c; }
+  }
   p.lat_slots = lat_slots;
   p.rope_slots = rope_slots;
-  const int smem = L::smem_bytes(NB, p.SUB, lat_slots, rope_slots);
+  p.p_slots = p_slots;
+  const int smem = L::smem_bytes(NB, p.SUB, lat_slots, rope_slots, p_slots);
   if (smem > kSmemBudget) return fail(MLRA_ERR_CONFIG, "decode: smem %d exceeds budget", smem);
   auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS, NB, GQA>;
   static unsigned attr_done = 0;  // per instantiation, one bit per device

@@ -47,6 +47,7 @@ struct DecodeParams {
   int B, H, SUB, DR, W;         // W = NB*SUB*DLS + DR (pool row width, elements)
   int page_size, max_pages, nsplit;
   int lat_slots, rope_slots;    // ring depths (set by the host from the smem budget)
+  int p_slots;                  // P buffers (1 or 2)
   int box_rows;                 // token rows per TMA box: T when pages hold whole tiles, else 64
   float rescale_threshold;      // lazy-rescale threshold (log2 units)
   long long* trace;             // debug: per-round clock64 events of CTA `trace_cta`, or null
@@ -78,14 +79,16 @@ struct DecodeLayout {
   static constexpr int kQChunkBytes = NPAD * 128;
   static constexpr int kPBytes = T * NPAD * 2;
   static constexpr int kPSbo = (T / 8) * 128;                 // MN-group stride of the P operand
-  // red[2][4][NPAD] + aw[8][NPAD] + m_run[8][4][NPAD] + lred[4][4][NPAD] + invl[4][NPAD]
-  static constexpr int kScratchFloats = 8 * NPAD + 8 * NPAD + 32 * NPAD + 16 * NPAD + 4 * NPAD;
+  // red[2][4][NPAD] + aw[8][NPAD] + m_run[8][4][NPAD]; the epilogue's lred[4][4][NPAD] and
+  // invl[4][NPAD] alias the P buffer (dead once the last PV has completed)
+  static constexpr int kScratchFloats = 8 * NPAD + 8 * NPAD + 32 * NPAD;
+  static_assert(20 * NPAD * 4 <= kPBytes, "epilogue scratch must fit in one P buffer");
   static constexpr int kBarOff = ((kScratchFloats * 4 + 127) / 128) * 128;
   static constexpr int kNumBars = 2 * kMaxLat + 2 * kMaxRope + 8 + 4 + 1 + 2;
   static constexpr int kScratchBytes = kBarOff + kNumBars * 8 + 8;
-  static int smem_bytes(int NB, int SUB, int lat_slots, int rope_slots) {
+  static int smem_bytes(int NB, int SUB, int lat_slots, int rope_slots, int p_slots) {
     const int q_chunks = NB * SUB * (DLS / 64) + 1;
-    return lat_slots * kLatBytes + rope_slots * kRopeBytes + q_chunks * kQChunkBytes + 2 * kPBytes +
+    return lat_slots * kLatBytes + rope_slots * kRopeBytes + q_chunks * kQChunkBytes + p_slots * kPBytes +
            kScratchBytes;
   }
 };
@@ -150,11 +153,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint8_t* q_smem = rope_ring + p.rope_slots * L::kRopeBytes;
   const int q_chunks = NB * SUB * (DLS / 64) + 1;
   uint8_t* p_smem = q_smem + q_chunks * L::kQChunkBytes;
-  uint8_t* scratch = p_smem + 2 * L::kPBytes;
+  uint8_t* scratch = p_smem + p.p_slots * L::kPBytes;
   float* red = reinterpret_cast<float*>(scratch);  // [2][4][NPAD] per-quarter tile maxima
   float* aw = red + 8 * NPAD;                      // [8][NPAD] per-softmax-warp rescale factor
   float* m_run = aw + 8 * NPAD;                    // [8][4][NPAD] per-softmax-warp running max per branch
-  float* lred = m_run + 32 * NPAD;                 // [4][4][NPAD] per-quarter softmax sums (epilogue)
+  float* lred = reinterpret_cast<float*>(p_smem);  // [4][4][NPAD] per-quarter softmax sums (epilogue)
   float* invl = lred + 16 * NPAD;                  // [4][NPAD]
   uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + L::kBarOff);
   uint64_t* lat_full = bars;
@@ -383,13 +386,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll 1
           for (int b = 0; b < NB; ++b) {
             const int r = t * NB + b;
-            const int pslot = r & 1;
+            const int pslot = r % p.p_slots;
             if constexpr (GQA) {
               // step over K_b (the QK warp's) to V_b, and wait for V_b itself
               if (++lslot == p.lat_slots) { lslot = 0; lphase ^= 1; }
               mbar_wait(&lat_full[lslot], lphase);
             }
-            mbar_wait(&p_full[pslot], (r >> 1) & 1);
+            mbar_wait(&p_full[pslot], (r / p.p_slots) & 1);
             if (lane == 0) trace_event(p.trace, p.trace_cta, 2, r);
             tc_fence_after();
             const uint64_t pb = pdesc + ((p_base + pslot * L::kPBytes) >> 4);
@@ -540,8 +543,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           rescale = t > 0;
         }
         // ---- probabilities (log2 domain; the score scale is folded into the queries)
-        const int pslot = r & 1;
-        if (r >= 2) mbar_wait(&p_empty[pslot], ((r >> 1) - 1) & 1);
+        const int pslot = r % p.p_slots;
+        if (r >= p.p_slots) mbar_wait(&p_empty[pslot], ((r / p.p_slots) - 1) & 1);
         if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 9, r);
         if (lane_ok) {
           uint8_t* prow = prow0 + pslot * L::kPBytes;
@@ -600,12 +603,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // softmax sums: reduce this warp's 32 token lanes for all NB*kHG (branch, head) values at
     // once by recursive halving (a lane keeps one half and receives the partner's other half:
     // V/2 + V/4 + ... shuffles instead of 5*V), then the 4 quarters in smem.
+    constexpr int V = NB * kHG;
+    float vals[V];
+    int base = 0;  // original index of vals[0] on this lane
     {
-      constexpr int V = NB * kHG;
-      float vals[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) vals[i] = lsum[i / kHG][i % kHG];
-      int base = 0;  // original index of vals[0] on this lane
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         const int o = 16 >> k;
@@ -624,17 +627,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           vals[0] += __shfl_xor_sync(0xffffffffu, vals[0], o);
         }
       }
+    }
+    if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = clock64();
+    if (ntiles > 0) {
+      mbar_wait(o_final, 0);  // every PV done: the P buffer (lred/invl) and TMEM O are final
+      tc_fence_after();
+    }
+    {
       constexpr int kLive = (V >> 5) >= 1 ? (V >> 5) : 1;
 #pragma unroll
       for (int i = 0; i < kLive; ++i) {
         const int idx = base + i;
         lred[((idx / kHG) * 4 + q) * NPAD + h_lo + idx % kHG] = vals[i];
       }
-    }
-    if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 3] = clock64();
-    if (ntiles > 0) {
-      mbar_wait(o_final, 0);
-      tc_fence_after();
     }
     named_bar_sync(1, kSoftThreads);
     if (p.trace != nullptr && tid == 64 && cta_lin < 1024 && true) p.trace[7 * 256 + 2048 + 8 * cta_lin + 4] = clock64();
