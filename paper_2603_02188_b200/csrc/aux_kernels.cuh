@@ -309,25 +309,29 @@ absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __
 //   w_k  = 2^(lse_k - max) / sum_j 2^(lse_j - max)  per (sequence, split);
 //   Z[c] = sum_k w_k O_k[c], thread = (latent c, sequence), all split loads in flight;
 //   y[d] = alpha * sum_c Z[c] W[c][d], thread = (column d, quarter of c), quarters added in smem.
-template <int SEQS>
+template <int SEQS, int THREADS = 256>
 inline size_t combine4_smem(int DLAT, int DH, int nsplit) {
-  return ((size_t(DLAT) * DH * 2 + 15) / 16) * 16 + size_t(DLAT) * SEQS * 4 + size_t(kG4Q) * SEQS * DH * 4 + 16;
+  return ((size_t(DLAT) * DH * 2 + 15) / 16) * 16 + size_t(DLAT) * SEQS * 4 + size_t(THREADS / kG4Cols) * SEQS * DH * 4 +
+         16;
 }
 
 constexpr int kMergeChunk = 12;  // split loads in flight per thread (B = 16 -> 9 splits: one pass)
 
-template <int SEQS>
-__global__ void __launch_bounds__(kG4Threads, 2)
+// 256 threads = 128 columns x 2 halves of the contraction: small enough that every CTA of
+// the TP1 grid (384) is resident at once (4 per SM).
+template <int SEQS, int THREADS = 256>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
                 int nsplit, float alpha, int per_branch, const int* __restrict__ done, int target) {
   static_assert(SEQS == 4 || SEQS == 8, "4 or 8 sequences per CTA");
+  constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
   const size_t wbytes = size_t(DLAT) * DH * 2;
   const __nv_bfloat16* wsm = reinterpret_cast<const __nv_bfloat16*>(c4_smem);  // [DLAT][DH]
   float* zs = reinterpret_cast<float*>(c4_smem + ((wbytes + 15) / 16) * 16);    // [DLAT][SEQS]
   float* ys = zs + DLAT * SEQS;                                                 // [Q][SEQS][DH]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ys + kG4Q * SEQS * DH);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ys + kQ * SEQS * DH);
   const int s0 = blockIdx.x * SEQS, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   MLRA_STAMP(0);
   if (tid == 0) {
@@ -356,7 +360,7 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
   // merge: thread = (latent column c, sequence); the split weights are computed by every
   // thread of a sequence redundantly (L2-resident lse loads) -- no extra barrier
-  for (int i = tid; i < DLAT * SEQS; i += kG4Threads) {
+  for (int i = tid; i < DLAT * SEQS; i += THREADS) {
     const int c = i / SEQS, sq = i % SEQS, s = s0 + sq;
     float z = 0.f;
     if (s < B) {
@@ -398,7 +402,7 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   MLRA_STAMP(3);
   const bool cluster_sum = NB > 1 && !per_branch;
   const int cq = tid / kG4Cols;
-  const int q_len = (DLAT + kG4Q - 1) / kG4Q, cr0 = cq * q_len, cr1 = min(DLAT, cr0 + q_len);
+  const int q_len = (DLAT + kQ - 1) / kQ, cr0 = cq * q_len, cr1 = min(DLAT, cr0 + q_len);
   for (int d0 = 0; d0 < DH; d0 += kG4Cols) {
     const int d = d0 + tid % kG4Cols;
     float acc[SEQS];
@@ -427,16 +431,16 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   }
   __syncthreads();
   // quarters -> ys[0] (scaled); thread = (sequence, column)
-  for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+  for (int i = tid; i < SEQS * DH; i += THREADS) {
     float v = ys[i];
 #pragma unroll
-    for (int q = 1; q < kG4Q; ++q) v += ys[q * SEQS * DH + i];
+    for (int q = 1; q < kQ; ++q) v += ys[q * SEQS * DH + i];
     ys[i] = v * alpha;
   }
   MLRA_STAMP(4);
   if (!cluster_sum) {
     __syncthreads();
-    for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+    for (int i = tid; i < SEQS * DH; i += THREADS) {
       const int s = s0 + i / DH, d = i % DH;
       if (s >= B) continue;
       if (per_branch) out[((size_t(s) * NB + b) * H + h) * DH + d] = ys[i];
@@ -448,7 +452,7 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     cluster_wait_acquire();
     if (b == 0) {
       const uint32_t ys_addr = smem_u32(ys);
-      for (int i = tid; i < SEQS * DH; i += kG4Threads) {
+      for (int i = tid; i < SEQS * DH; i += THREADS) {
         const int s = s0 + i / DH, d = i % DH;
         float tot = ys[i];
         for (int r = 1; r < NB; ++r) tot += ld_shared_cluster_f32(mapa_shared(ys_addr + i * 4, r));

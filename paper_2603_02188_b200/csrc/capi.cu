@@ -445,7 +445,7 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
     const int seqs = 4;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
-    cfg.blockDim = dim3(mlra::kG4Threads);
+    cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = c4smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];

@@ -72,7 +72,7 @@ int main() {
         timeit(nm, [&] {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
-          cfg.blockDim = dim3(kG4Threads);
+          cfg.blockDim = dim3(256);
           cfg.dynamicSmemBytes = cs;
           cfg.stream = cs0;
           cudaLaunchAttribute attr[1];
