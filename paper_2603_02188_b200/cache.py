@@ -185,6 +185,21 @@ class PagedCache:
         self.seqlens += 1
         self._host_lens = [n + 1 for n in self._host_lens]
 
+    def append_latent(self, kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos, *, branches: int, block0: int,
+                      nblocks: int, alpha_kv: float, rope_base: float = 10000.0) -> None:
+        """Fused K0 for one new token per sequence: kv_raw [B, d_c] / kr_raw [B, dr] fp32 raw
+        projections, rope_pos [B] absolute positions (host list or int32 device tensor)."""
+        lay = self.layout
+        if max(self._host_lens) >= self.capacity:
+            raise ConfigError(f"cache full: capacity {self.capacity} tokens per sequence")
+        pos = rope_pos if torch.is_tensor(rope_pos) else torch.tensor(list(rope_pos), dtype=torch.int32)
+        ops.cache_append_latent(kv_raw.float().contiguous(), kr_raw.float().contiguous(),
+                                pos.to(device=self.device, dtype=torch.int32), self.seqlens, self.block_table,
+                                self.pool, self.page_size, branches=branches, block0=block0, nblocks=nblocks,
+                                dlp=lay.dlp, drp=lay.drp, alpha_kv=alpha_kv, rope_base=rope_base)
+        self.seqlens += 1
+        self._host_lens = [n + 1 for n in self._host_lens]
+
     def fill(self, rows: torch.Tensor, lengths) -> None:
         """Bulk prefill: rows [B, n_max, W] bf16 (device); sequence s keeps its first lengths[s]."""
         lengths = [int(x) for x in lengths]
@@ -259,6 +274,15 @@ class PagedLatentCache:
         if self.n >= self.paged.capacity:
             self._grow()
         self.paged.append(row)
+
+    def append_latent(self, kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: int, *, branches: int,
+                      block0: int, nblocks: int, alpha_kv: float) -> None:
+        """Fused write side (K0): rmsnorm*alpha_kv of the raw down-projection [1, d_c], rope of the
+        raw rotary key [1, dr] at rope_pos, owned blocks + key appended as one row."""
+        if self.n >= self.paged.capacity:
+            self._grow()
+        self.paged.append_latent(kv_raw, kr_raw, [rope_pos], branches=branches, block0=block0, nblocks=nblocks,
+                                 alpha_kv=alpha_kv)
 
     def read(self, name: str) -> np.ndarray:
         """Debug copy of one stream as float64 [n, width], charging n*width reads."""

@@ -40,6 +40,63 @@ __global__ void cache_append_kernel(const __nv_bfloat16* __restrict__ rows, cons
     reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
 }
 
+// ----------------------------------------------------------------------------- K0 (fused write side)
+// attnkit/latent.py:129-159 (the cache half of latent_projections) + decode.py:129-150
+// (append_owned): from the token's raw down-projections
+//   c_kv = alpha_kv * rmsnorm(h W^DKV)            (latent.py:149, tensors.py:83-87, eps 1e-6)
+//   k_rope = rope(h W^KR, pos)                     (latent.py:140, rope.py:37-60: pairs (2l, 2l+1),
+//                                                   theta_l = base^(-2l/dr))
+// write the device's owned latent blocks (each zero-padded to dlp) and the rotary key (padded
+// to drp) as one bf16 pool row at the sequence's next slot. One CTA per sequence. The RMS needs
+// the whole c_kv row even when the device owns one block (TP4), so kv_raw is the full row.
+// Angles are formed in fp64 and reduced mod 2*pi before the fp32 sincos: at 128K positions an
+// fp32 angle would be off by ~1e-2 rad.
+constexpr int kK0Threads = 128;
+__global__ void __launch_bounds__(kK0Threads)
+cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __restrict__ kr_raw,
+                           const int32_t* __restrict__ rope_pos, const int32_t* __restrict__ slots,
+                           const int32_t* __restrict__ block_table, int d_c, int bs, int block0, int nblocks, int dlp,
+                           int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size, int max_pages,
+                           __nv_bfloat16* __restrict__ pool) {
+  __shared__ float red[kK0Threads / 32];
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const float* kv = kv_raw + size_t(s) * d_c;
+  float ss = 0.f;
+  for (int c = tid; c < d_c; c += kK0Threads) ss = fmaf(kv[c], kv[c], ss);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kK0Threads / 32; ++w) tot += red[w];
+  const float scale = alpha_kv * rsqrtf(tot / float(d_c) + eps);
+  const int slot = slots[s];
+  const int page = block_table[size_t(s) * max_pages + slot / page_size];
+  const int W = nblocks * dlp + drp;
+  __nv_bfloat16* dst = pool + (size_t(page) * page_size + slot % page_size) * W;
+  for (int i = tid; i < nblocks * dlp; i += kK0Threads) {
+    const int u = i / dlp, c = i % dlp;
+    const float v = c < bs ? kv[(block0 + u) * bs + c] * scale : 0.f;
+    dst[i] = __float2bfloat16(v);
+  }
+  const double pos = double(rope_pos[s]);
+  const float* kr = kr_raw + size_t(s) * dr;
+  for (int l = tid; l < drp / 2; l += kK0Threads) {
+    float e = 0.f, o = 0.f;
+    if (2 * l + 1 < dr) {
+      const double theta = pow(double(rope_base), -2.0 * l / dr);
+      const double ang = fmod(pos * theta, 6.283185307179586476925286766559);
+      float sn, cs;
+      sincosf(float(ang), &sn, &cs);
+      const float x0 = kr[2 * l], x1 = kr[2 * l + 1];
+      e = x0 * cs - x1 * sn;
+      o = x0 * sn + x1 * cs;
+    }
+    reinterpret_cast<__nv_bfloat162*>(dst + nblocks * dlp)[l] = __floats2bfloat162_rn(e, o);
+  }
+}
+
 // ----------------------------------------------------------------------------- per-head GEMM
 // Y[s, h, n] = scale * sum_k X[s, h, k] * W[h][k][n] for a batch of sequences, one weight
 // matrix per head. Used twice:

@@ -274,6 +274,26 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
   return cuda_check("absorb_query launch");
 }
 
+int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, const int32_t* slots,
+                             const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
+                             int dlp, int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size,
+                             int max_pages, void* pool, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (d_c <= 0 || branches <= 0 || d_c % branches != 0)
+    return fail(MLRA_ERR_SHAPE, "cache_append_latent: d_c=%d not split into %d branches", d_c, branches);
+  const int bs = d_c / branches;
+  if (block0 < 0 || nblocks < 1 || block0 + nblocks > branches || dlp < bs)
+    return fail(MLRA_ERR_CONFIG, "cache_append_latent: blocks [%d, %d) of %d (width %d, padded %d)", block0,
+                block0 + nblocks, branches, bs, dlp);
+  if (dr < 0 || dr % 2 != 0 || drp < dr || drp % 2 != 0)
+    return fail(MLRA_ERR_CONFIG, "cache_append_latent: rope width %d (padded %d) must be even", dr, drp);
+  if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append_latent: bad page geometry");
+  mlra::cache_append_latent_kernel<<<B, mlra::kK0Threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      kv_raw, kr_raw, rope_pos, slots, block_table, d_c, bs, block0, nblocks, dlp, dr, drp, alpha_kv, rope_base, eps,
+      page_size, max_pages, static_cast<__nv_bfloat16*>(pool));
+  return cuda_check("cache_append_latent launch");
+}
+
 int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
   return absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_out, B, H, DH, NB, DLAT, DR, score_scale, stream, nullptr, 0);

@@ -273,18 +273,25 @@ def _state(cfg: AttnConfig, w, device) -> _StepState:
     return st
 
 
-def _project_rows(cfg, st: _StepState, layout: RowLayout, h_t, pos: int, device):
-    hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=device)
-    positions = torch.tensor([pos], device=device)
-    q_nope, q_rope, k_rope, c_kv = st.projector(hidden, positions)
+def _owned_blocks(cfg: AttnConfig, layout: RowLayout) -> tuple[int, int, int]:
+    """(branches, first block, block count) of a latent layout's units, for the fused K0."""
     if cfg.variant == "mla":
-        lat = {"latent": c_kv[0]}
-    else:
-        bs = cfg.block_dim
-        lat = {f"latent_b{b}": c_kv[0, b * bs:(b + 1) * bs] for b in range(4)}
-    rows = {u: lat[u] for u in layout.units}
-    rows["rope"] = k_rope[0]
-    return rows, q_nope[0], q_rope[0]
+        return 1, 0, 1
+    blocks = [int(u.rsplit("_b", 1)[1]) for u in layout.units]
+    if blocks != list(range(blocks[0], blocks[0] + len(blocks))):
+        raise ConfigError(f"owned latent blocks {blocks} are not contiguous")
+    return 4, blocks[0], len(blocks)
+
+
+def append_token_latent(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, hidden: torch.Tensor,
+                        pos: int) -> None:
+    """Write side of one decode step for a latent-family cache: the raw down-projections
+    (h W^DKV, h W^KR -- pre-attention GEMVs, torch) then the fused K0 kernel (rmsnorm*alpha_kv,
+    owned blocks, rope, padding, paged append)."""
+    branches, block0, nblocks = _owned_blocks(cfg, cache.layout)
+    proj = st.projector
+    cache.append_latent(hidden @ proj.w_dkv, hidden @ proj.w_kr, pos, branches=branches, block0=block0,
+                        nblocks=nblocks, alpha_kv=proj.alpha_kv)
 
 
 def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tuple[np.ndarray, PagedLatentCache]:
@@ -301,9 +308,10 @@ def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tu
         contribs = attend_local(cfg, {}, st.own, cache, {"q": q[0]})
         out, _ = reduce_contributions(cfg, contribs)
         return out, cache
-    rows, q_nope, q_rope = _project_rows(cfg, st, cache.layout, h_t, pos, dev)
-    cache.append_packed(cache.layout.pack_rows(rows, device=dev)[None])
-    qn, qr = _queries_to_device(cfg, cache.layout, q_nope, q_rope, list(range(cfg.h)), dev)
+    hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
+    append_token_latent(cfg, st, cache, hidden, pos)
+    q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
+    qn, qr = _queries_to_device(cfg, cache.layout, q_nope[0], q_rope[0], list(range(cfg.h)), dev)
     alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
     out = _run_units(cfg, cache, st.lw, qn, qr, upproj=1, alpha=alpha)
     cache.reads += cache.n * cache.row_elements()

@@ -55,6 +55,29 @@ def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch
     _lib.check(rc, "mlra_cache_append")
 
 
+def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor, slots: torch.Tensor,
+                        block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
+                        nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
+                        eps: float = 1e-6) -> None:
+    """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
+    rope_pos, padded, appended as one bf16 pool row per sequence at slots[s]."""
+    _need(kv_raw, torch.float32, "kv_raw", 2)
+    _need(kr_raw, torch.float32, "kr_raw", 2)
+    _need(rope_pos, torch.int32, "rope_pos", 1)
+    _need(slots, torch.int32, "slots", 1)
+    _need(block_table, torch.int32, "block_table", 2)
+    _need(pool, torch.bfloat16, "pool", 2)
+    B, d_c = kv_raw.shape
+    dr = kr_raw.shape[1]
+    if pool.shape[1] != nblocks * dlp + drp:
+        raise ShapeMismatchError(f"cache_append_latent: pool width {pool.shape[1]} != {nblocks * dlp + drp}")
+    rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(), rope_pos.data_ptr(),
+                                              slots.data_ptr(), block_table.data_ptr(), B, d_c, branches, block0,
+                                              nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
+                                              page_size, block_table.shape[1], pool.data_ptr(), _stream())
+    _lib.check(rc, "mlra_cache_append_latent")
+
+
 def absorb_query(q_nope: torch.Tensor, q_rope: torch.Tensor, w_uk_packed: torch.Tensor, nb: int, dlat: int,
                  score_scale: float, out: tuple[torch.Tensor, torch.Tensor] | None = None):
     """K1: q_abs [B, NB, H, DLAT] and scaled q_rope [B, H, DR] (both bf16)."""

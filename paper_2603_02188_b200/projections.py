@@ -46,6 +46,15 @@ class LatentProjector:
         sf = calib_factors(cfg)
         self.alpha_q, self.alpha_kv = sf.alpha_q, sf.alpha_kv
 
+    def queries(self, hidden: torch.Tensor, positions: torch.Tensor):
+        """hidden [n, d] fp32 -> q_nope [n,h,d_h], q_rope [n,h,dr] (latent.py:134-139)."""
+        cfg = self.cfg
+        n = hidden.shape[0]
+        c_q = self.alpha_q * rmsnorm(hidden @ self.w_dq)
+        q_nope = (c_q @ self.w_uq).reshape(n, cfg.h, cfg.d_h)
+        q_rope = rope_rotate((c_q @ self.w_qr).reshape(n, cfg.h, cfg.d_h_rope), positions)
+        return q_nope, q_rope
+
     def __call__(self, hidden: torch.Tensor, positions: torch.Tensor):
         """hidden [n, d] fp32 -> q_nope [n,h,d_h], q_rope [n,h,dr], k_rope [n,dr], c_kv [n,d_c]."""
         cfg = self.cfg

@@ -28,8 +28,8 @@ from fractions import Fraction
 import numpy as np
 
 from .config import TP_DEGREES, AttnConfig
-from .decode import (LatentUnit, Ownership, _check_served, attend_local, local_weights, new_cache,
-                     reduce_contributions, _project_rows, _state)
+from .decode import (LatentUnit, Ownership, _check_served, append_token_latent, attend_local, local_weights,
+                     new_cache, reduce_contributions, _state)
 from .errors import ConfigError, IntegrityError
 
 
@@ -172,8 +172,9 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
     st = _state(cfg, w, dev)
     before = [s.cache.reads for s in shards.shards]
     by_device: dict = {}
+    import torch
+
     if cfg.variant == "gqa":
-        import torch
 
         hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
         q, k, v = st.projector(hidden, torch.tensor([pos], device=dev))
@@ -186,9 +187,11 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
             by_device[shard.device_id] = attend_local(cfg, {}, shard.own, shard.cache,
                                                       {"q": q[0].double().cpu().numpy()})
             continue
-        rows, q_nope, q_rope = _project_rows(cfg, st, shard.cache.layout, h_t, pos, dev)
-        shard.cache.append_packed(shard.cache.layout.pack_rows(rows, device=dev)[None])
-        queries = {"q_nope": q_nope.double().cpu().numpy(), "q_rope": q_rope.double().cpu().numpy()}
+        hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32,
+                                 device=dev)
+        append_token_latent(cfg, st, shard.cache, hidden, pos)  # fused K0 (owned blocks)
+        q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
+        queries = {"q_nope": q_nope[0].double().cpu().numpy(), "q_rope": q_rope[0].double().cpu().numpy()}
         by_device[shard.device_id] = attend_local(cfg, shard.attn_weights, shard.own, shard.cache, queries)
     contribs = [c for did in sorted(by_device) for c in by_device[did]]
     out, kind = reduce_contributions(cfg, contribs)

@@ -1,0 +1,72 @@
+"""GPU parity of the fused write side (K0: rmsnorm * alpha_kv + block split + RoPE + paged
+append, mlra_cache_append_latent) against the oracle's latent_projections
+(attnkit/latent.py:129-159), including RoPE at 128K-scale positions, a TP4 shard's single
+block, and MLA's undivided latent. Rows are stored in bf16: gate = bf16 rounding of the
+oracle's float64 row (relative 2^-8 of the row's max)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attnkit_port as ak
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(variant, own_blocks, positions):
+    import paper_2603_02188_b200 as mlra
+    from paper_2603_02188_b200.cache import PagedCache
+    from paper_2603_02188_b200.decode import _owned_blocks, full_ownership, row_layout
+    from paper_2603_02188_b200.tp import shard_ownership
+
+    cfg = mlra.trained_config("mla" if variant == "mla" else "mlra4").with_(d=512)
+    ocfg = ak.cfg_from(cfg)
+    w = ak.build_weights(ocfg, 0.02, 3, ("k0",))
+    own = full_ownership(cfg) if own_blocks is None else shard_ownership(cfg, 4, own_blocks)
+    lay = row_layout(cfg, own)
+    B = len(positions)
+    hidden = ak.normal(3, ("k0-h",), (B, cfg.d))
+    dev = torch.device("cuda", 0)
+    cache = PagedCache(lay, B, 256, 64, dev)
+    h = torch.tensor(hidden, dtype=torch.float32, device=dev)
+    branches, block0, nblocks = _owned_blocks(cfg, lay)
+    alpha_kv = ak.calib_alphas(ocfg)[1]
+    kv_raw = torch.tensor(hidden @ w["w_dkv"], dtype=torch.float32, device=dev)
+    kr_raw = torch.tensor(hidden @ w["w_kr"], dtype=torch.float32, device=dev)
+    cache.append_latent(kv_raw, kr_raw, positions, branches=branches, block0=block0, nblocks=nblocks,
+                        alpha_kv=alpha_kv)
+    torch.cuda.synchronize()
+    del h
+    for s, pos in enumerate(positions):
+        _, _, k_rope, lats = ak.latent_projections(ocfg, w, hidden[s:s + 1], [pos])
+        row = cache.pool[cache.token_slots(s)][0]
+        for name in list(lay.units) + ["rope"]:
+            want = (k_rope if name == "rope" else lats[name])[0]
+            got = lay.extract(name, row[None]).double().cpu().numpy()[0]
+            err = np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30)
+            assert err <= 2 ** -7, f"{variant} seq {s} pos {pos} stream {name}: rel err {err:.3e}"
+        pad = row[lay.width - lay.drp + lay.dr:]
+        assert float(pad.abs().max() if pad.numel() else 0.0) == 0.0
+
+
+@pytest.mark.parametrize("variant,blocks", [("mlra", None), ("mlra", 2), ("mla", None)])
+def test_fused_append_matches_oracle(variant, blocks):
+    _check(variant, blocks, [0, 1, 17, 4095, 65537, 131071])
+
+
+def test_fused_append_through_drop_in_step_tracks_packed_rows():
+    """absorbed_decode_step appends through the fused K0: the stored rows equal the oracle's
+    latent streams (bf16) token by token."""
+    import paper_2603_02188_b200 as mlra
+
+    cfg = mlra.tiny_config()
+    ocfg = ak.cfg_from(cfg)
+    w = ak.build_weights(ocfg, 0.3, 5, ("k0s",))
+    hidden = ak.normal(5, ("k0s-h",), (20, cfg.d))
+    cache = mlra.new_cache(cfg, pos_offset=1000)
+    for t in range(20):
+        mlra.absorbed_decode_step(cfg, w, cache, hidden[t])
+    streams = ak.latent_streams(ocfg, w, hidden, pos_offset=1000)
+    for name, want in streams.items():
+        got = cache.peek(name)
+        assert np.max(np.abs(got - want)) <= 2 ** -7 * np.max(np.abs(want)), name
