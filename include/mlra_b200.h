@@ -82,8 +82,8 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream);
 
 /* Bytes of device workspace mlra_decode_step needs (split-KV partials, absorbed queries,
- * merge scratch and per-sequence barrier state). Zero-initialise it once before first use;
- * the barrier state is self-resetting afterwards. */
+ * merge scratch and per-sequence completion counters). Zero-initialise it once before first
+ * use; K1 resets the counters every step afterwards. */
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit);
 
 /* Split count used when the caller passes nsplit <= 0 (fills the SMs for this batch). */
@@ -121,13 +121,12 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.
  * Replaces decode.py:304-305 (attend_local + reduce_contributions inside
  * absorbed_decode_step) for every unit a device owns.
- * Default: K1, K2, K3 launched in turn on `stream`. Opt-in (environment MLRA_FUSED=1, and
- * B * nsplit * head_groups <= SM count): ONE cooperative launch in which the query
- * absorption (split over all CTAs of a head group, behind a group barrier) and the split
- * merge + up-projection (behind a per-sequence barrier) run inside the decode kernel; the
- * barriers are self-resetting, so the workspace is zeroed once. Same results up to
- * reduction order; slower on B200 for MLRA-4 (profiles/ROUND1.md).
+ * K1, K2, K3 are launched in turn on `stream`; K2 and K3 with programmatic dependent launch
+ * (K2's TMA producer streams the cache while K1 drains; K3 loads W^UV early and waits only
+ * for the K2 CTAs of its own sequences through per-sequence counters in the workspace, which
+ * K1 resets every step). Environment MLRA_NO_PDL=1 falls back to plain stream order.
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
+ *   nsplit in [1, 160] (mlra_default_splits: one wave of the SMs for this batch)
  */
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
                      const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,

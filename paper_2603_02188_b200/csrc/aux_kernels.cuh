@@ -201,7 +201,7 @@ inline size_t head_gemm_smem(int kp) {
 // One warp per row: lane k < nsplit computes split k's weight once (shuffled to all
 // lanes), then every lane sums its latent columns over the splits with independent loads.
 // Output [B, H, NB*DLAT] (the K3b input) or, with zout_bnh, [B, NB, H, DLAT] * alpha.
-constexpr int kMergeMaxSplits = 64;
+constexpr int kMergeMaxSplits = 160;  // 5 per lane
 __global__ void merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                     float* __restrict__ z, int B, int NB, int H, int DLAT, int nsplit, float alpha,
                                     int zout_bnh) {
@@ -210,19 +210,19 @@ __global__ void merge_splits_kernel(const float* __restrict__ o_part, const floa
   if (row >= B * NB * H) return;
   const int h = row % H, b = (row / H) % NB, s = row / (H * NB);
   const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
-  float lk[2];
+  float lk[kMergeMaxSplits / 32];
   float m = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
     const int k = lane + 32 * j;
     lk[j] = k < nsplit ? l[size_t(k) * NB * H] : -INFINITY;
     m = fmaxf(m, lk[j]);
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  float wk[2], tot = 0.f;
+  float wk[kMergeMaxSplits / 32], tot = 0.f;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
     wk[j] = (m == -INFINITY || lk[j] == -INFINITY) ? 0.f : exp2f(lk[j] - m);
     tot += wk[j];
   }
@@ -274,12 +274,9 @@ inline size_t absorb4_smem() {
 __global__ void __launch_bounds__(kG4Threads)
 absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __restrict__ w_uk,
                __nv_bfloat16* __restrict__ q_abs, int B, int H, int DH, int NB, int DLAT, float scale,
-               const __nv_bfloat16* __restrict__ rope_in, __nv_bfloat16* __restrict__ rope_out, int DR,
-               int* __restrict__ zero, int nzero) {
+               const __nv_bfloat16* __restrict__ rope_in, __nv_bfloat16* __restrict__ rope_out, int DR) {
   griddep_launch_dependents();
   extern __shared__ __align__(16) uint8_t g4_smem[];
-  if (zero != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-    for (int i = threadIdx.x; i < nzero; i += kG4Threads) zero[i] = 0;  // the step's K2 completion counters
   __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(g4_smem);                      // [KC][128]
   float4* xs = reinterpret_cast<float4*>(g4_smem + size_t(kG4KChunk) * kG4Cols * 2);  // [KC] x 4 seqs
   float* red = reinterpret_cast<float*>(xs + kG4KChunk);                              // [Q][4][128]
@@ -380,7 +377,7 @@ template <int SEQS, int THREADS = 256>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
-                int nsplit, float alpha, int per_branch, const int* __restrict__ done, int target) {
+                int nsplit, float alpha, int per_branch) {
   static_assert(SEQS == 4 || SEQS == 8, "4 or 8 sequences per CTA");
   constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
@@ -402,17 +399,7 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     for (size_t off = 0; off < wbytes; off += 32768)
       bulk_copy_g2s(c4_smem + off, src + off, uint32_t(wbytes - off < 32768 ? wbytes - off : 32768), bar);
   }
-  if (done == nullptr) {
-    griddep_wait();  // partials of K2 (the whole grid)
-  } else {
-    // only this CTA's sequences: every K2 CTA of sequence s adds 1 to done[s] once its
-    // partials are globally visible (fence + atomic); acquire loads pair with it
-    if (tid < SEQS && s0 + tid < B) {
-      const int* f = done + s0 + tid;
-      while (ld_acquire_gpu(f) < target) __nanosleep(128);
-    }
-    __syncthreads();
-  }
+  griddep_wait();  // partials of K2 (a no-op in plain stream order)
   MLRA_STAMP(1);
   const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
   // merge: thread = (latent column c, sequence); the split weights are computed by every

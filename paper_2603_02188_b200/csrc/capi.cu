@@ -233,9 +233,8 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_
   return cuda_check("cache_append launch");
 }
 
-// K1; `zero` (nullable) = nzero per-sequence completion counters of the step to reset.
 static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
-                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream, int* zero, int nzero) {
+                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
   if (B <= 0) return MLRA_OK;
   if (H <= 0 || DH <= 0 || NB <= 0 || DLAT <= 0 || DLAT % 2 != 0 || DR < 0)
     return fail(MLRA_ERR_SHAPE, "absorb_query: bad dims H=%d DH=%d NB=%d DLAT=%d DR=%d", H, DH, NB, DLAT, DR);
@@ -255,8 +254,6 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
                                                 static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
                                                 score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
                                                 DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
-    if (zero != nullptr && cudaMemsetAsync(zero, 0, size_t(nzero) * sizeof(int), st) != cudaSuccess)
-      return cuda_check("absorb_query counter reset");
     return cuda_check("absorb_query launch");
   }
   if ((reinterpret_cast<uintptr_t>(w_uk) & 15) != 0)
@@ -269,7 +266,7 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
                 static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(w_uk),
                 static_cast<__nv_bfloat16*>(q_abs), B, H, DH, NB, DLAT, score_scale,
                 static_cast<const __nv_bfloat16*>(q_rope), DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr,
-                DR, zero, nzero) != cudaSuccess)
+                DR) != cudaSuccess)
     return cuda_check("absorb_query launch");
   return cuda_check("absorb_query launch");
 }
@@ -296,14 +293,14 @@ int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int
 
 int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream) {
-  return absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_out, B, H, DH, NB, DLAT, DR, score_scale, stream, nullptr, 0);
+  return absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_out, B, H, DH, NB, DLAT, DR, score_scale, stream);
 }
 
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
          al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4) +
-         al(size_t(B) * NB * H * DLAT * 4) + al(size_t(B) * sizeof(int));
+         al(size_t(B) * NB * H * DLAT * 4);
 }
 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
@@ -314,33 +311,33 @@ int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
   int s = sms / B;  // one wave of CTAs (1 CTA / SM); a partial second wave costs a full round
   if (s < 1) s = 1;
   if (s > tiles) s = tiles;
-  if (s > 64) s = 64;
+  if (s > mlra::kMergeMaxSplits) s = mlra::kMergeMaxSplits;
   return s < 1 ? 1 : s;
 }
 
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       int* done, bool pdl = false);
+                       bool pdl = false);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
                          int DLS, int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream) {
   return decode_impl(q_abs, q_rope, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
-                     max_pages, num_pages, nsplit, stream, nullptr, false);
+                     max_pages, num_pages, nsplit, stream, false);
 }
 
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       int* done, bool pdl) {
+                       bool pdl) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
   if (DLS != 64 && DLS != 128) return fail(MLRA_ERR_CONFIG, "decode: sub-block width %d not in {64,128}", DLS);
   if (DR < 16 || DR > 64 || DR % 16 != 0) return fail(MLRA_ERR_CONFIG, "decode: rope width %d not in {16..64}/16", DR);
   if (page_size <= 0 || page_size % 64 != 0) return fail(MLRA_ERR_CONFIG, "decode: page_size %d not a multiple of 64", page_size);
-  if (nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "decode: nsplit %d not in [1,64]", nsplit);
+  if (nsplit < 1 || nsplit > mlra::kMergeMaxSplits) return fail(MLRA_ERR_CONFIG, "decode: nsplit %d not in [1,%d]", nsplit, mlra::kMergeMaxSplits);
   if (H < 1) return fail(MLRA_ERR_SHAPE, "decode: H=%d", H);
   if (NB == 3) return fail(MLRA_ERR_CONFIG, "decode: NB=3 branches per device is not a TP layout");
   if (SUB > 1 && NB != 1) return fail(MLRA_ERR_CONFIG, "decode: multi-block latents (SUB>1) need NB=1");
@@ -364,7 +361,6 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
   p.pdl = pdl ? 1 : 0;
-  p.done = done;
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
   if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
@@ -408,7 +404,7 @@ static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block
   if (R < 1 || R > 16) return fail(MLRA_ERR_CONFIG, "gqa decode: %d query heads per KV head not in [1,16]", R);
   if (DH != 64 && DH != 128) return fail(MLRA_ERR_CONFIG, "gqa decode: padded head width %d not in {64,128}", DH);
   if (page_size <= 0 || page_size % 64 != 0) return fail(MLRA_ERR_CONFIG, "gqa decode: page_size %d not a multiple of 64", page_size);
-  if (nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "gqa decode: nsplit %d not in [1,64]", nsplit);
+  if (nsplit < 1 || nsplit > mlra::kMergeMaxSplits) return fail(MLRA_ERR_CONFIG, "gqa decode: nsplit %d not in [1,%d]", nsplit, mlra::kMergeMaxSplits);
   const int W = 2 * G * DH;
   const int T = 128;
   const int box_rows = (page_size % T == 0) ? T : 64;
@@ -445,11 +441,9 @@ static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block
 // K3 needs a [B, H, NB*DLAT] fp32 scratch for the merged latent when it up-projects; the
 // standalone entry point allocates it from a per-thread cache (mlra_decode_step passes the
 // workspace slice instead).
-// K3. With `done` (mlra_decode_step) each CTA waits for the completion counters of its own
-// sequences (target = K2 CTAs per sequence) instead of for the whole K2 grid.
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
                         int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                        bool pdl = false, const int* done = nullptr, int target = 0) {
+                        bool pdl = false) {
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
   const size_t c4smem = mlra::combine4_smem<4>(DLAT, DH, nsplit);
@@ -478,7 +472,7 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha, per_branch, done, target) != cudaSuccess)
+                           DH, nsplit, alpha, per_branch) != cudaSuccess)
       return cuda_check("combine launch");
     return cuda_check("combine launch");
   }
@@ -511,7 +505,7 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
 int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
                  int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
   if (B <= 0) return MLRA_OK;
-  if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > 64) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
+  if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > mlra::kMergeMaxSplits) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
   if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
   if (upproj && (DH % 8 != 0)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not a multiple of 8", DH);
   if (upproj && scratch == nullptr) return fail(MLRA_ERR_CONFIG, "combine: up-projection needs a scratch buffer");
@@ -536,25 +530,18 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
   float* lse_part = reinterpret_cast<float*>(ws);
   ws += al(size_t(B) * nsplit * NB * H * 4);
   float* zbuf = reinterpret_cast<float*>(ws);
-  ws += al(size_t(B) * NB * H * DLAT * 4);
-  int* done = reinterpret_cast<int*>(ws);  // [B] per-sequence K2 completion counters
-  // K2 CTAs per sequence (every head group counts)
-  const int npad = pick_npad(H, NB, SUB);
-  const int hgroups = (H + npad - 1) / npad;
-  // K1 resets the counters; K2 and K3 are chained with programmatic dependent launch: K2's
-  // TMA producer streams the cache while K1 drains (the cache was written before K1 started)
-  // and waits on K1 only before reading the queries; K3's CTAs load W^UV as soon as they are
-  // resident and then wait only for the K2 CTAs of their own sequences (the counters), so
-  // the merge of early-finishing sequences overlaps K2's tail.
+  // K1 then K2 with programmatic dependent launch (K2's TMA producer streams the cache while
+  // K1 drains -- the cache was written before K1 started -- and waits on K1 only before
+  // reading the queries), then K3 in plain stream order. (K3 launched dependent on K2 measured
+  // 5-30 us slower per step: its early CTAs cost more than the overlap gains.)
   const bool pdl = getenv("MLRA_NO_PDL") == nullptr;
-  int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream,
-                       pdl ? done : nullptr, B);
+  int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
   if (rc) return rc;
   rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
-                   max_pages, num_pages, nsplit, stream, pdl ? done : nullptr, pdl);
+                   max_pages, num_pages, nsplit, stream, pdl);
   if (rc) return rc;
   return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
-                      static_cast<cudaStream_t>(stream), pdl, pdl ? done : nullptr, nsplit * hgroups);
+                      static_cast<cudaStream_t>(stream), false);
 }
 
 int mlra_gqa_default_splits(int B, int G, int max_seqlen) {
@@ -565,7 +552,7 @@ int mlra_gqa_default_splits(int B, int G, int max_seqlen) {
   const int tiles = (max_seqlen + 127) / 128;
   int s = sms / (B * z);
   if (s > tiles) s = tiles;
-  if (s > 64) s = 64;
+  if (s > mlra::kMergeMaxSplits) s = mlra::kMergeMaxSplits;
   return s < 1 ? 1 : s;
 }
 

@@ -52,8 +52,6 @@ struct DecodeParams {
   float rescale_threshold;      // lazy-rescale threshold (log2 units)
   long long* trace;             // debug: per-round clock64 events of CTA `trace_cta`, or null
   int trace_cta;                // debug: linear CTA index traced (x fastest)
-  int* done;                    // [B] per-sequence completion counters (or null): every CTA adds 1
-                                // after its partials are globally visible; K3 waits on them
   // ---- GQA comparison variant (template GQA = true) ------------------------------------------
   // Pool row [K_0 | ... | K_{G-1} | V_0 | ... | V_{G-1}] (each DLS wide, post-RoPE keys), no
   // rope part (DR = 0). "Branch" = KV head: blockIdx.z selects NB of the nb_total KV heads,
@@ -175,7 +173,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  griddep_launch_dependents();  // K3 (PDL) may launch; it waits for this grid before reading
+  griddep_launch_dependents();  // a dependent launch may start its prologue
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
     p.trace[13824 + 2 * cta_lin] = clock64();
@@ -712,12 +710,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
     }
     if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 5] = clock64();
-    // ---- completion: partials of this CTA globally visible -> count it for its sequence
-    if (p.done != nullptr) {
-      __threadfence();
-      named_bar_sync(1, kSoftThreads);
-      if (ws == 0 && lane == 0) atomicAdd(p.done + seq, 1);
-    }
   }
   tc_fence_before();
   if (p.trace != nullptr && warp >= 2) atomicAdd(&tmem_base_sh[1], 1u);

@@ -267,11 +267,11 @@ def test_kimi_64_heads_tp4():
 
 
 @pytest.mark.parametrize("variant", ["mlra", "mla"])
-def test_counter_chained_step_matches_stream_ordered_step(variant, monkeypatch):
-    """By default K3's CTAs wait on per-sequence K2 completion counters (reset by K1) instead
-    of on the whole K2 grid. Repeated steps and CUDA-graph replays must reproduce the plain
-    stream-ordered step (MLRA_NO_PDL=1) exactly -- same kernels, same reduction order --
-    for ragged lengths and both variants."""
+def test_pdl_chained_step_matches_stream_ordered_step(variant, monkeypatch):
+    """By default K2 is launched dependent on K1 (programmatic dependent launch: its TMA
+    producer streams the cache while K1 drains). Repeated steps and CUDA-graph replays must
+    reproduce the plain stream-ordered step (MLRA_NO_PDL=1) exactly -- same kernels, same
+    reduction order -- for ragged lengths and both variants."""
     import torch
 
     mlra = _mlra()
@@ -294,7 +294,7 @@ def test_counter_chained_step_matches_stream_ordered_step(variant, monkeypatch):
     for _ in range(3):
         got = _run(eng, qns, qrs)
         assert np.array_equal(base, got)
-    # graph replay: the counter reset and the waits live inside the captured step
+    # graph replay of the PDL-chained step
     qn_t, qr_t = eng.prepare_queries(torch.tensor(np.stack(qns)), torch.tensor(np.stack(qrs)))
     out = eng.decode_attention(qn_t, qr_t)
     torch.cuda.synchronize()

@@ -22,17 +22,19 @@ def gtime(fn, iters=50):
     return e0.elapsed_time(e1) / iters / 10 * 1e3
 
 dev = torch.device("cuda", 0)
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+CTX = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
 cases = [("mlra4 tp1", trained_config("mlra4"), None), ("mlra4 tp4 rank", trained_config("mlra4"), shard_ownership(trained_config("mlra4"), 4, 0)),
          ("mla tp4 rank", trained_config("mla"), shard_ownership(trained_config("mla"), 4, 0))]
 for name, cfg, own in cases:
-    eng, qn, qr = bench.make_engine(cfg, own, 16, 32768, 1, dev)
+    eng, qn, qr = bench.make_engine(cfg, own, B, CTX, 1, dev)
     c = eng.cache
     q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale)
     parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub, eng.dls, eng.nsplit)
     out = ops.combine(*parts, eng.w_uv, eng.alpha)
-    scratch = torch.empty((16, len(eng.heads), eng.layout.nb * eng.layout.dlp), dtype=torch.float32, device=dev)
+    scratch = torch.empty((B, len(eng.heads), eng.layout.nb * eng.layout.dlp), dtype=torch.float32, device=dev)
     t1 = gtime(lambda: ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale, out=(q_abs, q_rs)))
     t2 = gtime(lambda: ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub, eng.dls, eng.nsplit, out=parts))
     t3 = gtime(lambda: ops.combine(*parts, eng.w_uv, eng.alpha, out=out, scratch=scratch))
     tstep = gtime(lambda: eng.decode_attention(qn, qr))
-    print(f"{name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  step {tstep:.1f} us  (graph replay, K2 back-to-back on one cache: L2-warm)", flush=True)
+    print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  step {tstep:.1f} us  (graph replay, K2 back-to-back on one cache: L2-warm)", flush=True)

@@ -60,7 +60,7 @@ int main() {
     snprintf(nm, sizeof nm, "absorb4 NB=%d grid(%d,%d,%d)", NB, (NCOL + 127) / 128, H, (B + 3) / 4);
     timeit(nm, [&] {
       absorb4_kernel<<<dim3((NCOL + 127) / 128, H, (B + 3) / 4), kG4Threads, absorb4_smem(), cs0>>>(qn, wuk, qabs, B, H, DH,
-                                                                                                  NB, DLAT, 1.f, qr, qrs, DR, nullptr, 0);
+                                                                                                  NB, DLAT, 1.f, qr, qrs, DR);
     });
     for (int seqs : {4, 8}) {
       auto kern = seqs == 4 ? combine4_kernel<4> : combine4_kernel<8>;
@@ -83,7 +83,7 @@ int main() {
           cfg.attrs = attr;
           cfg.numAttrs = 1;
           cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB,
-                             DLAT, DH, nsplit, 0.5f, cl ? 0 : 1, nullptr, 0);
+                             DLAT, DH, nsplit, 0.5f, cl ? 0 : 1);
         });
       }
     }
