@@ -510,4 +510,159 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   MLRA_STAMP(5);
 }
 
+// ----------------------------------------------------------------------------- K3 (split-K, cluster)
+// K3 for the summed output, with the split merge spread over a thread-block cluster:
+// grid (ceil(B/4), H, KP), cluster (1, 1, KP), 256 threads. CTA (sequence group, head h, kp):
+//   1. cp.async its slice of W^UV_b[h] for every branch b: rows [NB*DLAT], output columns
+//      [kp*DH/KP, (kp+1)*DH/KP)  (kp owns those output columns);
+//   2. merges splits [kp*nsplit/KP, (kp+1)*nsplit/KP) of all (sequence, branch, latent)
+//      items into an unnormalised partial (local max m, sum l, mixture z) in its smem;
+//   3. cluster barrier; reads the KP partials through DSMEM and forms the final merged
+//      latent Z = sum_kp z_kp 2^(m_kp - M) / sum_kp l_kp 2^(m_kp - M) for every item;
+//   4. cluster barrier (remote reads done); y[s, d] = alpha * sum_b sum_c Z[s,b,c] W_b[c, d]
+//      for its columns, branches summed in ascending order inside the CTA (deterministic).
+// The per-thread merge loop is nsplit/KP long instead of nsplit (small batches run up to
+// 148 splits), and KP x more CTAs share the work.
+constexpr int kSkThreads = 256;
+template <int KP>
+inline size_t combine_splitk_smem(int NB, int DLAT, int DH) {
+  const size_t rows = size_t(NB) * DLAT;
+  return rows * (DH / KP) * 2            // W slice
+         + size_t(4) * rows * 4          // this CTA's partial z [4][NB*DLAT]
+         + size_t(4) * NB * 2 * 4        // its (m, l) [4][NB]
+         + rows * 16                     // merged Z [NB*DLAT][4]
+         + size_t(4) * kSkThreads * 4;   // GEMV reduction [256/DSL][4][DSL]
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kSkThreads)
+combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
+                      const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT,
+                      int DH, int nsplit, float alpha) {
+  extern __shared__ __align__(128) uint8_t sk_smem[];
+  const int rows = NB * DLAT, DSL = DH / KP;
+  __nv_bfloat16* wsl = reinterpret_cast<__nv_bfloat16*>(sk_smem);  // [rows][DSL]
+  float* pz = reinterpret_cast<float*>(wsl + size_t(rows) * DSL);   // [4][rows]
+  float* pml = pz + 4 * rows;                                       // [4][NB][2] (m, l)
+  float4* zf = reinterpret_cast<float4*>(pml + 8 * NB);             // [rows] x 4 seqs
+  float* red = reinterpret_cast<float*>(zf + rows);                 // [256/DSL][4][DSL]
+  const int s0 = blockIdx.x * 4, h = blockIdx.y, kp = blockIdx.z, tid = threadIdx.x;
+  const int d0 = kp * DSL;
+  MLRA_STAMP(0);
+  {
+    // W^UV slice: row r = b*DLAT + c of head h, columns [d0, d0+DSL): DSL*2 bytes = 16-byte chunks
+    const int cpr = DSL / 8;
+    const __nv_bfloat16* src = w_uv + size_t(h) * rows * DH + d0;
+    const uint32_t dst0 = smem_u32(wsl);
+    for (int i = tid; i < rows * cpr; i += kSkThreads) {
+      const int r = i / cpr, c = i % cpr;
+      cp_async16(dst0 + uint32_t((r * DSL + c * 8) * 2), src + size_t(r) * DH + c * 8, 16u);
+    }
+  }
+  griddep_wait();
+  // ---- 2. local merge over this CTA's splits; item = (sequence q, row r = b*DLAT + c)
+  const int k0 = int((long long)kp * nsplit / KP), k1 = int((long long)(kp + 1) * nsplit / KP);
+  const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
+  for (int it = tid; it < 4 * rows; it += kSkThreads) {
+    const int q = it / rows, r = it % rows, b = r / DLAT, c = r % DLAT, s = s0 + q;
+    float m = -INFINITY, l = 0.f, z = 0.f;
+    if (s < B) {
+      const float* lp = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
+      const float* op = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
+      for (int kb = k0; kb < k1; kb += kMergeChunk) {
+        float lk[kMergeChunk], v[kMergeChunk];
+#pragma unroll
+        for (int j = 0; j < kMergeChunk; ++j) {
+          const int k = min(kb + j, k1 - 1);
+          lk[j] = __ldcg(lp + size_t(k) * NB * H);
+          v[j] = __ldcg(op + size_t(k) * kstride);
+        }
+        float mc = m;
+#pragma unroll
+        for (int j = 0; j < kMergeChunk; ++j) mc = (kb + j < k1) ? fmaxf(mc, lk[j]) : mc;
+        if (mc != -INFINITY) {
+          const float a = (m == -INFINITY) ? 0.f : ex2(m - mc);
+          z *= a;
+          l *= a;
+#pragma unroll
+          for (int j = 0; j < kMergeChunk; ++j) {
+            const float w = (kb + j >= k1 || lk[j] == -INFINITY) ? 0.f : ex2(lk[j] - mc);
+            l += w;
+            z = fmaf(w, v[j], z);
+          }
+          m = mc;
+        }
+      }
+    }
+    pz[q * rows + r] = z;
+    if (c == 0) {
+      pml[(q * NB + b) * 2] = m;
+      pml[(q * NB + b) * 2 + 1] = l;
+    }
+  }
+  cp_async_wait_all();
+  cluster_arrive_release();  // also a CTA barrier: partials and the W slice are in place
+  cluster_wait_acquire();
+  MLRA_STAMP(1);
+  // ---- 3. combine the KP partials (DSMEM, ascending kp): merged latent for every item
+  {
+    const uint32_t pz_a = smem_u32(pz), pml_a = smem_u32(pml);
+    for (int it = tid; it < 4 * rows; it += kSkThreads) {
+      const int q = it / rows, r = it % rows, b = r / DLAT;
+      float mk[KP], lk[KP], zk[KP];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) {
+        mk[j] = ld_shared_cluster_f32(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2) * 4), j));
+        lk[j] = ld_shared_cluster_f32(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2 + 1) * 4), j));
+        zk[j] = ld_shared_cluster_f32(mapa_shared(pz_a + uint32_t((q * rows + r) * 4), j));
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < KP; ++j) M = fmaxf(M, mk[j]);
+      float L = 0.f, Z = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+          const float w = mk[j] == -INFINITY ? 0.f : ex2(mk[j] - M);
+          L = fmaf(lk[j], w, L);
+          Z = fmaf(zk[j], w, Z);
+        }
+      }
+      reinterpret_cast<float*>(zf)[r * 4 + q] = L > 0.f ? Z / L : 0.f;
+    }
+  }
+  // every CTA of the cluster is done reading this CTA's partial before anyone moves on
+  cluster_arrive_release();
+  cluster_wait_acquire();
+  MLRA_STAMP(2);
+  // ---- 4. up-projection of this CTA's columns: thread = (column dd, eighth of the rows)
+  {
+    const int dd = tid % DSL, part = tid / DSL;  // DSL divides 256
+    const int nparts = kSkThreads / DSL;
+    const int rl = (rows + nparts - 1) / nparts, r0 = part * rl, r1 = min(rows, r0 + rl);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+#pragma unroll 4
+      for (int r = r0; r < r1; ++r) {
+        const float w = __bfloat162float(wsl[r * DSL + dd]);
+        const float4 z = zf[r];
+        acc[0] = fmaf(z.x, w, acc[0]);
+        acc[1] = fmaf(z.y, w, acc[1]);
+        acc[2] = fmaf(z.z, w, acc[2]);
+        acc[3] = fmaf(z.w, w, acc[3]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[(part * 4 + q) * DSL + dd] = acc[q];
+    __syncthreads();
+    for (int i = tid; i < 4 * DSL; i += kSkThreads) {
+      const int q = i / DSL, d = i % DSL, s = s0 + q;
+      float v = 0.f;
+      for (int j = 0; j < nparts; ++j) v += red[(j * 4 + q) * DSL + d];
+      if (s < B) out[(size_t(s) * H + h) * DH + d0 + d] = v * alpha;
+    }
+  }
+  MLRA_STAMP(3);
+}
+
 }  // namespace mlra

@@ -446,6 +446,39 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
                         bool pdl = false) {
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
+  // summed output: split-K merge over a cluster of KP CTAs (KP = 8 once the splits are many)
+  const int KP = nsplit > 24 ? 8 : 4;
+  const size_t sksmem = KP == 8 ? mlra::combine_splitk_smem<8>(NB, DLAT, DH) : mlra::combine_splitk_smem<4>(NB, DLAT, DH);
+  // Cost model in dependent L2 round trips per thread (12 split loads in flight per item):
+  // per-branch CTAs (combine4) 2 * ceil(nsplit/12); split-K CTAs (all branches, 1/KP of the
+  // splits each) 2*NB * ceil(ceil(nsplit/KP)/12), plus two cluster barriers -- worth it at
+  // 1.5x fewer round trips (small batches: many splits per sequence).
+  const int rt_c4 = 2 * ((nsplit + 11) / 12);
+  const int rt_sk = 2 * NB * (((nsplit + KP - 1) / KP + 11) / 12);
+  if (upproj == 1 && 3 * rt_sk < 2 * rt_c4 && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
+      sksmem <= size_t(kSmemBudget) && (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
+    auto kern = KP == 8 ? mlra::combine_splitk_kernel<8> : mlra::combine_splitk_kernel<4>;
+    static unsigned attr4 = 0, attr8 = 0;
+    if (int rc = set_smem_once(kern, KP == 8 ? attr8 : attr4, kSmemBudget)) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((B + 3) / 4, H, KP);
+    cfg.blockDim = dim3(mlra::kSkThreads);
+    cfg.dynamicSmemBytes = sksmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = KP;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
+                           DH, nsplit, alpha) != cudaSuccess)
+      return cuda_check("combine launch");
+    return cuda_check("combine launch");
+  }
   const size_t c4smem = mlra::combine4_smem<4>(DLAT, DH, nsplit);
   if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
