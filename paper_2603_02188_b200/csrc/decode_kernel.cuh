@@ -199,14 +199,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tma_prefetch_desc(&lat_map);
     tma_prefetch_desc(&rope_map);
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_sh);
-
-  for (int i = tid; i < 32 * NPAD; i += kNumThreads) m_run[i] = 0.f;  // set exactly on tile 0
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tmem_base_sh;
+  // The TMA producer (warp 0) only needs the mbarriers: it announces them (bar.arrive) and
+  // starts streaming without waiting for the TMEM allocation and the consumers' setup.
+  if (warp == 0) {
+    __syncwarp();
+    named_bar_arrive(6, kNumThreads);
+  } else {
+    if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_sh);
+    for (int i = tid - 32; i < 32 * NPAD; i += kNumThreads - 32) m_run[i] = 0.f;  // set exactly on tile 0
+    fence_proxy_async_smem();
+    tc_fence_before();
+    named_bar_sync(6, kNumThreads);
+    tc_fence_after();
+  }
+  const uint32_t tbase = warp == 0 ? 0u : *tmem_base_sh;
   if (warp != 0) {
     // Under PDL this kernel overlaps K1's tail: the TMA producer is already streaming the
     // cache (written before K1 started); the queries are K1's output.
