@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
                 int nsplit, float alpha, int per_branch) {
-  static_assert(SEQS == 4 || SEQS == 8, "4 or 8 sequences per CTA");
+  static_assert(SEQS == 2 || SEQS == 4 || SEQS == 8, "2, 4 or 8 sequences per CTA");
   constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
   const size_t wbytes = size_t(DLAT) * DH * 2;
@@ -458,12 +458,19 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
       for (int c = cr0; c < cr1; ++c) {
         const float w = __bfloat162float(wc[size_t(c) * DH]);
 #pragma unroll
-        for (int s4 = 0; s4 < SEQS; s4 += 4) {
-          const float4 z = *reinterpret_cast<const float4*>(zs + c * SEQS + s4);
-          acc[s4 + 0] = fmaf(z.x, w, acc[s4 + 0]);
-          acc[s4 + 1] = fmaf(z.y, w, acc[s4 + 1]);
-          acc[s4 + 2] = fmaf(z.z, w, acc[s4 + 2]);
-          acc[s4 + 3] = fmaf(z.w, w, acc[s4 + 3]);
+        if constexpr (SEQS == 2) {
+          const float2 z = *reinterpret_cast<const float2*>(zs + c * SEQS);
+          acc[0] = fmaf(z.x, w, acc[0]);
+          acc[1] = fmaf(z.y, w, acc[1]);
+        } else {
+#pragma unroll
+          for (int s4 = 0; s4 < SEQS; s4 += 4) {
+            const float4 z = *reinterpret_cast<const float4*>(zs + c * SEQS + s4);
+            acc[s4 + 0] = fmaf(z.x, w, acc[s4 + 0]);
+            acc[s4 + 1] = fmaf(z.y, w, acc[s4 + 1]);
+            acc[s4 + 2] = fmaf(z.z, w, acc[s4 + 2]);
+            acc[s4 + 3] = fmaf(z.w, w, acc[s4 + 3]);
+          }
         }
       }
     }

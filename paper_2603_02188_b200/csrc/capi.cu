@@ -479,17 +479,26 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
       return cuda_check("combine launch");
     return cuda_check("combine launch");
   }
-  const size_t c4smem = mlra::combine4_smem<4>(DLAT, DH, nsplit);
+  // 2 sequences per CTA (one merge item per thread) while the grid stays within one wave
+  // (4 CTAs per SM), else 4
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool seq2 = long((B + 1) / 2) * H * NB <= 4L * sms && getenv("MLRA_K3_SEQ4") == nullptr;
+  const size_t c4smem = seq2 ? mlra::combine4_smem<2>(DLAT, DH, nsplit) : mlra::combine4_smem<4>(DLAT, DH, nsplit);
   if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
-    // CTA = (4 sequences, head, branch); with a summed output the NB branch CTAs of a
+    // CTA = (2 or 4 sequences, head, branch); with a summed output the NB branch CTAs of a
     // (sequence group, head) form a cluster and add their results through DSMEM.
     // (8 sequences per CTA measured slower even where 4 needs 1.3 waves.)
-    auto kern = mlra::combine4_kernel<4>;
-    static unsigned attr_done4 = 0;
-    if (int rc = set_smem_once(kern, attr_done4, kSmemBudget)) return rc;
+    auto kern = seq2 ? mlra::combine4_kernel<2> : mlra::combine4_kernel<4>;
+    static unsigned attr_done2 = 0, attr_done4 = 0;
+    if (int rc = set_smem_once(kern, seq2 ? attr_done2 : attr_done4, kSmemBudget)) return rc;
     const int per_branch = upproj == 2 ? 1 : 0;
-    const int seqs = 4;
+    const int seqs = seq2 ? 2 : 4;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
     cfg.blockDim = dim3(256);
