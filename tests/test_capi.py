@@ -67,3 +67,28 @@ def test_cpu_safe_calls(lib):
     assert rc == -2
     with pytest.raises(_lib.ConfigError):
         _lib.check(-2, "probe")
+
+
+def test_cpu_safe_calls_gqa_and_fused_append(lib):
+    # GQA entry points: validation before any CUDA call
+    assert lib.mlra_gqa_workspace_bytes(16, 6, 4, 128, 3) >= 16 * 3 * 6 * 4 * 128 * 4
+    assert 1 <= lib.mlra_gqa_default_splits(16, 6, 32768) <= 160
+    rc = lib.mlra_gqa_decode_partials(None, None, None, None, None, None, 1, 6, 4, 96, 128, 1, 1, 1, 1.0, None)
+    assert rc == -2 and b"head width" in lib.mlra_last_error()
+    rc = lib.mlra_gqa_decode_partials(None, None, None, None, None, None, 1, 6, 32, 128, 128, 1, 1, 1, 1.0, None)
+    assert rc == -2 and b"query heads per KV head" in lib.mlra_last_error()
+    rc = lib.mlra_gqa_decode_step(None, None, None, None, None, None, 1, 6, 4, 128, 100, 1, 1, 1, 1.0, None)
+    assert rc == -2 and b"page_size" in lib.mlra_last_error()
+    # fused K0: shape / config validation
+    rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 510, 4, 0, 4, 128, 64, 64, 1.0, 1e4, 1e-6,
+                                      128, 1, None, None)
+    assert rc == -1 and b"branches" in lib.mlra_last_error()
+    rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 512, 4, 3, 2, 128, 64, 64, 1.0, 1e4, 1e-6,
+                                      128, 1, None, None)
+    assert rc == -2 and b"blocks" in lib.mlra_last_error()
+    rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 512, 4, 0, 1, 128, 63, 64, 1.0, 1e4, 1e-6,
+                                      128, 1, None, None)
+    assert rc == -2 and b"even" in lib.mlra_last_error()
+    # splits beyond the merge kernels' limit
+    rc = lib.mlra_decode_partials(None, None, None, None, None, None, None, 1, 24, 1, 1, 128, 64, 128, 1, 1, 161, None)
+    assert rc == -2 and b"nsplit" in lib.mlra_last_error()
