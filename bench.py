@@ -350,7 +350,7 @@ def cpu_oracle_sample(phi: int, n: int, seqs: int, seed: int = 0):
     w = {"w_uk": rng.standard_normal((512, 24 * 128)) * 0.02, "w_uv": rng.standard_normal((512, 24 * 128)) * 0.02}
     units = ak.shard_units(cfg, phi, 0)[1]
     streams = {"rope": rng.standard_normal((n, 64))}
-    for _, b, _h in units:
+    for _, _g, b, _h in units:
         streams[f"latent_b{b}"] = rng.standard_normal((n, 128)) * 24 ** 0.5 / 8
     qn = rng.standard_normal((24, 128))
     qr = rng.standard_normal((24, 64))

@@ -6,7 +6,7 @@ arm may import it; the product package ``paper_2603_02188_b200`` never does.
 
 It restates, function by function, the reference kit's decode path
 (/root/reference/pkg/src/attnkit, cited as ``attnkit/<file>:<line>``) for the
-variants the B200 path serves (mla, mlra, gqa) and is pinned against golden
+variants the B200 path serves (mla, mlra-4, mlra-2, gla, gqa) and is pinned against golden
 vectors generated from the reference itself (``oracle/gen_golden.py`` ->
 ``tests/golden/*.npz``; checked by ``tests/test_oracle.py``).
 
@@ -67,6 +67,14 @@ class Cfg:
     @property
     def block_dim(self) -> int:  # attnkit/config.py:114-117
         return self.d_c // 4
+
+    @property
+    def group_latent_dim(self) -> int:  # attnkit/config.py:119-121
+        return self.d_c // self.g
+
+    @property
+    def grouped(self) -> bool:  # attnkit/weights.py:104-105 (gla, or mlra with two branches)
+        return self.variant == "gla" or (self.variant == "mlra" and self.branches == 2)
 
 
 def cfg_from(obj) -> Cfg:
@@ -134,16 +142,23 @@ def calib_alphas(cfg: Cfg) -> tuple[float, float, float]:  # attnkit/latent.py:4
     return float(q2) ** 0.5, float(kv2) ** 0.5, float(a2) ** 0.5
 
 
-def weight_shapes(cfg: Cfg) -> dict:  # attnkit/weights.py:45-99 (latent single-latent + gqa)
+def weight_shapes(cfg: Cfg) -> dict:  # attnkit/weights.py:45-99 (latent family + gqa)
     h, d, d_h = cfg.h, cfg.d, cfg.d_h
     if cfg.variant == "gqa":
         s = {"w_q": (d, h * d_h), "w_k": (d, cfg.g * d_h), "w_v": (d, cfg.g * d_h)}
-    elif cfg.variant in ("mla", "mlra") and not (cfg.variant == "mlra" and cfg.branches == 2):
+    elif cfg.variant in LATENT:
         s = {"w_dq": (d, cfg.d_cq), "w_uq": (cfg.d_cq, h * d_h), "w_qr": (cfg.d_cq, h * cfg.d_h_rope),
-             "w_kr": (d, cfg.d_h_rope), "w_dkv": (d, cfg.d_c), "w_uk": (cfg.d_c, h * d_h),
-             "w_uv": (cfg.d_c, h * d_h)}
+             "w_kr": (d, cfg.d_h_rope)}
+        if cfg.grouped:  # weights.py:85-91: one latent (and up-projections) per group
+            r, dg = h // cfg.g, cfg.group_latent_dim
+            for j in range(cfg.g):
+                s[f"w_dkv_{j}"] = (d, dg)
+                s[f"w_uk_{j}"] = (dg, r * d_h)
+                s[f"w_uv_{j}"] = (dg, r * d_h)
+        else:
+            s.update({"w_dkv": (d, cfg.d_c), "w_uk": (cfg.d_c, h * d_h), "w_uv": (cfg.d_c, h * d_h)})
     else:
-        raise OracleError(f"oracle covers mla / mlra-4 / gqa, not {cfg.variant}")
+        raise OracleError(f"oracle covers the latent family and gqa, not {cfg.variant}")
     s["w_o"] = (h * d_h, d)
     return s
 
@@ -161,12 +176,20 @@ def latent_projections(cfg: Cfg, w: dict, hidden: np.ndarray, positions):  # att
     q_nope = (c_q @ w["w_uq"]).reshape(n, cfg.h, cfg.d_h)
     q_rope = rope_rotate((c_q @ w["w_qr"]).reshape(n, cfg.h, cfg.d_h_rope), positions)
     k_rope = rope_rotate(hidden @ w["w_kr"], positions)
-    c_kv = akv * rmsnorm(hidden @ w["w_dkv"])
+    bs = cfg.block_dim
     if cfg.variant == "mla":
-        latents = {"latent": c_kv}
-    else:
-        bs = cfg.block_dim
+        latents = {"latent": akv * rmsnorm(hidden @ w["w_dkv"])}
+    elif cfg.variant == "gla":  # latent.py:145-147: one normalised latent per group
+        latents = {f"latent_{j}": akv * rmsnorm(hidden @ w[f"w_dkv_{j}"]) for j in range(cfg.g)}
+    elif cfg.branches == 4:
+        c_kv = akv * rmsnorm(hidden @ w["w_dkv"])
         latents = {f"latent_b{b}": c_kv[:, b * bs:(b + 1) * bs] for b in range(4)}
+    else:  # mlra-2, latent.py:154-158: two blocks within each of the two group latents
+        latents = {}
+        for grp in range(2):
+            c_grp = akv * rmsnorm(hidden @ w[f"w_dkv_{grp}"])
+            for b in range(2):
+                latents[f"latent_{grp}_{b}"] = c_grp[:, b * bs:(b + 1) * bs]
     return q_nope, q_rope, k_rope, latents
 
 
@@ -220,31 +243,57 @@ def absorb_query(q_nope: np.ndarray, w_uk: np.ndarray) -> np.ndarray:  # attnkit
     return np.einsum("mp,cmp->mc", q_nope, w_uk)
 
 
+def stream_name(group: int, block: int) -> str:  # attnkit/cache.py:147-155
+    if group < 0 and block < 0:
+        return "latent"
+    if block < 0:
+        return f"latent_{group}"
+    if group < 0:
+        return f"latent_b{block}"
+    return f"latent_{group}_{block}"
+
+
+def unit(group: int, block: int, heads) -> tuple:
+    """A latent unit as (stream, group, block, heads) -- attnkit/decode.py:31-41."""
+    return (stream_name(group, block), group, block, tuple(heads))
+
+
 def units(cfg: Cfg, heads=None):
-    """(stream, block, heads) per latent unit -- full_ownership, attnkit/decode.py:53-76."""
-    heads = tuple(range(cfg.h)) if heads is None else tuple(heads)
+    """Latent units of full ownership -- attnkit/decode.py:53-76."""
+    all_heads = tuple(range(cfg.h))
     if cfg.variant == "mla":
-        return [("latent", -1, heads)]
-    return [(f"latent_b{b}", b, heads) for b in range(4)]
+        return [unit(-1, -1, all_heads)]
+    if cfg.variant == "gla":
+        r = cfg.h // cfg.g
+        return [unit(j, -1, range(j * r, (j + 1) * r)) for j in range(cfg.g)]
+    if cfg.branches == 4:
+        return [unit(-1, b, all_heads) for b in range(4)]
+    half = cfg.h // 2
+    return [unit(grp, b, range(grp * half, (grp + 1) * half)) for grp in range(2) for b in range(2)]
 
 
-def unit_weights(cfg: Cfg, w: dict, block: int, heads) -> tuple:  # attnkit/decode.py:170-187
-    w_uk, w_uv = w["w_uk"], w["w_uv"]
+def unit_weights(cfg: Cfg, w: dict, group: int, block: int, heads) -> tuple:  # attnkit/decode.py:170-187
+    heads = list(heads)
+    if group < 0:
+        w_uk, w_uv, local = w["w_uk"], w["w_uv"], heads
+    else:
+        r = cfg.h // cfg.g
+        w_uk, w_uv = w[f"w_uk_{group}"], w[f"w_uv_{group}"]
+        local = [i - group * r for i in heads]
     if block >= 0:
         bs = cfg.block_dim
         w_uk, w_uv = w_uk[block * bs:(block + 1) * bs], w_uv[block * bs:(block + 1) * bs]
     d_lat = w_uk.shape[0]
-    heads = list(heads)
-    return (w_uk.reshape(d_lat, -1, cfg.d_h)[:, heads], w_uv.reshape(d_lat, -1, cfg.d_h)[:, heads])
+    return (w_uk.reshape(d_lat, -1, cfg.d_h)[:, local], w_uv.reshape(d_lat, -1, cfg.d_h)[:, local])
 
 
 def attend_latent(cfg: Cfg, w: dict, cache: Cache, q_nope, q_rope, unit_list) -> list:
     """attend_local, latent branch (attnkit/decode.py:217-230)."""
     rope_hist = cache.read("rope")
     contribs = []
-    for stream, block, heads in unit_list:
+    for stream, group, block, heads in unit_list:
         latent_hist = cache.read(stream)
-        uk, uv = unit_weights(cfg, w, block, heads)
+        uk, uv = unit_weights(cfg, w, group, block, heads)
         hl = list(heads)
         q_tilde = absorb_query(q_nope[hl], uk)
         logits = cfg.tau * (q_tilde @ latent_hist.T + q_rope[hl] @ rope_hist.T)
@@ -317,9 +366,9 @@ def naive_decode_step(cfg: Cfg, w: dict, cache: Cache, h_t: np.ndarray) -> np.nd
     cache.append(rows)
     rope_hist = cache.read("rope")
     out = np.zeros((cfg.h, cfg.d_h))
-    for stream, block, heads in units(cfg):
+    for stream, group, block, heads in units(cfg):
         latent_hist = cache.read(stream)
-        uk, uv = unit_weights(cfg, w, block, heads)
+        uk, uv = unit_weights(cfg, w, group, block, heads)
         for j, head in enumerate(heads):
             k_head = latent_hist @ uk[:, j]
             v_head = latent_hist @ uv[:, j]
@@ -357,13 +406,36 @@ def shard_units(cfg: Cfg, phi: int, k: int):
         return heads, (group,)
     if cfg.variant == "mla":
         heads = _ranges(h, phi, "query-head axis")[k]
-        return heads, [("latent", -1, heads)]
-    if phi <= 4:
-        blocks = _ranges(4, phi, "latent-block axis")[k]
-        return all_heads, [(f"latent_b{b}", b, all_heads) for b in blocks]
-    block, half = k // 2, k % 2
-    heads = _ranges(h, 2, "query-head axis")[half]
-    return heads, [(f"latent_b{block}", block, heads)]
+        return heads, [unit(-1, -1, heads)]
+    if cfg.variant == "gla":  # tpsim.py:92-106: latent-group axis, then heads within a group
+        g, r = cfg.g, h // cfg.g
+        if phi <= g:
+            us = [unit(j, -1, range(j * r, (j + 1) * r)) for j in _ranges(g, phi, "latent-group axis")[k]]
+            return tuple(i for u in us for i in u[3]), us
+        per_group = phi // g
+        if phi % g != 0 or r % per_group != 0:
+            raise OracleError(f"gla: cannot split {r} heads per group across {per_group} devices")
+        group = k // per_group
+        heads = tuple(i + group * r for i in _ranges(r, per_group, "query-head axis")[k % per_group])
+        return heads, [unit(group, -1, heads)]
+    if cfg.branches == 4:  # tpsim.py:108-116
+        if phi <= 4:
+            return all_heads, [unit(-1, b, all_heads) for b in _ranges(4, phi, "latent-block axis")[k]]
+        block, half = k // 2, k % 2
+        heads = _ranges(h, 2, "query-head axis")[half]
+        return heads, [unit(-1, block, heads)]
+    pairs = [(grp, b) for grp in range(2) for b in range(2)]  # mlra-2, tpsim.py:117-131
+    half_heads = [tuple(range(grp * (h // 2), (grp + 1) * (h // 2))) for grp in range(2)]
+    if phi == 1:
+        return all_heads, [unit(grp, b, half_heads[grp]) for grp, b in pairs]
+    if phi == 2:
+        return half_heads[k], [unit(k, b, half_heads[k]) for b in range(2)]
+    if phi == 4:
+        grp, b = pairs[k]
+        return half_heads[grp], [unit(grp, b, half_heads[grp])]
+    grp, b = pairs[k // 2]
+    heads = tuple(i + grp * (h // 2) for i in _ranges(h // 2, 2, "query-head axis")[k % 2])
+    return heads, [unit(grp, b, heads)]
 
 
 def sim_decode_attention(cfg: Cfg, w: dict, streams: dict, q_nope, q_rope, phi: int) -> tuple:
@@ -390,6 +462,8 @@ def per_device_load(cfg: Cfg, phi: int) -> Fraction:  # attnkit/costs.py:70-102 
         return Fraction(2 * cfg.g, min(phi, cfg.g))
     if cfg.variant == "mla":
         return Fraction(cfg.d_c + cfg.d_h_rope, cfg.d_h)
+    if cfg.variant == "gla":
+        return Fraction(cfg.d_c, min(phi, cfg.g) * cfg.d_h) + Fraction(cfg.d_h_rope, cfg.d_h)
     if cfg.variant == "mlra":
         return Fraction(cfg.d_c, min(phi, 4) * cfg.d_h) + Fraction(cfg.d_h_rope, cfg.d_h)
     raise OracleError(f"no loading rule for {cfg.variant}")

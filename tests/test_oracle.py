@@ -69,7 +69,8 @@ def test_naive_step_and_queries_match_reference(name):
     assert ak.max_rel_err(arrays["out_absorbed"], att) <= 1e-10
 
 
-@pytest.mark.parametrize("name", [c for c in CASES if c in ("tiny_mlra4", "refdims_mlra4", "refdims_mla")])
+@pytest.mark.parametrize("name", [c for c in CASES if c in ("tiny_mlra4", "refdims_mlra4", "refdims_mla",
+                                                           "refdims_mlra2", "refdims_gla2")])
 def test_tensor_parallel_matches_reference(name):
     meta, arrays = load(name)
     cfg, w, hidden = regen(meta)
@@ -95,6 +96,11 @@ def test_per_device_load_table():
     assert [str(ak.per_device_load(p, phi)) for phi in (1, 2, 4, 8)] == ["9/2", "5/2", "3/2", "3/2"]
     mla = ak.Cfg("mla", 24, 3072, 128, 64, 512, 1536, scaling=True)
     assert {ak.per_device_load(mla, phi) for phi in (1, 2, 4, 8)} == {ak.Fraction(9, 2)}
+    # MLRA-2 also reaches 1.5 d_h at TP4; GLA-2 plateaus at 2.5 d_h
+    m2 = ak.Cfg("mlra", 24, 3072, 128, 64, 512, 1024, branches=2, scaling=True)
+    assert [str(ak.per_device_load(m2, phi)) for phi in (1, 2, 4, 8)] == ["9/2", "5/2", "3/2", "3/2"]
+    g2 = ak.Cfg("gla", 24, 3072, 128, 64, 512, 1024, g=2, scaling=True)
+    assert [str(ak.per_device_load(g2, phi)) for phi in (1, 2, 4, 8)] == ["9/2", "5/2", "5/2", "5/2"]
 
 
 def test_softmax_guards():
