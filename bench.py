@@ -261,9 +261,9 @@ def time_k2_alone(eng_qs, iters):
     stream = torch.cuda.current_stream()
     preps = []
     for eng, qn, qr in eng_qs:
-        q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale)
+        q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.nb, eng.dlat, eng.scale)
         c = eng.cache
-        outs = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub,
+        outs = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub,
                                    eng.dls, eng.nsplit)
         preps.append((eng, q_abs, q_rs, outs))
     side = torch.cuda.Stream()
@@ -274,7 +274,7 @@ def time_k2_alone(eng_qs, iters):
         for i in range(per):
             eng, q_abs, q_rs, outs = preps[i % 2]
             c = eng.cache
-            ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub,
+            ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub,
                                 eng.dls, eng.nsplit, out=outs)
     g.replay()
     torch.cuda.synchronize()

@@ -56,18 +56,20 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_
 /*
  * K0 (fused write side) -- the cache half of latent.py:129-159 (latent_projections) plus
  * decode.py:129-150 (append_owned), for a batch of new tokens:
- *   c_kv  = alpha_kv * rmsnorm(kv_raw)  (eps, tensors.py:83-87), blocks [block0, block0+nblocks)
- *           of the `branches` equal blocks kept (latent.py:150-153), each zero-padded to dlp
+ *   c_kv  = alpha_kv * rmsnorm(kv_raw) per latent group (norm_groups consecutive groups of
+ *           d_c/norm_groups columns: 1 for MLA / MLRA-4, one per group for GLA / MLRA-2;
+ *           eps, tensors.py:83-87), blocks [block0, block0+nblocks) of the `branches` equal
+ *           blocks kept (latent.py:145-158), each zero-padded to dlp
  *   k_rope = rope(kr_raw, rope_pos)     (rope.py:37-60: pairs (2l, 2l+1), theta_l =
  *           rope_base^(-2l/dr)), zero-padded to drp
  *   pool row [c_kv blocks | k_rope] bf16 written at slot slots[s] of sequence s.
- *   kv_raw [B, d_c] fp32 = h W^DKV (the whole row: the RMS spans all blocks), kr_raw [B, dr]
- *   fp32 = h W^KR. MLA: branches = 1.
+ *   kv_raw [B, d_c] fp32 = h W^DKV (whole groups: the RMS spans a group's blocks), kr_raw
+ *   [B, dr] fp32 = h W^KR. MLA: branches = 1.
  */
 int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, const int32_t* slots,
                              const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
                              int dlp, int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size,
-                             int max_pages, void* pool, void* stream);
+                             int max_pages, int norm_groups, void* pool, void* stream);
 
 /*
  * K1 -- query absorption (decode.py:155-167 absorb_query, applied per branch at :224).

@@ -186,7 +186,7 @@ class PagedCache:
         self._host_lens = [n + 1 for n in self._host_lens]
 
     def append_latent(self, kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos, *, branches: int, block0: int,
-                      nblocks: int, alpha_kv: float, rope_base: float = 10000.0) -> None:
+                      nblocks: int, alpha_kv: float, rope_base: float = 10000.0, norm_groups: int = 1) -> None:
         """Fused K0 for one new token per sequence: kv_raw [B, d_c] / kr_raw [B, dr] fp32 raw
         projections, rope_pos [B] absolute positions (host list or int32 device tensor)."""
         lay = self.layout
@@ -196,7 +196,8 @@ class PagedCache:
         ops.cache_append_latent(kv_raw.float().contiguous(), kr_raw.float().contiguous(),
                                 pos.to(device=self.device, dtype=torch.int32), self.seqlens, self.block_table,
                                 self.pool, self.page_size, branches=branches, block0=block0, nblocks=nblocks,
-                                dlp=lay.dlp, drp=lay.drp, alpha_kv=alpha_kv, rope_base=rope_base)
+                                dlp=lay.dlp, drp=lay.drp, alpha_kv=alpha_kv, rope_base=rope_base,
+                                norm_groups=norm_groups)
         self.seqlens += 1
         self._host_lens = [n + 1 for n in self._host_lens]
 
@@ -276,13 +277,13 @@ class PagedLatentCache:
         self.paged.append(row)
 
     def append_latent(self, kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: int, *, branches: int,
-                      block0: int, nblocks: int, alpha_kv: float) -> None:
+                      block0: int, nblocks: int, alpha_kv: float, norm_groups: int = 1) -> None:
         """Fused write side (K0): rmsnorm*alpha_kv of the raw down-projection [1, d_c], rope of the
         raw rotary key [1, dr] at rope_pos, owned blocks + key appended as one row."""
         if self.n >= self.paged.capacity:
             self._grow()
         self.paged.append_latent(kv_raw, kr_raw, [rope_pos], branches=branches, block0=block0, nblocks=nblocks,
-                                 alpha_kv=alpha_kv)
+                                 alpha_kv=alpha_kv, norm_groups=norm_groups)
 
     def read(self, name: str) -> np.ndarray:
         """Debug copy of one stream as float64 [n, width], charging n*width reads."""

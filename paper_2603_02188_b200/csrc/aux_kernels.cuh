@@ -57,27 +57,38 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
                            const int32_t* __restrict__ rope_pos, const int32_t* __restrict__ slots,
                            const int32_t* __restrict__ block_table, int d_c, int bs, int block0, int nblocks, int dlp,
                            int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size, int max_pages,
-                           __nv_bfloat16* __restrict__ pool) {
-  __shared__ float red[kK0Threads / 32];
+                           int norm_groups, __nv_bfloat16* __restrict__ pool) {
+  // RMS per latent group: the row is norm_groups consecutive groups of d_c/norm_groups
+  // columns (1 for MLA / MLRA-4; one per group for GLA / MLRA-2, latent.py:145-158)
+  constexpr int kMaxGroups = 4;
+  __shared__ float red[kMaxGroups][kK0Threads / 32];
+  __shared__ float gscale[kMaxGroups];
   const int s = blockIdx.x, tid = threadIdx.x;
   const float* kv = kv_raw + size_t(s) * d_c;
-  float ss = 0.f;
-  for (int c = tid; c < d_c; c += kK0Threads) ss = fmaf(kv[c], kv[c], ss);
+  const int gw = d_c / norm_groups;
+  for (int g = 0; g < norm_groups; ++g) {
+    float ss = 0.f;
+    for (int c = tid; c < gw; c += kK0Threads) ss = fmaf(kv[g * gw + c], kv[g * gw + c], ss);
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-  if ((tid & 31) == 0) red[tid >> 5] = ss;
+    for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((tid & 31) == 0) red[g][tid >> 5] = ss;
+  }
   __syncthreads();
-  float tot = 0.f;
+  if (tid < norm_groups) {
+    float tot = 0.f;
 #pragma unroll
-  for (int w = 0; w < kK0Threads / 32; ++w) tot += red[w];
-  const float scale = alpha_kv * rsqrtf(tot / float(d_c) + eps);
+    for (int w = 0; w < kK0Threads / 32; ++w) tot += red[tid][w];
+    gscale[tid] = alpha_kv * rsqrtf(tot / float(gw) + eps);
+  }
+  __syncthreads();
   const int slot = slots[s];
   const int page = block_table[size_t(s) * max_pages + slot / page_size];
   const int W = nblocks * dlp + drp;
   __nv_bfloat16* dst = pool + (size_t(page) * page_size + slot % page_size) * W;
   for (int i = tid; i < nblocks * dlp; i += kK0Threads) {
     const int u = i / dlp, c = i % dlp;
-    const float v = c < bs ? kv[(block0 + u) * bs + c] * scale : 0.f;
+    const int col = (block0 + u) * bs + c;
+    const float v = c < bs ? kv[col] * gscale[col / gw] : 0.f;
     dst[i] = __float2bfloat16(v);
   }
   const double pos = double(rope_pos[s]);

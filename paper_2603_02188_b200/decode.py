@@ -32,7 +32,7 @@ from .costs import calib_factors
 from .errors import ConfigError, IntegrityError, RoutingError
 from .projections import LatentProjector
 
-SERVED = ("mla", "mlra", "gqa")
+SERVED = ("mla", "mlra", "gla", "gqa")
 
 
 @dataclass(frozen=True)
@@ -69,9 +69,7 @@ def latent_stream_name(group: int, block: int) -> str:  # attnkit/cache.py:147-1
 
 def _check_served(cfg: AttnConfig) -> None:
     if cfg.variant not in SERVED:
-        raise RoutingError(f"the B200 latent decode path serves {SERVED}; got {cfg.variant!r}")
-    if cfg.variant == "mlra" and cfg.branches != 4:
-        raise RoutingError("the B200 latent decode path serves the four-branch MLRA form (MLRA-4)")
+        raise RoutingError(f"the B200 decode path serves {SERVED}; got {cfg.variant!r}")
 
 
 def full_ownership(cfg: AttnConfig) -> Ownership:  # decode.py:53-76 (served variants)
@@ -81,11 +79,39 @@ def full_ownership(cfg: AttnConfig) -> Ownership:  # decode.py:53-76 (served var
         return Ownership(all_heads, kv_slots=tuple(range(cfg.g)))
     if cfg.variant == "mla":
         return Ownership(all_heads, units=(LatentUnit(-1, -1, all_heads),))
-    return Ownership(all_heads, units=tuple(LatentUnit(-1, b, all_heads) for b in range(4)))
+    if cfg.variant == "gla":
+        r = cfg.h // cfg.g
+        return Ownership(all_heads, units=tuple(LatentUnit(j, -1, tuple(range(j * r, (j + 1) * r)))
+                                               for j in range(cfg.g)))
+    if cfg.branches == 4:
+        return Ownership(all_heads, units=tuple(LatentUnit(-1, b, all_heads) for b in range(4)))
+    half = cfg.h // 2
+    return Ownership(all_heads, units=tuple(LatentUnit(grp, b, tuple(range(grp * half, (grp + 1) * half)))
+                                           for grp in range(2) for b in range(2)))
 
 
 def unit_width(cfg: AttnConfig) -> int:
-    return cfg.d_c if cfg.variant == "mla" else cfg.block_dim
+    if cfg.variant == "mla":
+        return cfg.d_c
+    if cfg.variant == "gla":
+        return cfg.group_latent_dim
+    return cfg.block_dim
+
+
+def kernel_geometry(layout: RowLayout, own: Ownership) -> tuple[int, int]:
+    """(NB, DLAT) of the decode kernels for an owner's units. Units serving the same heads are
+    kernel branches (MLRA-4, MLA). Units serving different head sets (MLRA-2, GLA) run on the
+    same kernels with block-diagonal weights: every branch computes every local head and the
+    weights of (unit, head) pairs the unit does not serve are zero, so those contributions
+    vanish in the up-projection. Narrow units (<= 128 columns) stay separate branches (the
+    kernel keeps up to 4); wide ones (GLA-2 at TP1: 2 x 256) are concatenated into one branch
+    of their summed width (the MLA geometry)."""
+    nu, dlp = layout.nb, layout.dlp
+    if nu in (1, 2, 4) and (dlp <= 128 or nu == 1):
+        return nu, dlp
+    if (nu * dlp) % 128 == 0 and nu * dlp <= 512:
+        return 1, nu * dlp
+    raise ConfigError(f"no kernel geometry for {nu} latent units of width {dlp}")
 
 
 def row_layout(cfg: AttnConfig, own: Ownership):
@@ -109,7 +135,12 @@ def new_cache(cfg: AttnConfig, own: Ownership | None = None, pos_offset: int = 0
 def _unit_weight_slices(cfg: AttnConfig, w, unit: LatentUnit) -> tuple[np.ndarray, np.ndarray]:
     """(latent, m, d_h) key/value up-projection slices (decode.py:170-187)."""
     heads = list(unit.heads)
-    w_uk, w_uv = w["w_uk"], w["w_uv"]
+    if unit.group < 0:
+        w_uk, w_uv = w["w_uk"], w["w_uv"]
+    else:  # grouped latents: the group's own up-projections, heads indexed within the group
+        w_uk, w_uv = w[f"w_uk_{unit.group}"], w[f"w_uv_{unit.group}"]
+        r = cfg.h // cfg.g
+        heads = [i - unit.group * r for i in heads]
     if unit.block >= 0:
         bs = cfg.block_dim
         w_uk = w_uk[unit.block * bs:(unit.block + 1) * bs]
@@ -120,20 +151,25 @@ def _unit_weight_slices(cfg: AttnConfig, w, unit: LatentUnit) -> tuple[np.ndarra
 
 class LocalWeights(dict):
     """``{"uk:<stream>": (latent, m, d_h), "uv:<stream>": ...}`` like decode.py:190-199, with a
-    cached device pack: w_uk [m, d_h, NU*dlp] and w_uv [m, NU*dlp, d_h] (bf16, zero-padded)."""
+    cached device pack over the owner's heads: w_uk [m, d_h, NU*dlp] and w_uv [m, NU*dlp, d_h]
+    (bf16, zero-padded; zero where a unit does not serve a head -- see kernel_geometry)."""
 
-    def packed(self, layout: RowLayout, device) -> tuple[torch.Tensor, torch.Tensor]:
-        key = ("__packed__", layout, str(device))
+    def packed(self, layout: RowLayout, device, own: Ownership | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        key = ("__packed__", layout, str(device), None if own is None else (own.heads, own.units))
         if key not in self.__dict__:
             uks = [np.asarray(self[f"uk:{u}"]) for u in layout.units]
             uvs = [np.asarray(self[f"uv:{u}"]) for u in layout.units]
-            m, dh = uks[0].shape[1], uks[0].shape[2]
+            dh = uks[0].shape[2]
+            heads = list(own.heads) if own is not None else list(range(uks[0].shape[1]))
+            unit_heads = [list(u.heads) for u in own.units] if own is not None else [heads] * len(uks)
+            m = len(heads)
             nu, dlp, dl = layout.nb, layout.dlp, layout.dl
             uk = np.zeros((m, dh, nu * dlp), dtype=np.float32)
             uv = np.zeros((m, nu * dlp, dh), dtype=np.float32)
             for i, (a, b) in enumerate(zip(uks, uvs)):
-                uk[:, :, i * dlp:i * dlp + dl] = np.transpose(a, (1, 2, 0))  # (lat, m, dh) -> (m, dh, lat)
-                uv[:, i * dlp:i * dlp + dl, :] = np.transpose(b, (1, 0, 2))  # (lat, m, dh) -> (m, lat, dh)
+                rows = [heads.index(hd) for hd in unit_heads[i]]
+                uk[rows, :, i * dlp:i * dlp + dl] = np.transpose(a, (1, 2, 0))  # (lat, m, dh) -> (m, dh, lat)
+                uv[rows, i * dlp:i * dlp + dl, :] = np.transpose(b, (1, 0, 2))  # (lat, m, dh) -> (m, lat, dh)
             self.__dict__[key] = (torch.as_tensor(uk, device=device).to(torch.bfloat16).contiguous(),
                                   torch.as_tensor(uv, device=device).to(torch.bfloat16).contiguous())
         return self.__dict__[key]
@@ -185,15 +221,16 @@ def _queries_to_device(cfg: AttnConfig, layout: RowLayout, q_nope, q_rope, heads
     return qn.to(torch.bfloat16)[None].contiguous(), qr.to(torch.bfloat16)[None].contiguous()
 
 
-def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, qn, qr, upproj: int, alpha: float):
+def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, own: Ownership, qn, qr, upproj: int,
+               alpha: float):
     layout = cache.layout
     dev = cache.paged.device
-    w_uk, w_uv = lw.packed(layout, dev)
-    sub, dls = layout.geometry
-    nb = layout.nb
+    w_uk, w_uv = lw.packed(layout, dev, own)
+    nb, dlat = kernel_geometry(layout, own)
+    sub, dls = ops.latent_geometry(dlat)
     pc = cache.paged
     nsplit = ops.default_splits(1, max(cache.n, 1), nb, sub)
-    q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, nb, layout.dlp, ops.score_scale(cfg.tau))
+    q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, nb, dlat, ops.score_scale(cfg.tau))
     o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, pc.block_table, pc.seqlens, pc.page_size, nb, sub, dls,
                                       nsplit)
     return ops.combine(o_part, lse, w_uv, alpha, per_branch=(upproj == 2))
@@ -214,19 +251,19 @@ def attend_local(cfg: AttnConfig, local_w, own: Ownership, cache: PagedLatentCac
         return attend_local_gqa(cfg, own, cache, queries)
     if cache.n == 0:
         raise ConfigError("cache read: stream 'rope' is empty")
-    heads = list(own.units[0].heads)
-    if any(list(u.heads) != heads for u in own.units):
-        raise ConfigError("B200 path: all units of one owner must serve the same heads")
+    heads = list(own.heads)
     if not isinstance(local_w, LocalWeights):
         lw = LocalWeights(local_w)
     else:
         lw = local_w
     qn, qr = _queries_to_device(cfg, cache.layout, queries["q_nope"], queries["q_rope"], heads, cache.paged.device)
-    per_unit = _run_units(cfg, cache, lw, qn, qr, upproj=2, alpha=1.0)[0].double().cpu().numpy()
+    per_branch = _run_units(cfg, cache, lw, own, qn, qr, upproj=2, alpha=1.0)[0].double().cpu().numpy()
     cache.reads += cache.n * cache.row_elements()
+    merged = per_branch.shape[0] != len(own.units)  # units concatenated into one kernel branch
     contribs = []
-    for i, _unit in enumerate(own.units):
-        contribs.extend((head, per_unit[i, j]) for j, head in enumerate(heads))
+    for i, unit in enumerate(own.units):
+        row = per_branch[0 if merged else i]
+        contribs.extend((head, row[heads.index(head)]) for head in unit.heads)
     return contribs
 
 
@@ -273,25 +310,36 @@ def _state(cfg: AttnConfig, w, device) -> _StepState:
     return st
 
 
-def _owned_blocks(cfg: AttnConfig, layout: RowLayout) -> tuple[int, int, int]:
-    """(branches, first block, block count) of a latent layout's units, for the fused K0."""
+def _write_plan(cfg: AttnConfig, own: Ownership) -> tuple[list, int, int, int, int]:
+    """What the fused K0 needs for an owner: (raw down-projection names concatenated into
+    kv_raw, blocks per kv_raw row, first owned block, owned block count, RMS groups)."""
+    units = list(own.units)
     if cfg.variant == "mla":
-        return 1, 0, 1
-    blocks = [int(u.rsplit("_b", 1)[1]) for u in layout.units]
-    if blocks != list(range(blocks[0], blocks[0] + len(blocks))):
-        raise ConfigError(f"owned latent blocks {blocks} are not contiguous")
-    return 4, blocks[0], len(blocks)
+        return ["w_dkv"], 1, 0, 1, 1
+    if cfg.variant == "mlra" and cfg.branches == 4:
+        blocks = [u.block for u in units]
+        if blocks != list(range(blocks[0], blocks[0] + len(blocks))):
+            raise ConfigError(f"owned latent blocks {blocks} are not contiguous")
+        return ["w_dkv"], 4, blocks[0], len(blocks), 1  # the RMS spans the whole latent
+    # grouped latents: each group normalised over its own latent (latent.py:145-158)
+    groups = sorted({u.group for u in units})
+    per_group = 1 if cfg.variant == "gla" else 2
+    idx = [groups.index(u.group) * per_group + max(u.block, 0) for u in units]
+    if idx != list(range(idx[0], idx[0] + len(idx))):
+        raise ConfigError(f"owned latent units {[u.stream for u in units]} are not contiguous")
+    return [f"w_dkv_{j}" for j in groups], per_group * len(groups), idx[0], len(idx), len(groups)
 
 
 def append_token_latent(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, hidden: torch.Tensor,
-                        pos: int) -> None:
+                        pos: int, own: Ownership | None = None) -> None:
     """Write side of one decode step for a latent-family cache: the raw down-projections
-    (h W^DKV, h W^KR -- pre-attention GEMVs, torch) then the fused K0 kernel (rmsnorm*alpha_kv,
-    owned blocks, rope, padding, paged append)."""
-    branches, block0, nblocks = _owned_blocks(cfg, cache.layout)
+    (h W^DKV, h W^KR -- pre-attention GEMVs, torch) then the fused K0 kernel (rmsnorm*alpha_kv
+    per latent group, owned blocks, rope, padding, paged append)."""
+    names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, own or st.own)
     proj = st.projector
-    cache.append_latent(hidden @ proj.w_dkv, hidden @ proj.w_kr, pos, branches=branches, block0=block0,
-                        nblocks=nblocks, alpha_kv=proj.alpha_kv)
+    kv_raw = torch.cat([hidden @ proj.w[n] for n in names], dim=-1)
+    cache.append_latent(kv_raw, hidden @ proj.w_kr, pos, branches=blocks, block0=block0, nblocks=nblocks,
+                        alpha_kv=proj.alpha_kv, norm_groups=norm_groups)
 
 
 def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tuple[np.ndarray, PagedLatentCache]:
@@ -313,7 +361,7 @@ def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tu
     q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
     qn, qr = _queries_to_device(cfg, cache.layout, q_nope[0], q_rope[0], list(range(cfg.h)), dev)
     alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
-    out = _run_units(cfg, cache, st.lw, qn, qr, upproj=1, alpha=alpha)
+    out = _run_units(cfg, cache, st.lw, st.own, qn, qr, upproj=1, alpha=alpha)
     cache.reads += cache.n * cache.row_elements()
     return out[0].double().cpu().numpy(), cache
 
@@ -346,19 +394,19 @@ class DecodeEngine:
         self.own = own or full_ownership(cfg)
         self.layout = row_layout(cfg, self.own)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.heads = list(self.own.units[0].heads)
+        self.heads = list(self.own.heads)
         self.cache = PagedCache(self.layout, batch, max_tokens, page_size, self.device, page_order)
         lw = local_weights(cfg, w, self.own)
-        self.w_uk, self.w_uv = lw.packed(self.layout, self.device)
-        self.sub, self.dls = self.layout.geometry
+        self.w_uk, self.w_uv = lw.packed(self.layout, self.device, self.own)
+        self.nb, self.dlat = kernel_geometry(self.layout, self.own)
+        self.sub, self.dls = ops.latent_geometry(self.dlat)
         self.scale = ops.score_scale(cfg.tau)
         if alpha is None:
             alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
         self.alpha = float(alpha)
-        self.nsplit = nsplit or ops.default_splits(batch, max_tokens, self.layout.nb, self.sub)
+        self.nsplit = nsplit or ops.default_splits(batch, max_tokens, self.nb, self.sub)
         hl = len(self.heads)
-        self.workspace = ops.DecodeWorkspace(batch, hl, self.layout.nb, self.layout.dlp, self.layout.drp, self.nsplit,
-                                             self.device)
+        self.workspace = ops.DecodeWorkspace(batch, hl, self.nb, self.dlat, self.layout.drp, self.nsplit, self.device)
         self.out = torch.empty((batch, hl, cfg.d_h), dtype=torch.float32, device=self.device)
 
     @property
@@ -378,5 +426,5 @@ class DecodeEngine:
         queries on this device -> fp32 [B, h_local, d_h] (alpha-scaled, branch-summed)."""
         c = self.cache
         return ops.decode_step(q_nope, q_rope, self.w_uk, self.w_uv, c.pool, c.block_table, c.seqlens, c.page_size,
-                               self.layout.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
+                               self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
                                self.workspace, out=self.out if out is None else out)

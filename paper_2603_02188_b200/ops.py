@@ -58,7 +58,7 @@ def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch
 def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor, slots: torch.Tensor,
                         block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
                         nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
-                        eps: float = 1e-6) -> None:
+                        eps: float = 1e-6, norm_groups: int = 1) -> None:
     """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
     rope_pos, padded, appended as one bf16 pool row per sequence at slots[s]."""
     _need(kv_raw, torch.float32, "kv_raw", 2)
@@ -74,7 +74,8 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
     rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(), rope_pos.data_ptr(),
                                               slots.data_ptr(), block_table.data_ptr(), B, d_c, branches, block0,
                                               nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
-                                              page_size, block_table.shape[1], pool.data_ptr(), _stream())
+                                              page_size, block_table.shape[1], norm_groups, pool.data_ptr(),
+                                              _stream())
     _lib.check(rc, "mlra_cache_append_latent")
 
 

@@ -42,7 +42,10 @@ class LatentProjector:
         self.cfg = cfg
         f = lambda name: torch.as_tensor(w[name], dtype=torch.float32, device=device)  # noqa: E731
         self.w_dq, self.w_uq, self.w_qr, self.w_kr = f("w_dq"), f("w_uq"), f("w_qr"), f("w_kr")
-        self.w_dkv = f("w_dkv")
+        # every raw down-projection by name (w_dkv, or w_dkv_<j> per latent group)
+        names = list(w.tensors) if hasattr(w, "tensors") else list(w.keys())  # WeightSet or plain dict
+        self.w = {n: f(n) for n in names if str(n).startswith("w_dkv")}
+        self.w_dkv = self.w.get("w_dkv")
         sf = calib_factors(cfg)
         self.alpha_q, self.alpha_kv = sf.alpha_q, sf.alpha_kv
 
@@ -63,7 +66,7 @@ class LatentProjector:
         q_nope = (c_q @ self.w_uq).reshape(n, cfg.h, cfg.d_h)
         q_rope = rope_rotate((c_q @ self.w_qr).reshape(n, cfg.h, cfg.d_h_rope), positions)
         k_rope = rope_rotate(hidden @ self.w_kr, positions)
-        c_kv = self.alpha_kv * rmsnorm(hidden @ self.w_dkv)
+        c_kv = self.alpha_kv * rmsnorm(hidden @ self.w_dkv) if self.w_dkv is not None else None
         return q_nope, q_rope, k_rope, c_kv
 
 

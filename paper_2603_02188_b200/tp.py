@@ -61,6 +61,31 @@ def shard_ownership(cfg: AttnConfig, phi: int, device_id: int) -> Ownership:  # 
     if cfg.variant == "mla":
         heads = _ranges(h, phi, "query-head axis")[k]
         return Ownership(heads, units=(LatentUnit(-1, -1, heads),))
+    if cfg.variant == "gla":  # latent-group axis, then the heads of one group (tpsim.py:92-106)
+        g, r = cfg.g, h // cfg.g
+        if phi <= g:
+            units = tuple(LatentUnit(j, -1, tuple(range(j * r, (j + 1) * r)))
+                          for j in _ranges(g, phi, "latent-group axis")[k])
+            return Ownership(tuple(i for u in units for i in u.heads), units=units)
+        per_group = phi // g
+        if phi % g != 0 or r % per_group != 0:
+            raise ConfigError(f"gla: cannot split {r} heads per group across {per_group} devices")
+        group = k // per_group
+        heads = tuple(i + group * r for i in _ranges(r, per_group, "query-head axis")[k % per_group])
+        return Ownership(heads, units=(LatentUnit(group, -1, heads),))
+    if cfg.branches == 2:  # mlra-2: (group, block) units, group-first (tpsim.py:117-131)
+        pairs = [(grp, b) for grp in range(2) for b in range(2)]
+        half_heads = [tuple(range(grp * (h // 2), (grp + 1) * (h // 2))) for grp in range(2)]
+        if phi == 1:
+            return Ownership(all_heads, units=tuple(LatentUnit(grp, b, half_heads[grp]) for grp, b in pairs))
+        if phi == 2:
+            return Ownership(half_heads[k], units=tuple(LatentUnit(k, b, half_heads[k]) for b in range(2)))
+        if phi == 4:
+            grp, b = pairs[k]
+            return Ownership(half_heads[grp], units=(LatentUnit(grp, b, half_heads[grp]),))
+        grp, b = pairs[k // 2]
+        heads = tuple(i + grp * (h // 2) for i in _ranges(h // 2, 2, "query-head axis")[k % 2])
+        return Ownership(heads, units=(LatentUnit(grp, b, heads),))
     if phi <= 4:
         blocks = _ranges(4, phi, "latent-block axis")[k]
         return Ownership(all_heads, units=tuple(LatentUnit(-1, b, all_heads) for b in blocks))
@@ -189,7 +214,7 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
             continue
         hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32,
                                  device=dev)
-        append_token_latent(cfg, st, shard.cache, hidden, pos)  # fused K0 (owned blocks)
+        append_token_latent(cfg, st, shard.cache, hidden, pos, shard.own)  # fused K0 (owned blocks)
         q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
         queries = {"q_nope": q_nope[0].double().cpu().numpy(), "q_rope": q_rope[0].double().cpu().numpy()}
         by_device[shard.device_id] = attend_local(cfg, shard.attn_weights, shard.own, shard.cache, queries)

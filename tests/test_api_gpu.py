@@ -21,7 +21,8 @@ def _mlra():
     return mlra
 
 
-@pytest.mark.parametrize("name", ["tiny_mlra4", "refdims_mlra4", "refdims_mla", "p_mlra4"])
+@pytest.mark.parametrize("name", ["tiny_mlra4", "refdims_mlra4", "refdims_mla", "p_mlra4", "p_mlra2", "p_gla2",
+                                  "refdims_mlra2", "refdims_gla2"])
 def test_decode_steps_track_reference(name):
     """absorbed_decode_step token by token from an empty cache; every step's output is
     compared with the oracle (f64) and the last one with the reference's golden output."""
@@ -147,3 +148,27 @@ def test_sim_decode_order_and_errors():
         mlra.sim_decode(a, hidden[0], order=[0, 0, 1, 2])
     with pytest.raises(mlra.ConfigError):
         mlra.make_shards(cfg, w, 16)
+
+
+@pytest.mark.parametrize("name", ["refdims_mlra2", "refdims_gla2", "p_mlra2", "p_gla2"])
+def test_grouped_latent_sim_decode_matches_reference(name):
+    """MLRA-2 / GLA on the shared kernels under tpsim sharding: every TP degree the reference
+    allows reproduces its golden output and per-device ledger."""
+    mlra = _mlra()
+    meta, arrays = load(name)
+    ocfg, w, hidden = regen(meta)
+    cfg = mlra.AttnConfig(**meta["cfg"])
+    n = meta["n"]
+    for phi_s, rec in meta["tp"].items():
+        phi = int(phi_s)
+        if "error" in rec:
+            with pytest.raises(mlra.ConfigError):
+                mlra.make_shards(cfg, w, phi)
+            continue
+        shards = mlra.make_shards(cfg, w, phi)
+        out = ledger = None
+        for t in range(n):
+            out, ledger = mlra.sim_decode(shards, hidden[t])
+        assert ak.max_rel_err(arrays[f"out_tp{phi}"], out) <= TOL, phi
+        assert ledger.to_json_dict()["per_token_load_dh"] == rec["ledger"], phi
+        assert ledger.reduction == rec["reduction"]

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 def _check(variant, own_blocks, positions):
     import paper_2603_02188_b200 as mlra
     from paper_2603_02188_b200.cache import PagedCache
-    from paper_2603_02188_b200.decode import _owned_blocks, full_ownership, row_layout
+    from paper_2603_02188_b200.decode import _write_plan, full_ownership, row_layout
     from paper_2603_02188_b200.tp import shard_ownership
 
     cfg = mlra.trained_config("mla" if variant == "mla" else "mlra4").with_(d=512)
@@ -29,12 +29,12 @@ def _check(variant, own_blocks, positions):
     dev = torch.device("cuda", 0)
     cache = PagedCache(lay, B, 256, 64, dev)
     h = torch.tensor(hidden, dtype=torch.float32, device=dev)
-    branches, block0, nblocks = _owned_blocks(cfg, lay)
+    _, branches, block0, nblocks, norm_groups = _write_plan(cfg, own)
     alpha_kv = ak.calib_alphas(ocfg)[1]
     kv_raw = torch.tensor(hidden @ w["w_dkv"], dtype=torch.float32, device=dev)
     kr_raw = torch.tensor(hidden @ w["w_kr"], dtype=torch.float32, device=dev)
     cache.append_latent(kv_raw, kr_raw, positions, branches=branches, block0=block0, nblocks=nblocks,
-                        alpha_kv=alpha_kv)
+                        alpha_kv=alpha_kv, norm_groups=norm_groups)
     torch.cuda.synchronize()
     del h
     for s, pos in enumerate(positions):

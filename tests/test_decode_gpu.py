@@ -28,8 +28,9 @@ def _mlra():
 
 def _bf16_weights(w):
     out = dict(w)
-    out["w_uk"] = ak.bf16_round(w["w_uk"])
-    out["w_uv"] = ak.bf16_round(w["w_uv"])
+    for k in w:
+        if k.startswith(("w_uk", "w_uv")):  # single latent or per-group up-projections
+            out[k] = ak.bf16_round(w[k])
     return out
 
 
@@ -60,7 +61,8 @@ def _oracle_cfg(cfg):
     return ak.cfg_from(cfg)
 
 
-@pytest.mark.parametrize("name", ["tiny_mlra4", "p_mlra4", "p_mla", "refdims_mlra4", "refdims_mla"])
+@pytest.mark.parametrize("name", ["tiny_mlra4", "p_mlra4", "p_mla", "refdims_mlra4", "refdims_mla", "p_mlra2", "p_gla2",
+                                  "refdims_mlra2", "refdims_gla2"])
 def test_engine_matches_oracle_and_reference(name):
     mlra = _mlra()
     meta, arrays = load(name)

@@ -82,6 +82,48 @@ def test_shard_ownership_rules():
         shard_ownership(trained_config("mla").with_(variant="mha"), 2, 0)
 
 
+@pytest.mark.parametrize("name", ["mlra2", "gla2", "gla4"])
+@pytest.mark.parametrize("phi", [1, 2, 4, 8])
+def test_grouped_latent_shard_ownership_matches_oracle(name, phi):
+    """tpsim.py:58-131 for MLRA-2 and GLA (2.9B shapes): same heads and units as the oracle."""
+    from oracle import attnkit_port as ak
+    from paper_2603_02188_b200.tp import shard_ownership
+
+    cfg = trained_config(name)
+    ocfg = ak.cfg_from(cfg)
+    for k in range(phi):
+        try:
+            heads, units = ak.shard_units(ocfg, phi, k)
+        except ak.OracleError:
+            with pytest.raises(ConfigError):
+                shard_ownership(cfg, phi, k)
+            continue
+        own = shard_ownership(cfg, phi, k)
+        assert own.heads == tuple(heads)
+        assert [(u.stream, u.group, u.block, u.heads) for u in own.units] == [tuple(u) for u in units]
+
+
+def test_grouped_latent_kernel_geometry_and_packing():
+    """MLRA-2 / GLA units with different head sets: block-diagonal packs on the shared kernels."""
+    import torch
+
+    from paper_2603_02188_b200.decode import full_ownership, kernel_geometry, local_weights, row_layout
+
+    for name, geom in (("mlra2", (4, 128)), ("gla2", (1, 512)), ("gla4", (4, 128))):
+        cfg = trained_config(name).with_(d=64)
+        w = mlra.build_weights(cfg, 0.02, mlra.Rng(3))
+        own = full_ownership(cfg)
+        lay = row_layout(cfg, own)
+        assert kernel_geometry(lay, own) == geom
+        uk, uv = local_weights(cfg, w, own).packed(lay, torch.device("cpu"), own)
+        assert tuple(uk.shape) == (24, 128, 512) and tuple(uv.shape) == (24, 512, 128)
+        for i, u in enumerate(own.units):  # zero where the unit does not serve the head
+            cols = slice(i * lay.dlp, (i + 1) * lay.dlp)
+            others = [hd for hd in range(24) if hd not in u.heads]
+            assert float(uk[others][:, :, cols].abs().max()) == 0.0
+            assert float(uk[list(u.heads)][:, :, cols].abs().max()) > 0.0
+
+
 @pytest.mark.parametrize("shape,phi", [("2.9b", 1), ("2.9b", 2), ("kimi", 1), ("kimi", 4), ("kimi", 8)])
 def test_gqa_shard_ownership_matches_oracle(shape, phi):
     """tpsim.py:58-131 for gqa (g=6 at the 2.9B shape, g=8 at the Kimi context shape):
@@ -171,8 +213,11 @@ def test_decode_routing_errors():
     with pytest.raises(RoutingError):
         full_ownership(trained_config("mla").with_(variant="mha"))
     cfg = AttnConfig("mlra", branches=2, h=4, d=32, d_h=8, d_h_rope=4, d_c=32, d_cq=16)
+    own = full_ownership(cfg)  # mlra-2: (group, block) units over half the heads each
+    assert [(u.group, u.block, u.heads) for u in own.units] == [(0, 0, (0, 1)), (0, 1, (0, 1)), (1, 0, (2, 3)),
+                                                                (1, 1, (2, 3))]
     with pytest.raises(RoutingError):
-        full_ownership(cfg)
+        full_ownership(trained_config("mla").with_(variant="tpa"))
     with pytest.raises(RoutingError):
         decode_step(trained_config("mlra4"), None, None, None, mode="turbo")
     with pytest.raises(RoutingError):

@@ -29,12 +29,12 @@ cases = [("mlra4 tp1", trained_config("mlra4"), None), ("mlra4 tp4 rank", traine
 for name, cfg, own in cases:
     eng, qn, qr = bench.make_engine(cfg, own, B, CTX, 1, dev)
     c = eng.cache
-    q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale)
-    parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub, eng.dls, eng.nsplit)
+    q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.nb, eng.dlat, eng.scale)
+    parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub, eng.dls, eng.nsplit)
     out = ops.combine(*parts, eng.w_uv, eng.alpha)
-    scratch = torch.empty((B, len(eng.heads), eng.layout.nb * eng.layout.dlp), dtype=torch.float32, device=dev)
-    t1 = gtime(lambda: ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale, out=(q_abs, q_rs)))
-    t2 = gtime(lambda: ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub, eng.dls, eng.nsplit, out=parts))
+    scratch = torch.empty((B, len(eng.heads), eng.nb * eng.dlat), dtype=torch.float32, device=dev)
+    t1 = gtime(lambda: ops.absorb_query(qn, qr, eng.w_uk, eng.nb, eng.dlat, eng.scale, out=(q_abs, q_rs)))
+    t2 = gtime(lambda: ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub, eng.dls, eng.nsplit, out=parts))
     t3 = gtime(lambda: ops.combine(*parts, eng.w_uv, eng.alpha, out=out, scratch=scratch))
     tstep = gtime(lambda: eng.decode_attention(qn, qr))
     print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  step {tstep:.1f} us  (graph replay, K2 back-to-back on one cache: L2-warm)", flush=True)

@@ -11,8 +11,8 @@ for name, cfg, own in [("tp1", trained_config("mlra4"), None),
     eng, qn, qr = bench.make_engine(cfg, own, 16, 32768, 1, dev)
     c = eng.cache
     for _ in range(3):
-        q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.layout.nb, eng.layout.dlp, eng.scale)
-        parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.layout.nb, eng.sub, eng.dls, eng.nsplit)
+        q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.nb, eng.dlat, eng.scale)
+        parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub, eng.dls, eng.nsplit)
         out = ops.combine(*parts, eng.w_uv, eng.alpha)
     torch.cuda.synchronize()
     print(name, "done", flush=True)
