@@ -121,8 +121,12 @@ def make_engine(cfg, own, batch, ctx, seed, device, page_size=128):
 
     g = torch.Generator(device=device).manual_seed(seed)
     rng = np.random.default_rng(seed)
-    w = {"w_uk": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02,
-         "w_uv": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02}
+    if cfg.variant == "gla" or (cfg.variant == "mlra" and cfg.branches == 2):  # per-group up-projections
+        r, dg = cfg.h // cfg.g, cfg.d_c // cfg.g
+        w = {f"{n}_{j}": rng.standard_normal((dg, r * cfg.d_h)) * 0.02 for n in ("w_uk", "w_uv") for j in range(cfg.g)}
+    else:
+        w = {"w_uk": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02,
+             "w_uv": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02}
     eng = DecodeEngine(cfg, w, own, batch=batch, max_tokens=ctx + 64, page_size=page_size, device=device)
     lay = eng.layout
     akv = calib_factors(cfg).alpha_kv
@@ -544,6 +548,18 @@ def per_gpu_comparisons(cfg, device, args):
                        "algorithmic_bytes": nbytes}
         del r
         torch.cuda.empty_cache()
+    # the other latent variants on the same kernels, per TP rank
+    v_res = {}
+    for name, phi in (("mlra2", 4), ("gla2", 2)):
+        c = trained_config(name)
+        r = StepRunner(c, shard_ownership(c, phi, 0), BATCH_PER_GROUP, CTX, device)
+        ms = time_graph_steps(r, args.steps, args.warmup, torch.cuda.synchronize)
+        nbytes = algorithmic_bytes(c, phi, [CTX] * BATCH_PER_GROUP)
+        v_res[f"{name}_tp{phi}_rank"] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                                         "algorithmic_bytes": nbytes}
+        del r
+        torch.cuda.empty_cache()
+    out["latent_variants"] = v_res
     out["vs_gqa"] = {
         "gqa_tp1": g_res["gqa_tp1"], "gqa_tp2_rank": g_res["gqa_tp2_rank"],
         "mlra4_tp4_rank_us": res["mlra4_tp4_rank"]["us_per_step"],
