@@ -292,49 +292,71 @@ def time_k2_alone(eng_qs, iters):
     return e0.elapsed_time(e1) / (reps * per)
 
 
-def e2e_steps(eng, steps, warmup):
-    """The plugin call a user makes, with HOST buffers: per step H2D of the new token's
-    cache row and queries (pinned), K0 append + K1..K3 through the C ABI, D2H of the output."""
+def e2e_steps(engines, steps, warmup):
+    """The plugin calls a user makes, with HOST buffers, every step: one H2D of the new token's
+    cache rows + queries from pinned memory, K0 (append, advancing seqlens) + K1..K3 through
+    the C ABI, one D2H of the fp32 output. Two micro-batches (the two caches) are stepped in
+    turn by host_loop.MicroBatchLoop: micro-batch k+1's upload and k-1's download overlap k's
+    kernels. Also returns the serial time (one micro-batch, copies in line on one stream)."""
     import torch
 
     from paper_2603_02188_b200 import ops
+    from paper_2603_02188_b200.host_loop import MicroBatchLoop
 
-    B = eng.batch
-    lay = eng.layout
-    hl = len(eng.heads)
-    h_rows = torch.randn((B, lay.width)).to(torch.bfloat16).pin_memory()
-    h_qn = torch.randn((B, hl, eng.cfg.d_h)).to(torch.bfloat16).pin_memory()
-    h_qr = torch.randn((B, hl, lay.drp)).to(torch.bfloat16).pin_memory()
-    h_out = torch.empty((B, hl, eng.cfg.d_h), dtype=torch.float32).pin_memory()
-    d_rows = torch.empty_like(h_rows, device=eng.device)
-    d_qn = torch.empty_like(h_qn, device=eng.device)
-    d_qr = torch.empty_like(h_qr, device=eng.device)
+    loop = MicroBatchLoop(engines)
+    g = torch.Generator().manual_seed(7)
+    for k in range(len(loop)):
+        for t in loop.host_inputs(k):
+            t.copy_(torch.randn(t.shape, generator=g).to(torch.bfloat16))
+    start_lens = [e.cache.lengths() for e in engines]
+
+    def run(n):
+        for i in range(n):
+            loop.submit(i % len(loop))
+
+    run(warmup * len(loop))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    loop.start()
+    t0 = time.perf_counter()
+    e0.record()
+    run(steps)
+    loop.join()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    piped = max(e0.elapsed_time(e1) / 1e3, wall) / steps
+
+    # serial reference point: same calls, one micro-batch, every copy in line
+    eng = engines[0]
     c = eng.cache
+    h_in = loop.host_inputs(0)
+    d_in = [torch.empty_like(t, device=eng.device) for t in h_in]
+    h_out = loop.host_output(0)
 
     def one():
-        d_rows.copy_(h_rows, non_blocking=True)
-        d_qn.copy_(h_qn, non_blocking=True)
-        d_qr.copy_(h_qr, non_blocking=True)
-        ops.cache_append(d_rows, c.block_table, c.seqlens, c.pool, c.page_size)
-        c.seqlens += 1
-        out = ops.decode_step(d_qn, d_qr, eng.w_uk, eng.w_uv, c.pool, c.block_table, c.seqlens, c.page_size,
-                              lay.nb, eng.sub, eng.dls, eng.nsplit, eng.scale, eng.alpha, eng.workspace, out=eng.out)
-        h_out.copy_(out, non_blocking=True)
+        for d, h in zip(d_in, h_in):
+            d.copy_(h, non_blocking=True)
+        c.reserve_token()
+        ops.cache_append(d_in[0], c.block_table, c.seqlens, c.pool, c.page_size, advance=True)
+        h_out.copy_(eng.decode_attention(d_in[1], d_in[2]), non_blocking=True)
 
+    nser = max(3, steps // 2)
     for _ in range(warmup):
         one()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(steps):
+    for _ in range(nser):
         one()
     e1.record()
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    c.seqlens -= steps + warmup
-    bytes_in = h_rows.numel() * 2 + h_qn.numel() * 2 + h_qr.numel() * 2
-    return max(e0.elapsed_time(e1) / 1e3, wall) / steps, bytes_in, h_out.numel() * 4
+    serial = max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0) / nser
+    for e, lens in zip(engines, start_lens):  # back to the benchmark context
+        e.cache.seqlens.copy_(torch.tensor(lens, dtype=torch.int32))
+        e.cache._host_lens = list(lens)
+    bin_, bout = loop.bytes_per_step(0)
+    return piped, serial, bin_, bout
 
 
 # ----------------------------------------------------------------------------- CPU side
@@ -466,14 +488,17 @@ def run_ours(args):
                               "kernel": "mlra_decode_kernel (K2)", "kernel_us": round(k2_ms * 1e3, 2),
                               "algorithmic_bytes_per_launch": k2_bytes, "peak_kind": f"{peak_kind} copy (burst)"}
         extras["clocks"] = clk.summary()
-        eng = runner.engines[0][0]
-        e2e_s, bin_, bout = e2e_steps(eng, max(3, args.steps // 2), args.warmup)
+        e2e_s, ser_s, bin_, bout = e2e_steps([e for e, _, _ in runner.engines], max(4, args.steps), args.warmup)
         # e2e is a single-GPU call through the C ABI; at N>1 it measures this rank's share
         e2e_bytes = bytes_rank * (n_gpus if world == 1 else 1)
         extras["e2e"] = {"value": round(e2e_bytes / e2e_s / 1e9, 1), "unit": "GB/s", "h2d_bytes_per_step": bin_,
                          "d2h_bytes_per_step": bout, "ms_per_step": round(e2e_s * 1e3, 4),
-                         "path": "mlra_cache_append + mlra_decode_step (C ABI), pinned host buffers"
-                                 + ("" if world == 1 else ", rank 0 share (no collective)")}
+                         "serial_ms_per_step": round(ser_s * 1e3, 4),
+                         "path": "host_loop.MicroBatchLoop: per step 1 H2D (pinned rows+queries), mlra_cache_append "
+                                 "(advance) + mlra_decode_step (C ABI), 1 D2H; 2 micro-batches, copies on side "
+                                 "streams overlapping the other micro-batch's kernels; serial_ms_per_step = same "
+                                 "calls on one stream, no overlap"
+                                 + ("" if world == 1 else "; rank 0 share (no collective)")}
         if n_gpus == 1 and not args.quick:
             extras.update(per_gpu_comparisons(cfg, device, args))
         if n_gpus == 1 and not args.no_cpu:

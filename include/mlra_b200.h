@@ -49,9 +49,12 @@ int mlra_num_sms(void);
  *   rows        [B, W] bf16, W = NB*DLAT + DR  ([latent block 0 | ... | rope])
  *   block_table [B, max_pages] int32 page ids; positions [B] int32 token slot to write
  *   pool        [num_pages*page_size, W] bf16
+ *   advance     != 0: positions[s] += 1 after the write, as the reference append grows the
+ *               cache (cache.py:44-57); pass the sequence lengths as positions. 0 leaves
+ *               positions untouched.
  */
-int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_t* positions, int B, int W,
-                      int page_size, int max_pages, void* pool, void* stream);
+int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* positions, int B, int W,
+                      int page_size, int max_pages, int advance, void* pool, void* stream);
 
 /*
  * K0 (fused write side) -- the cache half of latent.py:129-159 (latent_projections) plus
@@ -64,12 +67,13 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_
  *           rope_base^(-2l/dr)), zero-padded to drp
  *   pool row [c_kv blocks | k_rope] bf16 written at slot slots[s] of sequence s.
  *   kv_raw [B, d_c] fp32 = h W^DKV (whole groups: the RMS spans a group's blocks), kr_raw
- *   [B, dr] fp32 = h W^KR. MLA: branches = 1.
+ *   [B, dr] fp32 = h W^KR. MLA: branches = 1. advance != 0: slots[s] += 1 after the write
+ *   (slots are then the sequence lengths, as in mlra_cache_append).
  */
-int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, const int32_t* slots,
+int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, int32_t* slots,
                              const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
                              int dlp, int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size,
-                             int max_pages, int norm_groups, void* pool, void* stream);
+                             int max_pages, int norm_groups, int advance, void* pool, void* stream);
 
 /*
  * K1 -- query absorption (decode.py:155-167 absorb_query, applied per branch at :224).

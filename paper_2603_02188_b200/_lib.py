@@ -27,8 +27,8 @@ SIGNATURES = {
     "mlra_version": (_I, []),
     "mlra_last_error": (ctypes.c_char_p, []),
     "mlra_num_sms": (_I, []),
-    "mlra_cache_append": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P]),
-    "mlra_cache_append_latent": (_I, [_P] * 5 + [_I] * 8 + [_F, _F, _F, _I, _I, _I, _P, _P]),
+    "mlra_cache_append": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P]),
+    "mlra_cache_append_latent": (_I, [_P] * 5 + [_I] * 8 + [_F, _F, _F, _I, _I, _I, _I, _P, _P]),
     "mlra_absorb_query": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P]),
     "mlra_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "mlra_default_splits": (_I, [_I, _I, _I, _I]),

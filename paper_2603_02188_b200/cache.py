@@ -175,31 +175,31 @@ class PagedCache:
     def lengths(self) -> list[int]:
         return list(self._host_lens)
 
+    def reserve_token(self) -> None:
+        """Host bookkeeping for one appended token per sequence (capacity check first)."""
+        if max(self._host_lens) >= self.capacity:
+            raise ConfigError(f"cache full: capacity {self.capacity} tokens per sequence")
+        self._host_lens = [n + 1 for n in self._host_lens]
+
     def append(self, rows: torch.Tensor) -> None:
         """K0: write one new token row per sequence ([B, W] bf16, device) at its current end."""
         if rows.shape != (self.batch, self.layout.width):
             raise ShapeMismatchError(f"append: rows {tuple(rows.shape)} != {(self.batch, self.layout.width)}")
-        if max(self._host_lens) >= self.capacity:
-            raise ConfigError(f"cache full: capacity {self.capacity} tokens per sequence")
-        ops.cache_append(rows.contiguous(), self.block_table, self.seqlens, self.pool, self.page_size)
-        self.seqlens += 1
-        self._host_lens = [n + 1 for n in self._host_lens]
+        self.reserve_token()
+        ops.cache_append(rows.contiguous(), self.block_table, self.seqlens, self.pool, self.page_size, advance=True)
 
     def append_latent(self, kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos, *, branches: int, block0: int,
                       nblocks: int, alpha_kv: float, rope_base: float = 10000.0, norm_groups: int = 1) -> None:
         """Fused K0 for one new token per sequence: kv_raw [B, d_c] / kr_raw [B, dr] fp32 raw
         projections, rope_pos [B] absolute positions (host list or int32 device tensor)."""
         lay = self.layout
-        if max(self._host_lens) >= self.capacity:
-            raise ConfigError(f"cache full: capacity {self.capacity} tokens per sequence")
+        self.reserve_token()
         pos = rope_pos if torch.is_tensor(rope_pos) else torch.tensor(list(rope_pos), dtype=torch.int32)
         ops.cache_append_latent(kv_raw.float().contiguous(), kr_raw.float().contiguous(),
                                 pos.to(device=self.device, dtype=torch.int32), self.seqlens, self.block_table,
                                 self.pool, self.page_size, branches=branches, block0=block0, nblocks=nblocks,
                                 dlp=lay.dlp, drp=lay.drp, alpha_kv=alpha_kv, rope_base=rope_base,
-                                norm_groups=norm_groups)
-        self.seqlens += 1
-        self._host_lens = [n + 1 for n in self._host_lens]
+                                norm_groups=norm_groups, advance=True)
 
     def fill(self, rows: torch.Tensor, lengths) -> None:
         """Bulk prefill: rows [B, n_max, W] bf16 (device); sequence s keeps its first lengths[s]."""

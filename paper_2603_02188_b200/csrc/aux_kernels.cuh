@@ -28,11 +28,17 @@ __device__ unsigned long long g_small_trace[4096 * 8];
 // ----------------------------------------------------------------------------- K0
 // attnkit/decode.py:129-150 (append_owned) + cache.py:44-57: write one token row per
 // sequence into its page. rows [B, W] bf16; positions [B] = slot index of the new token.
+// advance != 0: positions[s] += 1 once the slot is read (the reference append grows the
+// cache length, cache.py:44-57), saving the separate length-update launch.
 __global__ void cache_append_kernel(const __nv_bfloat16* __restrict__ rows, const int32_t* __restrict__ block_table,
-                                    const int32_t* __restrict__ positions, int W, int page_size, int max_pages,
+                                    int32_t* __restrict__ positions, int W, int page_size, int max_pages, int advance,
                                     __nv_bfloat16* __restrict__ pool) {
   const int s = blockIdx.x;
   const int pos = positions[s];
+  if (advance) {
+    __syncthreads();
+    if (threadIdx.x == 0) positions[s] = pos + 1;
+  }
   const int page = block_table[size_t(s) * max_pages + pos / page_size];
   __nv_bfloat16* dst = pool + (size_t(page) * page_size + pos % page_size) * W;
   const __nv_bfloat16* src = rows + size_t(s) * W;
@@ -54,16 +60,17 @@ __global__ void cache_append_kernel(const __nv_bfloat16* __restrict__ rows, cons
 constexpr int kK0Threads = 128;
 __global__ void __launch_bounds__(kK0Threads)
 cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __restrict__ kr_raw,
-                           const int32_t* __restrict__ rope_pos, const int32_t* __restrict__ slots,
+                           const int32_t* __restrict__ rope_pos, int32_t* __restrict__ slots,
                            const int32_t* __restrict__ block_table, int d_c, int bs, int block0, int nblocks, int dlp,
                            int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size, int max_pages,
-                           int norm_groups, __nv_bfloat16* __restrict__ pool) {
+                           int norm_groups, int advance, __nv_bfloat16* __restrict__ pool) {
   // RMS per latent group: the row is norm_groups consecutive groups of d_c/norm_groups
   // columns (1 for MLA / MLRA-4; one per group for GLA / MLRA-2, latent.py:145-158)
   constexpr int kMaxGroups = 4;
   __shared__ float red[kMaxGroups][kK0Threads / 32];
   __shared__ float gscale[kMaxGroups];
   const int s = blockIdx.x, tid = threadIdx.x;
+  const int slot = slots[s];  // read before the barriers below; advanced after them
   const float* kv = kv_raw + size_t(s) * d_c;
   const int gw = d_c / norm_groups;
   for (int g = 0; g < norm_groups; ++g) {
@@ -81,7 +88,7 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
     gscale[tid] = alpha_kv * rsqrtf(tot / float(gw) + eps);
   }
   __syncthreads();
-  const int slot = slots[s];
+  if (advance && tid == 0) slots[s] = slot + 1;
   const int page = block_table[size_t(s) * max_pages + slot / page_size];
   const int W = nblocks * dlp + drp;
   __nv_bfloat16* dst = pool + (size_t(page) * page_size + slot % page_size) * W;

@@ -222,13 +222,13 @@ int mlra_num_sms(void) {
   return n;
 }
 
-int mlra_cache_append(const void* rows, const int32_t* block_table, const int32_t* positions, int B, int W,
-                      int page_size, int max_pages, void* pool, void* stream) {
+int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* positions, int B, int W,
+                      int page_size, int max_pages, int advance, void* pool, void* stream) {
   if (B <= 0) return MLRA_OK;
   if (W <= 0 || W % 8 != 0) return fail(MLRA_ERR_SHAPE, "cache_append: row width %d must be a positive multiple of 8", W);
   if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append: bad page geometry");
   mlra::cache_append_kernel<<<B, 64, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(rows), block_table, positions, W, page_size, max_pages,
+      static_cast<const __nv_bfloat16*>(rows), block_table, positions, W, page_size, max_pages, advance,
       static_cast<__nv_bfloat16*>(pool));
   return cuda_check("cache_append launch");
 }
@@ -271,10 +271,10 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
   return cuda_check("absorb_query launch");
 }
 
-int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, const int32_t* slots,
+int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, int32_t* slots,
                              const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
                              int dlp, int dr, int drp, float alpha_kv, float rope_base, float eps, int page_size,
-                             int max_pages, int norm_groups, void* pool, void* stream) {
+                             int max_pages, int norm_groups, int advance, void* pool, void* stream) {
   if (B <= 0) return MLRA_OK;
   if (norm_groups < 1 || norm_groups > 4 || d_c % norm_groups != 0)
     return fail(MLRA_ERR_CONFIG, "cache_append_latent: %d RMS groups over d_c=%d", norm_groups, d_c);
@@ -289,7 +289,7 @@ int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int
   if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append_latent: bad page geometry");
   mlra::cache_append_latent_kernel<<<B, mlra::kK0Threads, 0, static_cast<cudaStream_t>(stream)>>>(
       kv_raw, kr_raw, rope_pos, slots, block_table, d_c, bs, block0, nblocks, dlp, dr, drp, alpha_kv, rope_base, eps,
-      page_size, max_pages, norm_groups, static_cast<__nv_bfloat16*>(pool));
+      page_size, max_pages, norm_groups, advance, static_cast<__nv_bfloat16*>(pool));
   return cuda_check("cache_append_latent launch");
 }
 

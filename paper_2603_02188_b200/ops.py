@@ -41,8 +41,9 @@ def default_splits(batch: int, max_seqlen: int, nb: int, sub: int) -> int:
 
 
 def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch.Tensor, pool: torch.Tensor,
-                 page_size: int) -> None:
-    """K0: pool[page(pos), pos % page_size] = rows[s] for every sequence s."""
+                 page_size: int, advance: bool = False) -> None:
+    """K0: pool[page(pos), pos % page_size] = rows[s] for every sequence s; with ``advance``
+    the kernel also bumps positions[s] (pass the sequence lengths: the reference append)."""
     _need(rows, torch.bfloat16, "rows", 2)
     _need(block_table, torch.int32, "block_table", 2)
     _need(positions, torch.int32, "positions", 1)
@@ -51,16 +52,17 @@ def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch
     if pool.shape[1] != W:
         raise ShapeMismatchError(f"cache append: row width {W} != pool width {pool.shape[1]}")
     rc = _lib.load().mlra_cache_append(rows.data_ptr(), block_table.data_ptr(), positions.data_ptr(), B, W,
-                                       page_size, block_table.shape[1], pool.data_ptr(), _stream())
+                                       page_size, block_table.shape[1], int(advance), pool.data_ptr(), _stream())
     _lib.check(rc, "mlra_cache_append")
 
 
 def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor, slots: torch.Tensor,
                         block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
                         nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
-                        eps: float = 1e-6, norm_groups: int = 1) -> None:
+                        eps: float = 1e-6, norm_groups: int = 1, advance: bool = False) -> None:
     """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
-    rope_pos, padded, appended as one bf16 pool row per sequence at slots[s]."""
+    rope_pos, padded, appended as one bf16 pool row per sequence at slots[s] (then slots[s] += 1
+    with ``advance``)."""
     _need(kv_raw, torch.float32, "kv_raw", 2)
     _need(kr_raw, torch.float32, "kr_raw", 2)
     _need(rope_pos, torch.int32, "rope_pos", 1)
@@ -74,8 +76,8 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
     rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(), rope_pos.data_ptr(),
                                               slots.data_ptr(), block_table.data_ptr(), B, d_c, branches, block0,
                                               nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
-                                              page_size, block_table.shape[1], norm_groups, pool.data_ptr(),
-                                              _stream())
+                                              page_size, block_table.shape[1], norm_groups, int(advance),
+                                              pool.data_ptr(), _stream())
     _lib.check(rc, "mlra_cache_append_latent")
 
 

@@ -70,3 +70,79 @@ def test_fused_append_through_drop_in_step_tracks_packed_rows():
     for name, want in streams.items():
         got = cache.peek(name)
         assert np.max(np.abs(got - want)) <= 2 ** -7 * np.max(np.abs(want)), name
+
+
+def test_plain_append_advance_flag():
+    """mlra_cache_append: the row lands at positions[s]; advance=1 bumps positions (the
+    reference append grows the cache, cache.py:44-57), advance=0 leaves them alone."""
+    from paper_2603_02188_b200 import ops
+
+    dev = torch.device("cuda", 0)
+    B, W, ps, maxp = 5, 320, 64, 4
+    pool = torch.zeros((B * maxp * ps, W), dtype=torch.bfloat16, device=dev)
+    bt = torch.randperm(B * maxp, generator=torch.Generator().manual_seed(1)).to(torch.int32).reshape(B, maxp).to(dev)
+    pos0 = torch.tensor([0, 63, 64, 200, 255], dtype=torch.int32)
+    pos = pos0.clone().to(dev)
+    for step, adv in enumerate([False, True, True]):
+        rows = (torch.arange(B * W, dtype=torch.float32).reshape(B, W) % 251 + 100 * step).to(torch.bfloat16).to(dev)
+        before = pos.cpu()
+        ops.cache_append(rows, bt, pos, pool, ps, advance=adv)
+        torch.cuda.synchronize()
+        assert torch.equal(pos.cpu(), before + (1 if adv else 0))
+        for s in range(B):
+            p = int(before[s])
+            slot = int(bt[s, p // ps]) * ps + p % ps
+            assert torch.equal(pool[slot], rows[s])
+    assert torch.equal(pos.cpu(), pos0 + 2)
+
+
+def test_micro_batch_loop_matches_in_order_steps():
+    """host_loop.MicroBatchLoop (one H2D / D2H per step on side streams, K0 advance, two
+    micro-batches interleaved) gives exactly the outputs and cache of the plain in-order calls."""
+    import paper_2603_02188_b200 as mlra
+    from paper_2603_02188_b200 import DecodeEngine
+    from paper_2603_02188_b200.host_loop import MicroBatchLoop
+
+    cfg = mlra.trained_config("mlra4")
+    rng = np.random.default_rng(5)
+    w = {"w_uk": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02,
+         "w_uv": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02}
+    dev = torch.device("cuda", 0)
+    B, n0, steps = 3, 300, 4
+
+    def engines():
+        out = []
+        for k in range(2):
+            e = DecodeEngine(cfg, w, batch=B, max_tokens=n0 + 64, page_size=64, device=dev)
+            g = torch.Generator(device=dev).manual_seed(10 + k)
+            e.cache.pool.copy_((torch.randn(e.cache.pool.shape, generator=g, device=dev) * 0.3).to(torch.bfloat16))
+            e.cache.seqlens.fill_(n0 - k)
+            e.cache._host_lens = [n0 - k] * B
+            out.append(e)
+        return out
+
+    ea, eb = engines(), engines()
+    loop = MicroBatchLoop(ea)
+    g = torch.Generator().manual_seed(3)
+    host = [[[torch.randn(t.shape, generator=g).to(torch.bfloat16) for t in loop.host_inputs(k)]
+             for k in range(2)] for _ in range(steps)]
+    got, want = [], []
+    for i in range(steps):
+        for k in range(2):
+            for dst, src in zip(loop.host_inputs(k), host[i][k]):
+                dst.copy_(src)
+            loop.submit(k)
+        for k in range(2):
+            got.append(loop.wait(k).clone())
+    for i in range(steps):
+        for k in range(2):
+            rows, qn, qr = (t.to(dev) for t in host[i][k])
+            eb[k].cache.append(rows)
+            want.append(eb[k].decode_attention(qn, qr).cpu().clone())
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        assert torch.equal(a, b)
+    for a, b in zip(ea, eb):
+        assert torch.equal(a.cache.seqlens, b.cache.seqlens)
+        assert a.cache.lengths() == b.cache.lengths() == [n0 + steps - (a is ea[1])] * B
+        assert torch.equal(a.cache.pool, b.cache.pool)

@@ -61,7 +61,7 @@ def test_cpu_safe_calls(lib):
     assert rc == -2 and b"sub-block width" in lib.mlra_last_error()
     rc = lib.mlra_decode_partials(None, None, None, None, None, None, None, 1, 24, 1, 1, 128, 64, 100, 1, 1, 1, None)
     assert rc == -2 and b"page_size" in lib.mlra_last_error()
-    rc = lib.mlra_cache_append(None, None, None, 1, 7, 64, 1, None, None)
+    rc = lib.mlra_cache_append(None, None, None, 1, 7, 64, 1, 1, None, None)
     assert rc == -1 and b"row width" in lib.mlra_last_error()
     rc = lib.mlra_combine(None, None, None, None, None, 1, 1, 1, 128, 128, 1, 1.0, 3, None)
     assert rc == -2
@@ -81,16 +81,16 @@ def test_cpu_safe_calls_gqa_and_fused_append(lib):
     assert rc == -2 and b"page_size" in lib.mlra_last_error()
     # fused K0: shape / config validation
     rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 510, 4, 0, 4, 128, 64, 64, 1.0, 1e4, 1e-6,
-                                      128, 1, 1, None, None)
+                                      128, 1, 1, 1, None, None)
     assert rc == -1 and b"branches" in lib.mlra_last_error()
     rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 512, 4, 3, 2, 128, 64, 64, 1.0, 1e4, 1e-6,
-                                      128, 1, 1, None, None)
+                                      128, 1, 1, 1, None, None)
     assert rc == -2 and b"blocks" in lib.mlra_last_error()
     rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 512, 4, 0, 1, 128, 63, 64, 1.0, 1e4, 1e-6,
-                                      128, 1, 1, None, None)
+                                      128, 1, 1, 1, None, None)
     assert rc == -2 and b"even" in lib.mlra_last_error()
     rc = lib.mlra_cache_append_latent(None, None, None, None, None, 1, 512, 4, 0, 1, 128, 64, 64, 1.0, 1e4, 1e-6,
-                                      128, 1, 3, None, None)
+                                      128, 1, 3, 1, None, None)
     assert rc == -2 and b"RMS groups" in lib.mlra_last_error()
     # splits beyond the merge kernels' limit
     rc = lib.mlra_decode_partials(None, None, None, None, None, None, None, 1, 24, 1, 1, 128, 64, 128, 1, 1, 161, None)
