@@ -81,7 +81,7 @@ def test_plain_append_advance_flag():
     B, W, ps, maxp = 5, 320, 64, 4
     pool = torch.zeros((B * maxp * ps, W), dtype=torch.bfloat16, device=dev)
     bt = torch.randperm(B * maxp, generator=torch.Generator().manual_seed(1)).to(torch.int32).reshape(B, maxp).to(dev)
-    pos0 = torch.tensor([0, 63, 64, 200, 255], dtype=torch.int32)
+    pos0 = torch.tensor([0, 63, 64, 200, 253], dtype=torch.int32)
     pos = pos0.clone().to(dev)
     for step, adv in enumerate([False, True, True]):
         rows = (torch.arange(B * W, dtype=torch.float32).reshape(B, W) % 251 + 100 * step).to(torch.bfloat16).to(dev)
