@@ -47,6 +47,7 @@ class Cfg:
     g: int = 1
     branches: int = 0
     scaling: bool = False
+    gated: bool = False
 
     def __post_init__(self):
         if self.d_h_rope < 0:
@@ -80,7 +81,7 @@ class Cfg:
 def cfg_from(obj) -> Cfg:
     """Build a Cfg from any object with AttnConfig-like attributes (duck-typed)."""
     return Cfg(obj.variant, obj.h, obj.d, obj.d_h, obj.d_h_rope, obj.d_c, obj.d_cq, obj.g, obj.branches,
-               bool(obj.scaling))
+               bool(obj.scaling), bool(getattr(obj, "gated", False)))
 
 
 # ----------------------------------------------------------------------------- substrate
@@ -159,6 +160,8 @@ def weight_shapes(cfg: Cfg) -> dict:  # attnkit/weights.py:45-99 (latent family 
             s.update({"w_dkv": (d, cfg.d_c), "w_uk": (cfg.d_c, h * d_h), "w_uv": (cfg.d_c, h * d_h)})
     else:
         raise OracleError(f"oracle covers the latent family and gqa, not {cfg.variant}")
+    if cfg.gated:  # weights.py:98-99
+        s["w_g"] = (d, h * d_h)
     s["w_o"] = (h * d_h, d)
     return s
 
@@ -467,6 +470,34 @@ def per_device_load(cfg: Cfg, phi: int) -> Fraction:  # attnkit/costs.py:70-102 
     if cfg.variant == "mlra":
         return Fraction(cfg.d_c, min(phi, 4) * cfg.d_h) + Fraction(cfg.d_h_rope, cfg.d_h)
     raise OracleError(f"no loading rule for {cfg.variant}")
+
+
+# ----------------------------------------------------------------------------- output side (8(f) row 2)
+def sigmoid(x: np.ndarray) -> np.ndarray:  # attnkit/tensors.py:101-102
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def gated_output(hidden: np.ndarray, out_flat: np.ndarray, w_g: np.ndarray) -> np.ndarray:  # attnkit/zoo.py:125-127
+    return out_flat * sigmoid(hidden @ w_g)
+
+
+def attention_block_output(hidden: np.ndarray, out_flat: np.ndarray, w_o: np.ndarray, w_g=None) -> np.ndarray:
+    """The attention half of attnkit/zoo.py:146-149 (block_forward): the gate is driven by the
+    un-normalised block input, then hidden + gated @ w_o."""
+    flat = gated_output(hidden, out_flat, w_g) if w_g is not None else out_flat
+    return hidden + flat @ w_o
+
+
+def tp_attention_block_output(hidden: np.ndarray, parts, w_o: np.ndarray, w_g, d_h: int) -> np.ndarray:
+    """The same under tensor parallelism: parts = [(heads, out_r [n, len(heads)*d_h])] in device
+    order (per-head contributions, summed like attnkit/decode.py:264-285); each device applies
+    the gate and W_o to its columns and the [n, d] results are summed in device order."""
+    acc = np.zeros((hidden.shape[0], w_o.shape[1]))
+    for heads, out_r in parts:
+        cols = np.concatenate([np.arange(i * d_h, (i + 1) * d_h) for i in heads])
+        g = out_r * sigmoid(hidden @ w_g[:, cols]) if w_g is not None else out_r
+        acc = acc + g @ w_o[cols]
+    return hidden + acc
 
 
 def max_rel_err(a: np.ndarray, b: np.ndarray) -> float:  # attnkit/selftest.py:101-103

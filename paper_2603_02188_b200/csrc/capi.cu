@@ -11,6 +11,7 @@
 #include "../../include/mlra_b200.h"
 #include "aux_kernels.cuh"
 #include "decode_kernel.cuh"
+#include "outproj_kernel.cuh"
 
 namespace {
 
@@ -627,6 +628,125 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
   // split merge; KV head b's query head j is output head b*R + j (out [B, G*R, DH])
   return combine_impl(o_part, lse_part, nullptr, out, nullptr, B, R, G, DH, DH, nsplit, 1.f, 0,
                       static_cast<cudaStream_t>(stream));
+}
+
+// ----------------------------------------------------------------------------- K4 (output side)
+size_t mlra_outproj_comm_bytes(int B, int D, int world) {
+  if (B <= 0 || D <= 0 || world <= 0) return 0;
+  const size_t nslabs = (size_t(D) + mlra::kOpNC - 1) / mlra::kOpNC;
+  return size_t(2) * world * B * D * 4 + size_t(2) * world * nslabs * 4;
+}
+
+static int outproj_check(int B, int K, int D, int world) {
+  if (B <= 0 || B > mlra::kOpMaxB) return fail(MLRA_ERR_SHAPE, "outproj: B=%d outside [1, %d]", B, mlra::kOpMaxB);
+  if (K <= 0 || K % 8 != 0 || D <= 0 || D % 8 != 0)
+    return fail(MLRA_ERR_SHAPE, "outproj: K=%d and D=%d must be positive multiples of 8", K, D);
+  if (world < 1 || world > mlra::kOpMaxRanks)
+    return fail(MLRA_ERR_CONFIG, "outproj: world %d outside [1, %d]", world, mlra::kOpMaxRanks);
+  return MLRA_OK;
+}
+
+static unsigned g_outproj_attr = 0;
+
+static int outproj_launch(mlra::OutProjParams& p, int nlocal, bool cooperative, cudaStream_t st) {
+  const size_t smem = mlra::outproj_smem();
+  if (int rc = set_smem_once(mlra::outproj_allreduce_kernel, g_outproj_attr, int(smem))) return rc;
+  p.nslabs = (p.D + mlra::kOpNC - 1) / mlra::kOpNC;
+  const dim3 grid(p.nslabs, nlocal);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlra::outproj_allreduce_kernel, mlra::kOpThreads, smem);
+  // every CTA must be resident: a CTA waiting for its slab's flags may not hold back a CTA
+  // some peer is waiting for
+  if (p.world > 1 && size_t(grid.x) * grid.y > size_t(sms) * per_sm)
+    return fail(MLRA_ERR_CONFIG, "outproj: %d CTAs cannot all be resident (%d SMs x %d)", int(grid.x * grid.y), sms,
+                per_sm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(mlra::kOpThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, mlra::outproj_allreduce_kernel, p) != cudaSuccess) return cuda_check("outproj launch");
+  return cuda_check("outproj launch");
+}
+
+int mlra_outproj(const float* attn, const float* gate_pre, const void* w_o, const float* resid, float* y, int B,
+                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* stream) {
+  if (int rc = outproj_check(B, K, D, world)) return rc;
+  if (rank < 0 || rank >= world) return fail(MLRA_ERR_CONFIG, "outproj: rank %d of %d", rank, world);
+  if (world > 1 && (comm == nullptr || epoch == 0))
+    return fail(MLRA_ERR_CONFIG, "outproj: world %d needs the communication regions and an epoch >= 1", world);
+  mlra::OutProjParams p = {};
+  p.attn[0] = attn;
+  p.gate_pre[0] = gate_pre;
+  p.w_o[0] = static_cast<const __nv_bfloat16*>(w_o);
+  p.y[0] = y;
+  p.resid = resid;
+  for (int r = 0; r < world && world > 1; ++r) p.comm[r] = static_cast<float*>(comm[r]);
+  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = rank, p.epoch = epoch;
+  return outproj_launch(p, 1, false, static_cast<cudaStream_t>(stream));
+}
+
+int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, const void* const* w_o,
+                     const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
+                     unsigned epoch, void* stream) {
+  if (int rc = outproj_check(B, K, D, world)) return rc;
+  if (comm == nullptr || epoch == 0) return fail(MLRA_ERR_CONFIG, "outproj_sim: needs comm regions and epoch >= 1");
+  mlra::OutProjParams p = {};
+  for (int r = 0; r < world; ++r) {
+    p.attn[r] = attn[r];
+    p.gate_pre[r] = gate_pre != nullptr ? gate_pre[r] : nullptr;
+    p.w_o[r] = static_cast<const __nv_bfloat16*>(w_o[r]);
+    p.y[r] = y[r];
+    p.comm[r] = static_cast<float*>(comm[r]);
+  }
+  p.resid = resid;
+  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = 0, p.epoch = epoch;
+  if (world == 1) return outproj_launch(p, 1, false, static_cast<cudaStream_t>(stream));
+  return outproj_launch(p, world, true, static_cast<cudaStream_t>(stream));
+}
+
+int mlra_comm_alloc(size_t bytes, void** dev_ptr_out) {
+  if (bytes == 0 || dev_ptr_out == nullptr) return fail(MLRA_ERR_CONFIG, "comm_alloc: empty request");
+  if (cudaMalloc(dev_ptr_out, bytes) != cudaSuccess) return cuda_check("cudaMalloc (comm region)");
+  if (cudaMemset(*dev_ptr_out, 0, bytes) != cudaSuccess) return cuda_check("cudaMemset (comm region)");
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_check("comm_alloc sync");
+  return MLRA_OK;
+}
+
+int mlra_comm_free(void* dev_ptr) {
+  if (dev_ptr != nullptr && cudaFree(dev_ptr) != cudaSuccess) return cuda_check("cudaFree (comm region)");
+  return MLRA_OK;
+}
+
+int mlra_ipc_handle(const void* dev_ptr, void* handle_out) {
+  if (dev_ptr == nullptr || handle_out == nullptr) return fail(MLRA_ERR_CONFIG, "ipc_handle: null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return cuda_check("cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, sizeof h);
+  return MLRA_OK;
+}
+
+int mlra_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (handle == nullptr || dev_ptr_out == nullptr) return fail(MLRA_ERR_CONFIG, "ipc_open: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  if (cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return cuda_check("cudaIpcOpenMemHandle");
+  return MLRA_OK;
+}
+
+int mlra_ipc_close(void* dev_ptr) {
+  if (dev_ptr == nullptr) return MLRA_OK;
+  if (cudaIpcCloseMemHandle(dev_ptr) != cudaSuccess) return cuda_check("cudaIpcCloseMemHandle");
+  return MLRA_OK;
 }
 
 }  // extern "C"

@@ -266,3 +266,102 @@ def ceil_div(a: int, b: int) -> int:
 
 
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("math", "torch")]
+
+
+# ----------------------------------------------------------------------------- K4: output side
+def outproj_comm_bytes(batch: int, d: int, world: int) -> int:
+    return int(_lib.load().mlra_outproj_comm_bytes(batch, d, world))
+
+
+def _ptr_array(ptrs):
+    import ctypes
+
+    arr = (ctypes.c_void_p * len(ptrs))(*[int(p) if p is not None else None for p in ptrs])
+    return arr
+
+
+def _outproj_shapes(attn, gate_pre, w_o, resid, y):
+    _need(attn, torch.float32, "attn", 2)
+    _need(w_o, torch.bfloat16, "w_o", 2)
+    _need(y, torch.float32, "y", 2)
+    B, K = attn.shape
+    D = w_o.shape[1]
+    if w_o.shape[0] != K:
+        raise ShapeMismatchError(f"outproj: w_o rows {w_o.shape[0]} != attention width {K}")
+    if tuple(y.shape) != (B, D):
+        raise ShapeMismatchError(f"outproj: y {tuple(y.shape)} != {(B, D)}")
+    if gate_pre is not None:
+        _need(gate_pre, torch.float32, "gate_pre", 2)
+        if gate_pre.shape != attn.shape:
+            raise ShapeMismatchError(f"outproj: gate_pre {tuple(gate_pre.shape)} != attn {tuple(attn.shape)}")
+    if resid is not None:
+        _need(resid, torch.float32, "resid", 2)
+        if tuple(resid.shape) != (B, D):
+            raise ShapeMismatchError(f"outproj: resid {tuple(resid.shape)} != {(B, D)}")
+    return B, K, D
+
+
+def outproj(attn: torch.Tensor, gate_pre: torch.Tensor | None, w_o: torch.Tensor, resid: torch.Tensor | None,
+            y: torch.Tensor, rank: int = 0, world: int = 1, comm_ptrs=None, epoch: int = 0) -> torch.Tensor:
+    """K4: y = resid + sum over ranks of (attn * sigmoid(gate_pre)) @ w_o (zoo.py:125-149).
+    world > 1: comm_ptrs = every rank's communication region as mapped here, epoch >= 1."""
+    B, K, D = _outproj_shapes(attn, gate_pre, w_o, resid, y)
+    comm = _ptr_array(comm_ptrs) if comm_ptrs is not None else None
+    rc = _lib.load().mlra_outproj(attn.data_ptr(), _lib.ptr(gate_pre), w_o.data_ptr(), _lib.ptr(resid), y.data_ptr(),
+                                  B, K, D, rank, world, comm, epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "mlra_outproj")
+    return y
+
+
+def outproj_sim(attns, gates, w_os, resid, ys, comms, epoch: int) -> None:
+    """K4 with len(attns) ranks simulated on one device (tests): per-rank lists of tensors,
+    comms = per-rank communication regions (uint8 CUDA tensors of outproj_comm_bytes)."""
+    world = len(attns)
+    B, K, D = _outproj_shapes(attns[0], None if gates is None else gates[0], w_os[0], resid, ys[0])
+    for r in range(world):
+        _outproj_shapes(attns[r], None if gates is None else gates[r], w_os[r], resid, ys[r])
+        if comms[r].numel() < outproj_comm_bytes(B, D, world):
+            raise ShapeMismatchError("outproj_sim: communication region too small")
+    rc = _lib.load().mlra_outproj_sim(_ptr_array([a.data_ptr() for a in attns]),
+                                      None if gates is None else _ptr_array([g.data_ptr() for g in gates]),
+                                      _ptr_array([w.data_ptr() for w in w_os]), _lib.ptr(resid),
+                                      _ptr_array([y.data_ptr() for y in ys]), B, K, D, world,
+                                      _ptr_array([c.data_ptr() for c in comms]), epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "mlra_outproj_sim")
+
+
+def comm_alloc(nbytes: int) -> int:
+    """Zero-filled device allocation of its own (exact IPC mapping); returns the pointer."""
+    import ctypes
+
+    out = ctypes.c_void_p()
+    _lib.check(_lib.load().mlra_comm_alloc(nbytes, ctypes.byref(out)), "mlra_comm_alloc")
+    return int(out.value)
+
+
+def comm_free(ptr: int) -> None:
+    _lib.check(_lib.load().mlra_comm_free(ptr), "mlra_comm_free")
+
+
+def ipc_handle(ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a comm_alloc allocation."""
+    import ctypes
+
+    buf = ctypes.create_string_buffer(64)
+    _lib.check(_lib.load().mlra_ipc_handle(ptr, buf), "mlra_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    import ctypes
+
+    if len(handle) != 64:
+        raise ConfigError(f"ipc_open: handle of {len(handle)} bytes, expected 64")
+    out = ctypes.c_void_p()
+    _lib.check(_lib.load().mlra_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(out)), "mlra_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().mlra_ipc_close(ptr), "mlra_ipc_close")
+

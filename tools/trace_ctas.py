@@ -8,7 +8,8 @@ os.environ["MLRA_DEBUG_TRACE_PTR"] = str(trace.data_ptr())
 from paper_2603_02188_b200 import ops
 which = sys.argv[1]
 NB, DLAT = {"tp4": (1, 128), "tp1": (4, 128), "mla": (1, 512)}[which]
-B, H, DH, DR, L = 16, 24, 128, 64, 32768
+B, H, DH, DR = 16, 24, 128, 64
+B = int(os.environ.get("TRACE_B", B)); L = int(os.environ.get("TRACE_L", 32768))
 c = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128)
 c2 = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128, seed=1)  # the bench alternates two caches
 sub, dls = ops.latent_geometry(DLAT)
