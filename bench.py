@@ -592,7 +592,61 @@ def per_gpu_comparisons(cfg, device, args):
                                                       res["mlra4_tp4_rank"]["us_per_step"], 3),
         "traffic_ratio_gqa_tp2_rank_vs_mlra4_tp4_rank": 4.0,
     }
+    out["output_side"] = output_side_times(device)
     return out
+
+
+def output_side_times(device):
+    """K4a + K4 (gate, W_o, residual; world 1) against the torch path (sigmoid, cast, cuBLAS
+    GEMM, add) at the step's batch: an MLRA-4 TP4 rank holds a partial of all 24 heads (K =
+    3072), an MLA TP4 rank 6 heads (K = 768); d = 3072. Eight W_o copies are cycled so W_o
+    comes from HBM (8 x 18.9 MB > L2). The multi-rank all-reduce needs peers (not timed here)."""
+    import torch
+
+    from paper_2603_02188_b200 import ops
+
+    def gtime(fn, reps=20):
+        fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(10):
+                fn()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / 10 * 1e3
+
+    res = {}
+    B, D = BATCH_PER_GROUP, 3072
+    for name, K in (("mlra4_tp4_rank", 3072), ("mla_tp4_rank", 768)):
+        attn, gate = torch.randn(B, K, device=device), torch.randn(B, K, device=device)
+        w_os = [torch.randn(K, D, device=device).to(torch.bfloat16) for _ in range(8)]
+        resid, y = torch.randn(B, D, device=device), torch.empty(B, D, device=device)
+        ws = ops.outproj_workspace(B, K, device)
+        it = [0]
+
+        def k4():
+            it[0] += 1
+            ops.outproj(attn, gate, w_os[it[0] % 8], resid, y, workspace=ws)
+
+        def ref():
+            it[0] += 1
+            y.copy_(resid + ((attn * torch.sigmoid(gate)).to(torch.bfloat16) @ w_os[it[0] % 8]).float())
+
+        t4, tr = gtime(k4), gtime(ref)
+        res[name] = {"K": K, "k4_us": round(t4, 2), "torch_us": round(tr, 2),
+                     "w_o_gbs": round(K * D * 2 / (t4 * 1e-6) / 1e9, 1)}
+        del w_os
+        torch.cuda.empty_cache()
+    return res
 
 
 def main():

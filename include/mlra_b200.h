@@ -169,8 +169,8 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
  *   gate_pre [B, K] fp32   hidden @ W_g[:, this rank's columns] (pre-activation), or NULL (no gate)
  *   w_o      [K, D] bf16   the rows of W_o for this rank's attention columns
  *   resid    [B, D] fp32   block input (the residual) or NULL; y [B, D] fp32 (same on every rank)
- *   B <= 64, K % 8 == 0, D % 8 == 0. The gated operand is rounded to bf16 for the tensor-core
- *   product (fp32 accumulation).
+ *   B <= 64, K % 8 == 0, D % 8 == 0. The gated operand is rounded to bf16 (into workspace,
+ *   mlra_outproj_workspace_bytes) for the tensor-core product (fp32 accumulation).
  * world == 1: comm may be NULL. world > 1: comm[r] = rank r's communication region
  * (mlra_outproj_comm_bytes, zero-filled once) as mapped in THIS process (its own region and
  * the peers' through mlra_ipc_open); epoch = 1, 2, 3, ... per call, identical on all ranks.
@@ -178,13 +178,15 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
  * ascending rank order -- no NCCL call; a peer missing for 4 s aborts the kernel.
  */
 size_t mlra_outproj_comm_bytes(int B, int D, int world);
+size_t mlra_outproj_workspace_bytes(int B, int K);  /* the gated bf16 operand [B, K] */
 int mlra_outproj(const float* attn, const float* gate_pre, const void* w_o, const float* resid, float* y, int B,
-                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* stream);
-/* The same kernel with `world` ranks simulated on ONE device (tests): arrays of world per-rank
+                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* workspace,
+                 void* stream);
+/* The same kernels with `world` ranks simulated on ONE device (tests): arrays of world per-rank
  * pointers, one cooperative launch. Fails with MLRA_ERR_CONFIG when the grid cannot be resident. */
 int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, const void* const* w_o,
                      const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
-                     unsigned epoch, void* stream);
+                     unsigned epoch, void* const* workspace, void* stream);
 
 /* Communication region: a dedicated zero-filled cudaMalloc (so its IPC handle maps exactly). */
 int mlra_comm_alloc(size_t bytes, void** dev_ptr_out);

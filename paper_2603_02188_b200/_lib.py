@@ -40,8 +40,9 @@ SIGNATURES = {
     "mlra_gqa_decode_partials": (_I, [_P] * 6 + [_I] * 8 + [_F, _P]),
     "mlra_gqa_decode_step": (_I, [_P] * 6 + [_I] * 8 + [_F, _P]),
     "mlra_outproj_comm_bytes": (ctypes.c_size_t, [_I, _I, _I]),
-    "mlra_outproj": (_I, [_P] * 5 + [_I] * 5 + [_P, ctypes.c_uint, _P]),
-    "mlra_outproj_sim": (_I, [_P] * 5 + [_I] * 4 + [_P, ctypes.c_uint, _P]),
+    "mlra_outproj_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
+    "mlra_outproj": (_I, [_P] * 5 + [_I] * 5 + [_P, ctypes.c_uint, _P, _P]),
+    "mlra_outproj_sim": (_I, [_P] * 5 + [_I] * 4 + [_P, ctypes.c_uint, _P, _P]),
     "mlra_comm_alloc": (_I, [ctypes.c_size_t, _P]),
     "mlra_comm_free": (_I, [_P]),
     "mlra_ipc_handle": (_I, [_P, _P]),

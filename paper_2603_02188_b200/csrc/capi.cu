@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -633,8 +634,8 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
 // ----------------------------------------------------------------------------- K4 (output side)
 size_t mlra_outproj_comm_bytes(int B, int D, int world) {
   if (B <= 0 || D <= 0 || world <= 0) return 0;
-  const size_t nslabs = (size_t(D) + mlra::kOpNC - 1) / mlra::kOpNC;
-  return size_t(2) * world * B * D * 4 + size_t(2) * world * nslabs * 4;
+  const size_t nslabs = size_t(mlra::outproj_nslabs(D));
+  return size_t(2) * world * B * D * 4 + size_t(2) * world * nslabs * mlra::kOpMaxKS * 4;
 }
 
 static int outproj_check(int B, int K, int D, int world) {
@@ -648,68 +649,109 @@ static int outproj_check(int B, int K, int D, int world) {
 
 static unsigned g_outproj_attr = 0;
 
-static int outproj_launch(mlra::OutProjParams& p, int nlocal, bool cooperative, cudaStream_t st) {
+size_t mlra_outproj_workspace_bytes(int B, int K) {
+  return (B <= 0 || K <= 0) ? 0 : (size_t(B) * K * 2 + 255) / 256 * 256;
+}
+
+// K4a (gate + bf16 cast) then K4. Grid of K4: nslabs x KS CTAs per local rank. Real mode:
+// clusters of KS CTAs (K slices of a slab), KS = the largest that keeps one wave (every CTA
+// resident: a CTA waiting for its slab's flags must not hold back one a peer waits for), K4 a
+// programmatic dependent of K4a. Sim mode: KS = 1, one cooperative launch per call.
+static int outproj_launch(mlra::OutProjParams& p, const float* const* attn, const float* const* gate,
+                          void* const* ws, int nlocal, bool sim, cudaStream_t st) {
   const size_t smem = mlra::outproj_smem();
-  if (int rc = set_smem_once(mlra::outproj_allreduce_kernel, g_outproj_attr, int(smem))) return rc;
-  p.nslabs = (p.D + mlra::kOpNC - 1) / mlra::kOpNC;
-  const dim3 grid(p.nslabs, nlocal);
+  auto kern = mlra::outproj_allreduce_kernel;
+  if (int rc = set_smem_once(kern, g_outproj_attr, int(smem))) return rc;
+  const int n = p.B * p.K;
+  for (int r = 0; r < nlocal; ++r) {
+    if (attn[r] == nullptr || ws[r] == nullptr || p.w_o[r] == nullptr || p.y[r] == nullptr)
+      return fail(MLRA_ERR_CONFIG, "outproj: null tensor pointer (rank slot %d)", r);
+    mlra::outproj_gate_kernel<<<(n / 8 + 255) / 256, 256, 0, st>>>(attn[r], gate != nullptr ? gate[r] : nullptr,
+                                                                   static_cast<__nv_bfloat16*>(ws[r]), n);
+    p.a[r] = static_cast<const __nv_bfloat16*>(ws[r]);
+  }
+  if (int rc = cuda_check("outproj gate launch")) return rc;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlra::outproj_allreduce_kernel, mlra::kOpThreads, smem);
-  // every CTA must be resident: a CTA waiting for its slab's flags may not hold back a CTA
-  // some peer is waiting for
-  if (p.world > 1 && size_t(grid.x) * grid.y > size_t(sms) * per_sm)
-    return fail(MLRA_ERR_CONFIG, "outproj: %d CTAs cannot all be resident (%d SMs x %d)", int(grid.x * grid.y), sms,
-                per_sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, mlra::kOpThreads, smem);
+  p.nslabs = mlra::outproj_nslabs(p.D);
+  const int kchunks = (p.K + mlra::kOpKC - 1) / mlra::kOpKC;
+  int ks = sim ? 1 : std::max(1, std::min({mlra::kOpMaxKS, kchunks, sms * per_sm / p.nslabs}));
+  if (const char* e = getenv("MLRA_DEBUG_OUTPROJ_KS")) ks = std::max(1, std::min(ks, atoi(e)));  // dev override
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
+  cudaLaunchAttribute attr[2];
   cfg.blockDim = dim3(mlra::kOpThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = cooperative ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, mlra::outproj_allreduce_kernel, p) != cudaSuccess) return cuda_check("outproj launch");
+  for (;; --ks) {
+    cfg.gridDim = dim3(p.nslabs * ks, nlocal);
+    if (sim) {
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.numAttrs = 1;
+      if (p.world > 1 && size_t(cfg.gridDim.x) * nlocal > size_t(sms) * per_sm)
+        return fail(MLRA_ERR_CONFIG, "outproj_sim: %d CTAs cannot all be resident (%d SMs x %d)",
+                    int(cfg.gridDim.x * nlocal), sms, per_sm);
+      break;
+    }
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+    int clusters = sms * per_sm;
+    if (ks > 1 && cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      clusters = 0;
+    }
+    if (clusters >= p.nslabs) break;
+    if (ks == 1) {
+      if (p.world > 1)
+        return fail(MLRA_ERR_CONFIG, "outproj: %d slabs cannot all be resident (%d SMs x %d)", p.nslabs, sms, per_sm);
+      break;
+    }
+  }
+  p.ks_count = ks;
+  p.k_slice = ((p.K + ks - 1) / ks + 63) / 64 * 64;
+  if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return cuda_check("outproj launch");
   return cuda_check("outproj launch");
 }
 
 int mlra_outproj(const float* attn, const float* gate_pre, const void* w_o, const float* resid, float* y, int B,
-                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* stream) {
+                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* workspace,
+                 void* stream) {
   if (int rc = outproj_check(B, K, D, world)) return rc;
   if (rank < 0 || rank >= world) return fail(MLRA_ERR_CONFIG, "outproj: rank %d of %d", rank, world);
   if (world > 1 && (comm == nullptr || epoch == 0))
     return fail(MLRA_ERR_CONFIG, "outproj: world %d needs the communication regions and an epoch >= 1", world);
   mlra::OutProjParams p = {};
-  p.attn[0] = attn;
-  p.gate_pre[0] = gate_pre;
   p.w_o[0] = static_cast<const __nv_bfloat16*>(w_o);
   p.y[0] = y;
   p.resid = resid;
   for (int r = 0; r < world && world > 1; ++r) p.comm[r] = static_cast<float*>(comm[r]);
   p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = rank, p.epoch = epoch;
-  return outproj_launch(p, 1, false, static_cast<cudaStream_t>(stream));
+  return outproj_launch(p, &attn, &gate_pre, &workspace, 1, false, static_cast<cudaStream_t>(stream));
 }
 
 int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, const void* const* w_o,
                      const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
-                     unsigned epoch, void* stream) {
+                     unsigned epoch, void* const* workspace, void* stream) {
   if (int rc = outproj_check(B, K, D, world)) return rc;
-  if (comm == nullptr || epoch == 0) return fail(MLRA_ERR_CONFIG, "outproj_sim: needs comm regions and epoch >= 1");
+  if (attn == nullptr || w_o == nullptr || y == nullptr || workspace == nullptr || comm == nullptr || epoch == 0)
+    return fail(MLRA_ERR_CONFIG, "outproj_sim: needs per-rank tensors, workspaces, comm regions and epoch >= 1");
   mlra::OutProjParams p = {};
   for (int r = 0; r < world; ++r) {
-    p.attn[r] = attn[r];
-    p.gate_pre[r] = gate_pre != nullptr ? gate_pre[r] : nullptr;
     p.w_o[r] = static_cast<const __nv_bfloat16*>(w_o[r]);
     p.y[r] = y[r];
     p.comm[r] = static_cast<float*>(comm[r]);
   }
   p.resid = resid;
   p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = 0, p.epoch = epoch;
-  if (world == 1) return outproj_launch(p, 1, false, static_cast<cudaStream_t>(stream));
-  return outproj_launch(p, world, true, static_cast<cudaStream_t>(stream));
+  return outproj_launch(p, attn, gate_pre, workspace, world, true, static_cast<cudaStream_t>(stream));
 }
 
 int mlra_comm_alloc(size_t bytes, void** dev_ptr_out) {

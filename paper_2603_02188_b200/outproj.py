@@ -10,10 +10,10 @@ ranks' [B, d] results are summed once:
 
     y = hidden + sum_r (attn_r * sigmoid(hidden @ W_g[:, cols_r])) @ W_o[cols_r, :]
 
-``OutputProjection`` runs that as ONE kernel per rank (K4, ``mlra_outproj``): W^O GEMM on
-tensor cores, then a one-shot all-reduce over peer memory (every rank stores its slab partials
-into every peer's communication region and sums the world partials in rank order) -- no NCCL
-call. ``TpComm`` sets the regions up: a dedicated allocation per rank, CUDA IPC handles
+``OutputProjection`` runs that per rank as K4a (gate + bf16 cast of the attention output) and
+K4 (``mlra_outproj``): the W^O GEMM on tensor cores fused with a one-shot all-reduce over peer
+memory (every rank stores its slab partials into every peer's communication region and sums
+the world partials in rank order) -- no NCCL call. ``TpComm`` sets the regions up: a dedicated allocation per rank, CUDA IPC handles
 exchanged over the process group (any backend), peers opened with lazy peer access.
 
 The gate pre-activation ``hidden @ W_g`` depends on the block input only; it is computed on
@@ -98,9 +98,10 @@ class OutputProjection:
             self.w_g = torch.tensor(np.asarray(tensors["w_g"])[:, cols], dtype=torch.float32, device=self.device)
         self.batch = int(batch)
         self.comm = comm
-        if comm is not None and (comm.batch != self.batch or comm.d != cfg.d):
+        if comm is not None and (comm.batch < self.batch or comm.d != cfg.d):
             raise ConfigError("TpComm was sized for another batch / model width")
         self.y = torch.empty((self.batch, cfg.d), dtype=torch.float32, device=self.device)
+        self.workspace = ops.outproj_workspace(self.batch, self.width, self.device)
 
     @property
     def width(self) -> int:
@@ -122,6 +123,6 @@ class OutputProjection:
         y = self.y[:B] if out is None else out
         resid = hidden.float().contiguous() if residual else None
         if self.comm is None or self.comm.world == 1:
-            return ops.outproj(a.contiguous(), gate_pre, self.w_o, resid, y)
+            return ops.outproj(a.contiguous(), gate_pre, self.w_o, resid, y, workspace=self.workspace)
         return ops.outproj(a.contiguous(), gate_pre, self.w_o, resid, y, self.comm.rank, self.comm.world,
-                           self.comm.ptrs, self.comm.epoch())
+                           self.comm.ptrs, self.comm.epoch(), workspace=self.workspace)

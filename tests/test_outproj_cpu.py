@@ -58,19 +58,20 @@ def test_outproj_c_abi_validation():
     from paper_2603_02188_b200 import _lib
 
     lib = _lib.load()
-    assert lib.mlra_outproj_comm_bytes(16, 3072, 4) == 2 * 4 * 16 * 3072 * 4 + 2 * 4 * 96 * 4
+    assert lib.mlra_outproj_comm_bytes(16, 3072, 4) == 2 * 4 * 16 * 3072 * 4 + 2 * 4 * 24 * 8 * 4
     assert lib.mlra_outproj_comm_bytes(0, 3072, 4) == 0
-    rc = lib.mlra_outproj(None, None, None, None, None, 65, 768, 3072, 0, 1, None, 0, None)
+    assert lib.mlra_outproj_workspace_bytes(16, 3072) == 16 * 3072 * 2
+    rc = lib.mlra_outproj(None, None, None, None, None, 65, 768, 3072, 0, 1, None, 0, None, None)
     assert rc == -1 and b"B=65" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 764, 3072, 0, 1, None, 0, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 764, 3072, 0, 1, None, 0, None, None)
     assert rc == -1 and b"multiples of 8" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 2, 2, None, 1, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 2, 2, None, 1, None, None)
     assert rc == -2 and b"rank 2 of 2" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 2, None, 1, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 2, None, 1, None, None)
     assert rc == -2 and b"communication regions" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 9, None, 1, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 9, None, 1, None, None)
     assert rc == -2 and b"world 9" in lib.mlra_last_error()
-    rc = lib.mlra_outproj_sim(None, None, None, None, None, 16, 768, 3072, 2, None, 1, None)
+    rc = lib.mlra_outproj_sim(None, None, None, None, None, 16, 768, 3072, 2, None, 1, None, None)
     assert rc == -2
     assert lib.mlra_ipc_handle(None, None) == -2
     assert lib.mlra_comm_alloc(0, None) == -2
