@@ -12,4 +12,6 @@ for w in tp1 tp4; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:mlra_decode -s 2 -c 1 \
       -o gpurun_out/k2_$w python tools/step_once.py $w > gpurun_out/ncu_k2_$w.log 2>&1
 done
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:outproj_allreduce -s 2 -c 1 \
+    -o gpurun_out/k4 python tools/outproj_once.py 16 3072 3072 > gpurun_out/ncu_k4.log 2>&1
 ls -la gpurun_out
