@@ -593,7 +593,39 @@ def per_gpu_comparisons(cfg, device, args):
         "traffic_ratio_gqa_tp2_rank_vs_mlra4_tp4_rank": 4.0,
     }
     out["output_side"] = output_side_times(device)
+    out["prefill"] = prefill_times(device)
     return out
+
+
+def prefill_times(device):
+    """latent_prefill's device part (K0 over all tokens + K1..K3 over n prefix pseudo-sequences)
+    for one 2.9B MLRA-4 sequence at TP1, in tokens/s (random weights, one warm-up pass)."""
+    import torch
+
+    from paper_2603_02188_b200 import decode as dec
+    from paper_2603_02188_b200.config import trained_config
+    from paper_2603_02188_b200.weights import weight_shapes
+
+    cfg = trained_config("mlra4")
+    rng = np.random.default_rng(0)
+    w = {name: rng.standard_normal(shape) * 0.02 for name, shape in weight_shapes(cfg).items()}
+    st = dec._state(cfg, w, device)
+    res = {}
+    for n in (1024, 4096):
+        h_t = torch.randn((n, cfg.d), device=device)
+        times = []
+        for rep in range(3):
+            cache = dec.new_cache(cfg, device=device, initial_tokens=n)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dec.prefill_into(cfg, st, cache, h_t)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = min(times[1:])
+        res[f"n{n}"] = {"ms": round(ms, 3), "tokens_per_s": round(n / (ms * 1e-3), 1)}
+    return res
 
 
 def output_side_times(device):

@@ -5,7 +5,8 @@ Drop-in names (attnkit/__init__.py:25-53 subset for the decode path):
 ``AttnConfig``, ``trained_config``, ``table_context``, ``Rng``, ``WeightSet``,
 ``build_weights``, ``weight_shapes``, ``calib_factors``, ``new_cache``, ``absorb_query``,
 ``attend_local``, ``reduce_contributions``, ``absorbed_decode_step``, ``decode_step``,
-``make_shards``, ``sim_decode``, ``per_device_load`` and the error classes.
+``make_shards``, ``sim_decode``, ``per_device_load``, ``latent_prefill`` and the error classes;
+the output side (``OutputProjection``, ``TpComm``) and the host I/O loop (``MicroBatchLoop``).
 
 Compute runs on hand-written sm_100a kernels (``csrc/``) through the C ABI declared in
 ``include/mlra_b200.h`` and loaded from the in-tree ``libmlra_b200.so``. Importing the
@@ -41,6 +42,10 @@ def __getattr__(name):
         "PagedCache": ("cache", "PagedCache"), "PagedLatentCache": ("cache", "PagedLatentCache"),
         "RowLayout": ("cache", "RowLayout"), "GqaLayout": ("cache", "GqaLayout"),
         "gqa": ("gqa", None), "GqaDecodeEngine": ("gqa", "GqaDecodeEngine"),
+        "latent_prefill": ("decode", "latent_prefill"), "PrefillOutput": ("decode", "PrefillOutput"),
+        "outproj": ("outproj", None), "OutputProjection": ("outproj", "OutputProjection"),
+        "TpComm": ("outproj", "TpComm"), "host_loop": ("host_loop", None),
+        "MicroBatchLoop": ("host_loop", "MicroBatchLoop"),
     }
     if name in lazy:
         import importlib

@@ -29,7 +29,7 @@ from . import ops
 from .cache import GqaLayout, PagedCache, PagedLatentCache, RowLayout
 from .config import LATENT_VARIANTS, AttnConfig
 from .costs import calib_factors
-from .errors import ConfigError, IntegrityError, RoutingError
+from .errors import ConfigError, IntegrityError, RoutingError, ShapeMismatchError
 from .projections import LatentProjector
 
 SERVED = ("mla", "mlra", "gla", "gqa")
@@ -364,6 +364,90 @@ def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tu
     out = _run_units(cfg, cache, st.lw, st.own, qn, qr, upproj=1, alpha=alpha)
     cache.reads += cache.n * cache.row_elements()
     return out[0].double().cpu().numpy(), cache
+
+
+# ----------------------------------------------------------------------------- prefill
+@dataclass
+class PrefillOutput:  # latent.py PrefillOutput: per-token outputs and the filled cache
+    out: np.ndarray
+    cache: PagedLatentCache
+
+
+PREFILL_CHUNK = 4096  # queries per kernel pass (K2's grid.y and the split workspace scale with it)
+
+
+def latent_prefill(cfg: AttnConfig, w, hidden, pos_offset: int = 0, *, device=None,
+                   page_size: int = 128) -> PrefillOutput:
+    """Causal prefill (latent.py:172-230) writing the paged cache format directly (SURVEY.md
+    8(f) row 3).
+
+    Write side: the raw down-projections of all n tokens (GEMMs) and ONE fused K0 launch with n
+    rows, each row writing its token's slot of the sequence's pages (the page table repeated
+    per row, slots 0..n-1). Attention side: token t is a decode query over the first t+1 cached
+    rows, so the n queries run as n pseudo-sequences sharing the sequence's page table with
+    seqlens 1..n through K1 -> K2 -> K3 (causality by the lengths, no mask). The cache rows
+    K2 re-reads stay L2-resident across the pseudo-sequences; this is the decode kernels'
+    arithmetic (absorbed logits, bf16 cache, fp32 softmax and merge), not a separate prefill
+    kernel.
+    """
+    if cfg.variant not in LATENT_VARIANTS:
+        raise RoutingError(f"variant {cfg.variant!r} belongs to the baseline zoo, not latent_prefill")
+    _check_served(cfg)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    st = _state(cfg, w, dev)
+    hid = np.asarray(hidden, dtype=np.float64)
+    if hid.ndim != 2 or hid.shape[1] != cfg.d:
+        raise ShapeMismatchError(f"prefill hidden {hid.shape} != (n, {cfg.d})")
+    n = hid.shape[0]
+    cache = new_cache(cfg, pos_offset=pos_offset, device=dev, page_size=page_size,
+                      initial_tokens=max(n, page_size))
+    if n == 0:
+        return PrefillOutput(np.zeros((0, cfg.h, cfg.d_h)), cache)
+    out = prefill_into(cfg, st, cache, torch.as_tensor(hid, dtype=torch.float32, device=dev))
+    return PrefillOutput(out.double().cpu().numpy(), cache)
+
+
+def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t: torch.Tensor) -> torch.Tensor:
+    """Device part of latent_prefill: fill the EMPTY paged cache with the n tokens of h_t
+    [n, d] fp32 (positions pos_offset + t) and return the outputs [n, h, d_h] fp32."""
+    n = h_t.shape[0]
+    dev = h_t.device
+    pc = cache.paged
+    layout = cache.layout
+    positions = torch.arange(cache.pos_offset, cache.pos_offset + n, dtype=torch.int32, device=dev)
+    # ---- write side: one K0 launch for all n tokens
+    names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, st.own)
+    proj = st.projector
+    kv_raw = torch.cat([h_t @ proj.w[nm] for nm in names], dim=-1).contiguous()
+    kr_raw = (h_t @ proj.w_kr).contiguous()
+    bt_rep = pc.block_table[:1].expand(n, -1).contiguous()
+    slots = torch.arange(n, dtype=torch.int32, device=dev)
+    ops.cache_append_latent(kv_raw, kr_raw, positions, slots, bt_rep, pc.pool, pc.page_size, branches=blocks,
+                            block0=block0, nblocks=nblocks, dlp=layout.dlp, drp=layout.drp,
+                            alpha_kv=proj.alpha_kv, norm_groups=norm_groups)
+    pc.seqlens.fill_(n)
+    pc._host_lens = [n]
+    # ---- attention side: n pseudo-sequences of lengths 1..n over the same pages
+    q_nope, q_rope = proj.queries(h_t, positions.long())
+    heads = list(range(cfg.h))
+    qn = q_nope.to(torch.bfloat16).contiguous()
+    qr = torch.zeros((n, cfg.h, layout.drp), dtype=torch.bfloat16, device=dev)
+    qr[..., :layout.dr] = q_rope.to(torch.bfloat16)
+    w_uk, w_uv = st.lw.packed(layout, dev, st.own)
+    nb, dlat = kernel_geometry(layout, st.own)
+    sub, dls = ops.latent_geometry(dlat)
+    alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
+    out = torch.empty((n, len(heads), cfg.d_h), dtype=torch.float32, device=dev)
+    for t0 in range(0, n, PREFILL_CHUNK):
+        t1 = min(n, t0 + PREFILL_CHUNK)
+        m = t1 - t0
+        lens = torch.arange(t0 + 1, t1 + 1, dtype=torch.int32, device=dev)
+        nsplit = ops.default_splits(m, t1, nb, sub)
+        q_abs, q_rs = ops.absorb_query(qn[t0:t1], qr[t0:t1].contiguous(), w_uk, nb, dlat, ops.score_scale(cfg.tau))
+        o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, bt_rep[t0:t1], lens, pc.page_size, nb, sub, dls,
+                                          nsplit)
+        out[t0:t1] = ops.combine(o_part, lse, w_uv, alpha)
+    return out
 
 
 def decode_step(cfg: AttnConfig, w, cache, h_t, mode: str = "absorbed"):  # decode.py:341-348

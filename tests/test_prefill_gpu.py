@@ -1,0 +1,90 @@
+"""Causal prefill into the paged cache (attnkit/latent.py:172-230) on
+the GPU: outputs against the reference's own latent_prefill (golden vectors: first and last
+4 tokens), the cache it leaves against the oracle's latent streams (bf16 rounding), and a
+decode step continuing from it against the reference decode output (out_absorbed, which the
+golden generator computes after a cache of the same n-1 tokens).
+
+Tolerance: the decode kernels' (bf16 cache and queries, fp32 softmax / merge): max_rel_err
+against the float64 reference <= 2e-2, the same gate as the decode parity tests."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attnkit_port as ak
+
+from golden_util import load, regen
+
+pytestmark = pytest.mark.gpu
+CASES = ("refdims_mlra4", "refdims_mla", "refdims_mlra2", "refdims_gla2", "tiny_mlra4", "p_mlra4", "p_mla")
+
+
+def _cfg(meta):
+    import paper_2603_02188_b200 as mlra
+
+    c = meta["cfg"]
+    return mlra.AttnConfig(c["variant"], h=c["h"], d=c["d"], d_h=c["d_h"], d_h_rope=c["d_h_rope"], d_c=c["d_c"],
+                           d_cq=c["d_cq"], g=c["g"], branches=c["branches"], scaling=c["scaling"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_prefill_matches_reference_and_continues_decoding(name):
+    import paper_2603_02188_b200 as mlra
+
+    meta, arr = load(name)
+    ocfg, w, hidden = regen(meta)
+    cfg = _cfg(meta)
+    n = meta["n"] - 1
+    res = mlra.latent_prefill(cfg, w, hidden[:n], device="cuda:0")
+    out = res.out
+    assert out.shape == (n, cfg.h, cfg.d_h)
+    for got, want, which in ((out[:4], arr["prefill_head"], "head"), (out[-4:], arr["prefill_tail"], "tail")):
+        err = ak.max_rel_err(got, want)
+        assert err <= 2e-2, f"{name} prefill {which}: max_rel_err {err:.3e}"
+    # the cache it wrote holds the oracle's streams (bf16)
+    streams = ak.latent_streams(ocfg, w, hidden[:n])
+    cache = res.cache
+    assert cache.n == n and cache.reads == 0
+    for sname, want in streams.items():
+        got = cache.peek(sname)
+        scale = max(np.abs(want).max(), 1e-30)
+        assert np.abs(got - want).max() / scale <= 2 ** -7, f"{name} stream {sname}"
+    # decoding continues from the prefilled cache
+    step, cache = mlra.absorbed_decode_step(cfg, w, cache, hidden[n])
+    err = ak.max_rel_err(step, arr["out_absorbed"])
+    assert err <= 2e-2, f"{name} decode after prefill: {err:.3e}"
+
+
+def test_prefill_is_chunked_and_matches_decode_steps():
+    """More queries than one kernel pass (PREFILL_CHUNK patched small) and a position offset:
+    the prefill outputs equal the per-token decode outputs of the same tokens."""
+    import paper_2603_02188_b200 as mlra
+    from paper_2603_02188_b200 import decode as dec
+
+    meta, _ = load("refdims_mlra4")
+    ocfg, w, _ = regen(meta)
+    cfg = _cfg(meta)
+    rng = np.random.default_rng(0)
+    hidden = rng.standard_normal((40, cfg.d))
+    old = dec.PREFILL_CHUNK
+    dec.PREFILL_CHUNK = 16
+    try:
+        res = mlra.latent_prefill(cfg, w, hidden, pos_offset=11, device="cuda:0")
+    finally:
+        dec.PREFILL_CHUNK = old
+    cache = mlra.new_cache(cfg, pos_offset=11, device="cuda:0")
+    for t in range(40):
+        o, cache = mlra.absorbed_decode_step(cfg, w, cache, hidden[t])
+        np.testing.assert_allclose(res.out[t], o, rtol=0, atol=1e-5 * max(1.0, np.abs(o).max()))
+
+
+def test_prefill_rejects_zoo_variants_and_empty_input():
+    import paper_2603_02188_b200 as mlra
+
+    cfg = mlra.trained_config("gqa")
+    with pytest.raises(mlra.RoutingError):
+        mlra.latent_prefill(cfg, {}, np.zeros((2, cfg.d)), device="cuda:0")
+    meta, _ = load("refdims_mla")
+    _, w, _ = regen(meta)
+    res = mlra.latent_prefill(_cfg(meta), w, np.zeros((0, 32)), device="cuda:0")
+    assert res.out.shape == (0, 4, 8) and res.cache.n == 0

@@ -18,8 +18,10 @@ def to_bytes(val, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
 
 summary = {}
-for name, rep, algo in [("mlra4_tp1_b16_n32768", "gpurun_out/k2_tp1.ncu-rep", 603979776),
-                        ("mlra4_tp4_b16_n32768", "gpurun_out/k2_tp4.ncu-rep", 201326592)]:
+for name, rep, algo, kname in [
+        ("mlra4_tp1_b16_n32768", "gpurun_out/k2_tp1.ncu-rep", 603979776, "mlra_decode_kernel (K2)"),
+        ("mlra4_tp4_b16_n32768", "gpurun_out/k2_tp4.ncu-rep", 201326592, "mlra_decode_kernel (K2)"),
+        ("outproj_b16_k3072_d3072", "gpurun_out/k4.ncu-rep", 3072 * 3072 * 2, "outproj_allreduce_kernel (K4, world 1)")]:
     if not os.path.exists(rep):
         continue
     r = raw(rep)
@@ -28,7 +30,7 @@ for name, rep, algo in [("mlra4_tp1_b16_n32768", "gpurun_out/k2_tp1.ncu-rep", 60
     rd = to_bytes(*r["dram__bytes_read.sum"])
     wr = to_bytes(*r["dram__bytes_write.sum"])
     summary[name] = {
-        "kernel": "mlra_decode_kernel (K2)", "duration_us_ncu": dur_us, "dram_bytes_read": rd, "dram_bytes_write": wr,
+        "kernel": kname, "duration_us_ncu": dur_us, "dram_bytes_read": rd, "dram_bytes_write": wr,
         "dram_bytes_per_launch": rd + wr, "algorithmic_bytes": algo, "traffic_over_algorithmic": round((rd + wr) / algo, 4),
         "metrics": {k: " ".join(r[k]) for k in WANT if k in r},
         "note": "ncu --set full --clock-control none, cold L2, serialised: compare shares/bytes, not absolute time",
