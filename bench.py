@@ -156,12 +156,13 @@ class StepRunner:
 
     GRAPH_STEPS = 10
 
-    def __init__(self, cfg, own, batch, ctx, device, tp_group=None, full_heads=False):
+    def __init__(self, cfg, own, batch, ctx, device, tp_group=None, full_heads=False, reducer=None):
         import torch
 
         self.torch = torch
         self.engines = [make_engine(cfg, own, batch, ctx, 1000 + i, device) for i in range(2)]
         self.tp_group = tp_group
+        self.reducer = reducer  # collective.PeerAllReduce (K5) or None (NCCL all_reduce)
         self.cfg = cfg
         self.heads = list(self.engines[0][0].heads)
         self.full = torch.zeros((batch, cfg.h, cfg.d_h), dtype=torch.float32, device=device) if tp_group else None
@@ -191,7 +192,10 @@ class StepRunner:
             else:
                 self.full.zero_()
                 self.full[:, self.heads] = out
-            dist.all_reduce(self.full, group=self.tp_group)
+            if self.reducer is not None:
+                self.reducer(self.full)
+            else:
+                dist.all_reduce(self.full, group=self.tp_group)
         return out
 
     def run(self, steps):
@@ -461,7 +465,11 @@ def run_ours(args):
 
     cfg = trained_config("mlra4")
     own = shard_ownership(cfg, tp, rank % tp)
-    runner = StepRunner(cfg, own, BATCH_PER_GROUP, CTX, device, tp_group=groups[rank // tp] if groups else None)
+    tp_group = groups[rank // tp] if groups else None
+    reducer, allreduce_kind = None, "none (tp1)"
+    if tp_group is not None:
+        reducer, allreduce_kind = make_reducer(args.allreduce, tp_group, BATCH_PER_GROUP * cfg.h * cfg.d_h, device)
+    runner = StepRunner(cfg, own, BATCH_PER_GROUP, CTX, device, tp_group=tp_group, reducer=reducer)
     with ClockSampler(local_rank) as clk:
         ms = time_graph_steps(runner, args.steps, args.warmup, rank_sync)
         t = torch.tensor([ms], device=device)
@@ -516,7 +524,7 @@ def run_ours(args):
                        "d_c=512, d_h^R=64)", "global_batch": BATCH_PER_GROUP * max(1, n_gpus // 4), "seq_len": CTX,
                        "parallelism": f"tp{tp}" + (f"xdp{n_gpus // tp}" if n_gpus > tp else ""),
                        "l2": "2 distinct caches alternated; per-step working set > 126 MB L2",
-                       "graphs": "10 alternating steps per CUDA graph replay",
+                       "graphs": "10 alternating steps per CUDA graph replay", "allreduce": allreduce_kind,
                        "algorithmic_bytes_per_gpu_per_step": bytes_rank, "page_size": 128,
                        "nsplit": runner.engines[0][0].nsplit},
             "gpu_launches": 3 * args.steps,
@@ -681,6 +689,34 @@ def output_side_times(device):
     return res
 
 
+def make_reducer(kind, group, n, device):
+    """The TP step's sum over ranks: K5 over NVLink peer memory (default) or NCCL. K5 is checked
+    once against NCCL on a random buffer; any failure or mismatch falls back to NCCL (recorded)."""
+    import torch
+    import torch.distributed as dist
+
+    if kind == "nccl":
+        return None, "nccl all_reduce"
+    try:
+        from paper_2603_02188_b200.collective import PeerAllReduce
+
+        red = PeerAllReduce(group, n, device)
+        g = torch.Generator(device=device).manual_seed(dist.get_rank())
+        x = torch.randn(n, generator=g, device=device)
+        a, b = x.clone(), x.clone()
+        red(a)
+        dist.all_reduce(b, group=group)
+        torch.cuda.synchronize()
+        ok = torch.tensor([float(torch.allclose(a, b, rtol=1e-5, atol=1e-5))], device=device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() == 1.0:
+            return red, "peer (K5 mlra_allreduce: one-shot over NVLink IPC mappings, rank-order sum)"
+        red.close()
+        return None, "nccl all_reduce (K5 self-check mismatch)"
+    except Exception as e:  # IPC / peer access unavailable
+        return None, f"nccl all_reduce (K5 unavailable: {type(e).__name__})"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -689,6 +725,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--quick", action="store_true", help="skip the per-GPU TP4 / MLA comparison runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline sample")
+    ap.add_argument("--allreduce", choices=("peer", "nccl"), default="peer",
+                    help="TP step sum: K5 over NVLink peer memory (default) or NCCL")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

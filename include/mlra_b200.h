@@ -188,6 +188,18 @@ int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, con
                      const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
                      unsigned epoch, void* const* workspace, void* stream);
 
+/*
+ * K5 -- one-shot all-reduce of n fp32 values over peer memory: y = sum over ranks of x_r in
+ * ascending rank order (the device-order sum of per-rank contributions, attnkit/decode.py:
+ * 264-285, tpsim.py:275-276), bit-identical on every rank; replaces the TP step's NCCL
+ * all_reduce. comm[r] = rank r's region (mlra_allreduce_comm_bytes, zero-filled once) as mapped
+ * in this process. The call epoch is kept in device memory, so the call can be captured in a
+ * CUDA graph and replayed. All ranks must make the same sequence of calls.
+ */
+size_t mlra_allreduce_comm_bytes(int n, int world);
+int mlra_allreduce(const float* x, float* y, int n, int rank, int world, void* const* comm, void* stream);
+int mlra_allreduce_sim(const float* const* x, float* const* y, int n, int world, void* const* comm, void* stream);
+
 /* Communication region: a dedicated zero-filled cudaMalloc (so its IPC handle maps exactly). */
 int mlra_comm_alloc(size_t bytes, void** dev_ptr_out);
 int mlra_comm_free(void* dev_ptr);

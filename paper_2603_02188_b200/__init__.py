@@ -45,7 +45,8 @@ def __getattr__(name):
         "latent_prefill": ("decode", "latent_prefill"), "PrefillOutput": ("decode", "PrefillOutput"),
         "outproj": ("outproj", None), "OutputProjection": ("outproj", "OutputProjection"),
         "TpComm": ("outproj", "TpComm"), "host_loop": ("host_loop", None),
-        "MicroBatchLoop": ("host_loop", "MicroBatchLoop"),
+        "MicroBatchLoop": ("host_loop", "MicroBatchLoop"), "collective": ("collective", None),
+        "PeerAllReduce": ("collective", "PeerAllReduce"),
     }
     if name in lazy:
         import importlib

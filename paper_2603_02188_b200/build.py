@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmlra_b200.so")
 SOURCES = ["capi.cu"]
-HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cuh"]
+HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cuh", "allreduce_kernel.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

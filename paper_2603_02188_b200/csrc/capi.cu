@@ -13,6 +13,7 @@
 #include "aux_kernels.cuh"
 #include "decode_kernel.cuh"
 #include "outproj_kernel.cuh"
+#include "allreduce_kernel.cuh"
 
 namespace {
 
@@ -752,6 +753,66 @@ int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, con
   p.resid = resid;
   p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = 0, p.epoch = epoch;
   return outproj_launch(p, attn, gate_pre, workspace, world, true, static_cast<cudaStream_t>(stream));
+}
+
+// ----------------------------------------------------------------------------- K5 (peer all-reduce)
+size_t mlra_allreduce_comm_bytes(int n, int world) {
+  if (n <= 0 || world <= 0) return 0;
+  const int nchunks = (n + mlra::kArChunk - 1) / mlra::kArChunk;
+  return mlra::ar_recv_floats(n, world) * 4 + mlra::ar_flag_words(nchunks, world) * 4 + 16;
+}
+
+static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cudaStream_t st) {
+  if (p.n <= 0) return MLRA_OK;
+  if (p.world < 1 || p.world > mlra::kArMaxRanks)
+    return fail(MLRA_ERR_CONFIG, "allreduce: world %d outside [1, %d]", p.world, mlra::kArMaxRanks);
+  p.nchunks = (p.n + mlra::kArChunk - 1) / mlra::kArChunk;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mlra::allreduce_kernel, mlra::kArThreads, 0);
+  if (size_t(p.nchunks) * nlocal > size_t(sms) * per_sm)
+    return fail(MLRA_ERR_CONFIG, "allreduce: %d CTAs cannot all be resident (%d SMs x %d)", p.nchunks * nlocal, sms,
+                per_sm);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3(p.nchunks, nlocal);
+  cfg.blockDim = dim3(mlra::kArThreads);
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = sim ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, mlra::allreduce_kernel, p) != cudaSuccess) return cuda_check("allreduce launch");
+  return cuda_check("allreduce launch");
+}
+
+int mlra_allreduce(const float* x, float* y, int n, int rank, int world, void* const* comm, void* stream) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(MLRA_ERR_CONFIG, "allreduce: rank %d of %d", rank, world);
+  if (comm == nullptr || x == nullptr || y == nullptr) return fail(MLRA_ERR_CONFIG, "allreduce: null pointer");
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
+    return fail(MLRA_ERR_CONFIG, "allreduce: x and y must be 16-byte aligned");
+  mlra::AllReduceParams p = {};
+  p.x[0] = x;
+  p.y[0] = y;
+  for (int r = 0; r < world && r < mlra::kArMaxRanks; ++r) p.comm[r] = static_cast<float*>(comm[r]);
+  p.n = n, p.world = world, p.rank0 = rank;
+  return allreduce_launch(p, 1, false, static_cast<cudaStream_t>(stream));
+}
+
+int mlra_allreduce_sim(const float* const* x, float* const* y, int n, int world, void* const* comm, void* stream) {
+  if (world < 1 || world > mlra::kArMaxRanks) return fail(MLRA_ERR_CONFIG, "allreduce_sim: world %d", world);
+  if (comm == nullptr || x == nullptr || y == nullptr) return fail(MLRA_ERR_CONFIG, "allreduce_sim: null pointer");
+  mlra::AllReduceParams p = {};
+  for (int r = 0; r < world; ++r) {
+    if (((reinterpret_cast<uintptr_t>(x[r]) | reinterpret_cast<uintptr_t>(y[r])) & 15) != 0)
+      return fail(MLRA_ERR_CONFIG, "allreduce_sim: x and y must be 16-byte aligned");
+    p.x[r] = x[r];
+    p.y[r] = y[r];
+    p.comm[r] = static_cast<float*>(comm[r]);
+  }
+  p.n = n, p.world = world, p.rank0 = 0;
+  return allreduce_launch(p, world, true, static_cast<cudaStream_t>(stream));
 }
 
 int mlra_comm_alloc(size_t bytes, void** dev_ptr_out) {

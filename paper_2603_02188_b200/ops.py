@@ -375,3 +375,34 @@ def ipc_open(handle: bytes) -> int:
 def ipc_close(ptr: int) -> None:
     _lib.check(_lib.load().mlra_ipc_close(ptr), "mlra_ipc_close")
 
+
+# ----------------------------------------------------------------------------- K5: peer all-reduce
+def allreduce_comm_bytes(n: int, world: int) -> int:
+    return int(_lib.load().mlra_allreduce_comm_bytes(n, world))
+
+
+def allreduce(x: torch.Tensor, y: torch.Tensor, rank: int, world: int, comm_ptrs) -> torch.Tensor:
+    """K5: y = sum over ranks of x (ascending rank order) through the peer regions comm_ptrs."""
+    _need(x, torch.float32, "x")
+    _need(y, torch.float32, "y")
+    if x.numel() != y.numel():
+        raise ShapeMismatchError(f"allreduce: x has {x.numel()} values, y {y.numel()}")
+    rc = _lib.load().mlra_allreduce(x.data_ptr(), y.data_ptr(), x.numel(), rank, world, _ptr_array(comm_ptrs),
+                                    _stream())
+    _lib.check(rc, "mlra_allreduce")
+    return y
+
+
+def allreduce_sim(xs, ys, comms) -> None:
+    """K5 with len(xs) ranks simulated on one device (tests); comms: uint8 CUDA tensors."""
+    world = len(xs)
+    n = xs[0].numel()
+    for x, y, c in zip(xs, ys, comms):
+        _need(x, torch.float32, "x")
+        _need(y, torch.float32, "y")
+        if x.numel() != n or y.numel() != n or c.numel() < allreduce_comm_bytes(n, world):
+            raise ShapeMismatchError("allreduce_sim: inconsistent sizes")
+    rc = _lib.load().mlra_allreduce_sim(_ptr_array([x.data_ptr() for x in xs]), _ptr_array([y.data_ptr() for y in ys]),
+                                        n, world, _ptr_array([c.data_ptr() for c in comms]), _stream())
+    _lib.check(rc, "mlra_allreduce_sim")
+

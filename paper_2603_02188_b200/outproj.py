@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import ops
+from .collective import PeerRegions
 from .errors import ConfigError, ShapeMismatchError
 
 __all__ = ["TpComm", "OutputProjection", "next_epoch"]
@@ -38,38 +39,20 @@ def next_epoch(n: int) -> int:
     return n % _EPOCH_CYCLE + 1
 
 
-class TpComm:
+class TpComm(PeerRegions):
     """Communication regions of a process group for K4 (one per rank, mapped in every rank)."""
 
     def __init__(self, group, batch: int, d: int, device=None):
         import torch.distributed as dist
 
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
         self.batch, self.d = int(batch), int(d)
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.nbytes = ops.outproj_comm_bytes(batch, d, self.world)
-        with torch.cuda.device(self.device):
-            self.own = ops.comm_alloc(self.nbytes)
-            handles = [None] * self.world
-            dist.all_gather_object(handles, ops.ipc_handle(self.own), group=group)
-            self.ptrs = [self.own if r == self.rank else ops.ipc_open(handles[r]) for r in range(self.world)]
+        super().__init__(group, ops.outproj_comm_bytes(batch, d, dist.get_world_size(group)), device)
         self.calls = 0
 
     def epoch(self) -> int:
         e = next_epoch(self.calls)
         self.calls += 1
         return e
-
-    def close(self) -> None:
-        if self.ptrs is None:
-            return
-        with torch.cuda.device(self.device):
-            for r, p in enumerate(self.ptrs):
-                if r != self.rank:
-                    ops.ipc_close(p)
-            ops.comm_free(self.own)
-        self.ptrs = None
 
 
 def _head_columns(heads, d_h: int) -> np.ndarray:

@@ -253,7 +253,9 @@ class TPDecodeGroup:
     ``compute`` is injectable so the plumbing is testable on CPU with the gloo backend.
     """
 
-    def __init__(self, cfg: AttnConfig, tp: int, rank: int, world_size: int, group=None, compute=None):
+    def __init__(self, cfg: AttnConfig, tp: int, rank: int, world_size: int, group=None, compute=None,
+                 reducer=None):
+        self.reducer = reducer  # collective.PeerAllReduce (K5, peer memory) or None (torch.distributed)
         self.cfg = cfg
         self.tp = tp
         self.rank = rank
@@ -283,7 +285,10 @@ class TPDecodeGroup:
             full_out.zero_()
             full_out[:, heads] = local
         if self.tp > 1:
-            dist.all_reduce(full_out, op=dist.ReduceOp.SUM, group=self.group)
+            if self.reducer is not None:
+                self.reducer(full_out)
+            else:
+                dist.all_reduce(full_out, op=dist.ReduceOp.SUM, group=self.group)
         return full_out
 
 
