@@ -527,7 +527,7 @@ def run_ours(args):
                        "graphs": "10 alternating steps per CUDA graph replay", "allreduce": allreduce_kind,
                        "algorithmic_bytes_per_gpu_per_step": bytes_rank, "page_size": 128,
                        "nsplit": runner.engines[0][0].nsplit},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (3 + (1 if reducer is not None else 0)) * args.steps,
         }
         line.update(extras)
         print(json.dumps(line))

@@ -173,20 +173,20 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
  *   mlra_outproj_workspace_bytes) for the tensor-core product (fp32 accumulation).
  * world == 1: comm may be NULL. world > 1: comm[r] = rank r's communication region
  * (mlra_outproj_comm_bytes, zero-filled once) as mapped in THIS process (its own region and
- * the peers' through mlra_ipc_open); epoch = 1, 2, 3, ... per call, identical on all ranks.
+ * the peers' through mlra_ipc_open). The call epoch is kept in device memory (graph-safe); all
+ * ranks must make the same sequence of calls.
  * The rank partials are exchanged by one-shot stores into every peer's region and summed in
  * ascending rank order -- no NCCL call; a peer missing for 4 s aborts the kernel.
  */
 size_t mlra_outproj_comm_bytes(int B, int D, int world);
 size_t mlra_outproj_workspace_bytes(int B, int K);  /* the gated bf16 operand [B, K] */
 int mlra_outproj(const float* attn, const float* gate_pre, const void* w_o, const float* resid, float* y, int B,
-                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* workspace,
-                 void* stream);
+                 int K, int D, int rank, int world, void* const* comm, void* workspace, void* stream);
 /* The same kernels with `world` ranks simulated on ONE device (tests): arrays of world per-rank
  * pointers, one cooperative launch. Fails with MLRA_ERR_CONFIG when the grid cannot be resident. */
 int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, const void* const* w_o,
                      const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
-                     unsigned epoch, void* const* workspace, void* stream);
+                     void* const* workspace, void* stream);
 
 /*
  * K5 -- one-shot all-reduce of n fp32 values over peer memory: y = sum over ranks of x_r in

@@ -41,8 +41,8 @@ SIGNATURES = {
     "mlra_gqa_decode_step": (_I, [_P] * 6 + [_I] * 8 + [_F, _P]),
     "mlra_outproj_comm_bytes": (ctypes.c_size_t, [_I, _I, _I]),
     "mlra_outproj_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
-    "mlra_outproj": (_I, [_P] * 5 + [_I] * 5 + [_P, ctypes.c_uint, _P, _P]),
-    "mlra_outproj_sim": (_I, [_P] * 5 + [_I] * 4 + [_P, ctypes.c_uint, _P, _P]),
+    "mlra_outproj": (_I, [_P] * 5 + [_I] * 5 + [_P, _P, _P]),
+    "mlra_outproj_sim": (_I, [_P] * 5 + [_I] * 4 + [_P, _P, _P]),
     "mlra_allreduce_comm_bytes": (ctypes.c_size_t, [_I, _I]),
     "mlra_allreduce": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "mlra_allreduce_sim": (_I, [_P, _P, _I, _I, _P, _P]),

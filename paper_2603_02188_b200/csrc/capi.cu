@@ -636,7 +636,7 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
 size_t mlra_outproj_comm_bytes(int B, int D, int world) {
   if (B <= 0 || D <= 0 || world <= 0) return 0;
   const size_t nslabs = size_t(mlra::outproj_nslabs(D));
-  return size_t(2) * world * B * D * 4 + size_t(2) * world * nslabs * mlra::kOpMaxKS * 4;
+  return size_t(2) * world * B * D * 4 + size_t(2) * world * nslabs * mlra::kOpMaxKS * 4 + 16;
 }
 
 static int outproj_check(int B, int K, int D, int world) {
@@ -723,27 +723,26 @@ static int outproj_launch(mlra::OutProjParams& p, const float* const* attn, cons
 }
 
 int mlra_outproj(const float* attn, const float* gate_pre, const void* w_o, const float* resid, float* y, int B,
-                 int K, int D, int rank, int world, void* const* comm, unsigned epoch, void* workspace,
-                 void* stream) {
+                 int K, int D, int rank, int world, void* const* comm, void* workspace, void* stream) {
   if (int rc = outproj_check(B, K, D, world)) return rc;
   if (rank < 0 || rank >= world) return fail(MLRA_ERR_CONFIG, "outproj: rank %d of %d", rank, world);
-  if (world > 1 && (comm == nullptr || epoch == 0))
-    return fail(MLRA_ERR_CONFIG, "outproj: world %d needs the communication regions and an epoch >= 1", world);
+  if (world > 1 && comm == nullptr)
+    return fail(MLRA_ERR_CONFIG, "outproj: world %d needs the communication regions", world);
   mlra::OutProjParams p = {};
   p.w_o[0] = static_cast<const __nv_bfloat16*>(w_o);
   p.y[0] = y;
   p.resid = resid;
   for (int r = 0; r < world && world > 1; ++r) p.comm[r] = static_cast<float*>(comm[r]);
-  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = rank, p.epoch = epoch;
+  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = rank;
   return outproj_launch(p, &attn, &gate_pre, &workspace, 1, false, static_cast<cudaStream_t>(stream));
 }
 
 int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, const void* const* w_o,
                      const float* resid, float* const* y, int B, int K, int D, int world, void* const* comm,
-                     unsigned epoch, void* const* workspace, void* stream) {
+                     void* const* workspace, void* stream) {
   if (int rc = outproj_check(B, K, D, world)) return rc;
-  if (attn == nullptr || w_o == nullptr || y == nullptr || workspace == nullptr || comm == nullptr || epoch == 0)
-    return fail(MLRA_ERR_CONFIG, "outproj_sim: needs per-rank tensors, workspaces, comm regions and epoch >= 1");
+  if (attn == nullptr || w_o == nullptr || y == nullptr || workspace == nullptr || comm == nullptr)
+    return fail(MLRA_ERR_CONFIG, "outproj_sim: needs per-rank tensors, workspaces and comm regions");
   mlra::OutProjParams p = {};
   for (int r = 0; r < world; ++r) {
     p.w_o[r] = static_cast<const __nv_bfloat16*>(w_o[r]);
@@ -751,7 +750,7 @@ int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, con
     p.comm[r] = static_cast<float*>(comm[r]);
   }
   p.resid = resid;
-  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = 0, p.epoch = epoch;
+  p.B = B, p.K = K, p.D = D, p.world = world, p.rank0 = 0;
   return outproj_launch(p, attn, gate_pre, workspace, world, true, static_cast<cudaStream_t>(stream));
 }
 

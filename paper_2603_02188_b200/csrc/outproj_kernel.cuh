@@ -31,7 +31,9 @@
 //   every peer has pushed call e+1, which the peer does after finishing call e's reads.
 //
 // Communication region of a rank (mlra_outproj_comm_bytes): fp32 recv [2][world][B][D], then
-// uint32 flags [2][world][nslabs * kOpMaxKS]; zero-filled once, epochs 1, 2, 3, ...
+// uint32 flags [2][world][nslabs * kOpMaxKS], then uint32 {epoch counter, done counter};
+// zero-filled once. The call epoch lives there (read at kernel start, advanced by the last CTA
+// to finish), so the call can be captured in a CUDA graph and replayed.
 // Sim mode (tests on one GPU): gridDim.y = world CTA rows act as the ranks on one device, KS = 1,
 // one cooperative launch so every CTA is resident (flag waits cannot starve).
 #pragma once
@@ -63,7 +65,6 @@ struct OutProjParams {
   const float* resid;                        // [B, D] fp32 or null (shared by the ranks)
   float* comm[kOpMaxRanks];                  // communication region of every GLOBAL rank
   int B, K, D, world, rank0, nslabs, ks_count, k_slice;
-  uint32_t epoch;
 };
 
 inline size_t outproj_smem() { return size_t(kOpStages) * kOpWBytes + kOpABytes + kOpSlotBytes; }
@@ -227,10 +228,16 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
     return;
   }
   // ---- one-shot all-reduce of my rows across ranks
-  const int W = p.world, par = int(p.epoch & 1u);
+  const int W = p.world;
   const size_t recv_floats = size_t(2) * W * B * D;
   const size_t flag_idx = size_t(slab) * kOpMaxKS + ks;
   const size_t flags_per_rank = size_t(p.nslabs) * kOpMaxKS;
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(p.comm[rank] + recv_floats) + size_t(2) * W * flags_per_rank;
+  __shared__ uint32_t s_epoch;
+  if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(ctr) + 1u;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  const int par = int(epoch & 1u);
   for (int r = 0; r < W; ++r) {
     float* dst = p.comm[r] + (size_t(par) * W + rank) * size_t(B) * D;
     for (int i = tid; i < nrows * (kOpNC / 4); i += kOpThreads) {
@@ -244,13 +251,13 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
   if (tid < W) {
     __threadfence_system();
     uint32_t* flags = reinterpret_cast<uint32_t*>(p.comm[tid] + recv_floats);
-    st_release_sys_u32(flags + (size_t(par) * W + rank) * flags_per_rank + flag_idx, p.epoch);
+    st_release_sys_u32(flags + (size_t(par) * W + rank) * flags_per_rank + flag_idx, epoch);
   }
   if (tid < W) {  // wait for the world partials of my rows (a peer missing for 4 s traps)
     const uint32_t* flags = reinterpret_cast<const uint32_t*>(p.comm[rank] + recv_floats);
     const uint32_t* f = flags + (size_t(par) * W + tid) * flags_per_rank + flag_idx;
     const unsigned long long t_start = op_globaltimer();
-    while (ld_acquire_sys_u32(f) != p.epoch) {
+    while (ld_acquire_sys_u32(f) != epoch) {
       if (op_globaltimer() - t_start > 4000000000ull) __trap();
       __nanosleep(64);
     }
@@ -264,6 +271,13 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
     float s = 0.f;
     for (int r = 0; r < W; ++r) s += __ldcv(recv + size_t(r) * B * D + o);  // ascending rank order
     p.y[li][o] = (p.resid != nullptr ? p.resid[o] : 0.f) + s;
+  }
+  if (tid == 0) {  // advance this rank's epoch once every CTA of the call has read it
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1u) {
+      ctr[1] = 0u;
+      atomicExch(ctr, epoch);
+    }
   }
   MLRA_OP_STAMP(5);
 }

@@ -306,22 +306,22 @@ def outproj_workspace(batch: int, k: int, device) -> torch.Tensor:
 
 
 def outproj(attn: torch.Tensor, gate_pre: torch.Tensor | None, w_o: torch.Tensor, resid: torch.Tensor | None,
-            y: torch.Tensor, rank: int = 0, world: int = 1, comm_ptrs=None, epoch: int = 0,
+            y: torch.Tensor, rank: int = 0, world: int = 1, comm_ptrs=None,
             workspace: torch.Tensor | None = None) -> torch.Tensor:
     """K4a + K4: y = resid + sum over ranks of (attn * sigmoid(gate_pre)) @ w_o (zoo.py:125-149).
-    world > 1: comm_ptrs = every rank's communication region as mapped here, epoch >= 1."""
+    world > 1: comm_ptrs = every rank's communication region as mapped here."""
     B, K, D = _outproj_shapes(attn, gate_pre, w_o, resid, y)
     ws = workspace if workspace is not None else outproj_workspace(B, K, attn.device)
     if ws.numel() < _lib.load().mlra_outproj_workspace_bytes(B, K):
         raise ShapeMismatchError("outproj: workspace too small")
     comm = _ptr_array(comm_ptrs) if comm_ptrs is not None else None
     rc = _lib.load().mlra_outproj(attn.data_ptr(), _lib.ptr(gate_pre), w_o.data_ptr(), _lib.ptr(resid), y.data_ptr(),
-                                  B, K, D, rank, world, comm, epoch & 0xFFFFFFFF, ws.data_ptr(), _stream())
+                                  B, K, D, rank, world, comm, ws.data_ptr(), _stream())
     _lib.check(rc, "mlra_outproj")
     return y
 
 
-def outproj_sim(attns, gates, w_os, resid, ys, comms, epoch: int) -> None:
+def outproj_sim(attns, gates, w_os, resid, ys, comms) -> None:
     """K4 with len(attns) ranks simulated on one device (tests): per-rank lists of tensors,
     comms = per-rank communication regions (uint8 CUDA tensors of outproj_comm_bytes)."""
     world = len(attns)
@@ -335,7 +335,7 @@ def outproj_sim(attns, gates, w_os, resid, ys, comms, epoch: int) -> None:
                                       None if gates is None else _ptr_array([g.data_ptr() for g in gates]),
                                       _ptr_array([w.data_ptr() for w in w_os]), _lib.ptr(resid),
                                       _ptr_array([y.data_ptr() for y in ys]), B, K, D, world,
-                                      _ptr_array([c.data_ptr() for c in comms]), epoch & 0xFFFFFFFF,
+                                      _ptr_array([c.data_ptr() for c in comms]),
                                       _ptr_array([w.data_ptr() for w in wss]), _stream())
     _lib.check(rc, "mlra_outproj_sim")
 

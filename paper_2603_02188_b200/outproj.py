@@ -29,14 +29,7 @@ from . import ops
 from .collective import PeerRegions
 from .errors import ConfigError, ShapeMismatchError
 
-__all__ = ["TpComm", "OutputProjection", "next_epoch"]
-
-_EPOCH_CYCLE = 2 ** 31 - 2  # even: the epoch parity keeps alternating across the wrap
-
-
-def next_epoch(n: int) -> int:
-    """Epoch of the n-th call (n = 0, 1, ...): 1, 2, ..., 2^31 - 2, 1, 2, ..."""
-    return n % _EPOCH_CYCLE + 1
+__all__ = ["TpComm", "OutputProjection"]
 
 
 class TpComm(PeerRegions):
@@ -47,12 +40,6 @@ class TpComm(PeerRegions):
 
         self.batch, self.d = int(batch), int(d)
         super().__init__(group, ops.outproj_comm_bytes(batch, d, dist.get_world_size(group)), device)
-        self.calls = 0
-
-    def epoch(self) -> int:
-        e = next_epoch(self.calls)
-        self.calls += 1
-        return e
 
 
 def _head_columns(heads, d_h: int) -> np.ndarray:
@@ -108,4 +95,4 @@ class OutputProjection:
         if self.comm is None or self.comm.world == 1:
             return ops.outproj(a.contiguous(), gate_pre, self.w_o, resid, y, workspace=self.workspace)
         return ops.outproj(a.contiguous(), gate_pre, self.w_o, resid, y, self.comm.rank, self.comm.world,
-                           self.comm.ptrs, self.comm.epoch(), workspace=self.workspace)
+                           self.comm.ptrs, workspace=self.workspace)

@@ -1,7 +1,7 @@
 """Output side on the CPU: the oracle's gated_output / attention half of
 block_forward (attnkit/zoo.py:125-152) pinned to golden vectors from the reference, the
 tensor-parallel restatement (per-rank gate + W_o, summed in device order) against the
-single-device form for every sharding the decode path uses, the epoch sequence, and the C-ABI
+single-device form for every sharding the decode path uses, and the C-ABI
 validation of K4 (no GPU needed)."""
 
 import numpy as np
@@ -45,33 +45,24 @@ def test_tp_output_side_is_the_device_order_sum(phi, by):
     np.testing.assert_allclose(got, arr["y_gated"], rtol=1e-10, atol=1e-10)
 
 
-def test_epoch_sequence_alternates_parity_across_the_wrap():
-    from paper_2603_02188_b200.outproj import _EPOCH_CYCLE, next_epoch
-
-    assert [next_epoch(i) for i in range(4)] == [1, 2, 3, 4]
-    seq = [next_epoch(i) for i in range(_EPOCH_CYCLE - 3, _EPOCH_CYCLE + 3)]
-    assert 0 not in seq
-    assert all((a ^ b) & 1 for a, b in zip(seq, seq[1:]))
-
-
 def test_outproj_c_abi_validation():
     from paper_2603_02188_b200 import _lib
 
     lib = _lib.load()
-    assert lib.mlra_outproj_comm_bytes(16, 3072, 4) == 2 * 4 * 16 * 3072 * 4 + 2 * 4 * 24 * 8 * 4
+    assert lib.mlra_outproj_comm_bytes(16, 3072, 4) == 2 * 4 * 16 * 3072 * 4 + 2 * 4 * 24 * 8 * 4 + 16
     assert lib.mlra_outproj_comm_bytes(0, 3072, 4) == 0
     assert lib.mlra_outproj_workspace_bytes(16, 3072) == 16 * 3072 * 2
-    rc = lib.mlra_outproj(None, None, None, None, None, 65, 768, 3072, 0, 1, None, 0, None, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 65, 768, 3072, 0, 1, None, None, None)
     assert rc == -1 and b"B=65" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 764, 3072, 0, 1, None, 0, None, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 764, 3072, 0, 1, None, None, None)
     assert rc == -1 and b"multiples of 8" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 2, 2, None, 1, None, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 2, 2, None, None, None)
     assert rc == -2 and b"rank 2 of 2" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 2, None, 1, None, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 2, None, None, None)
     assert rc == -2 and b"communication regions" in lib.mlra_last_error()
-    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 9, None, 1, None, None)
+    rc = lib.mlra_outproj(None, None, None, None, None, 16, 768, 3072, 0, 9, None, None, None)
     assert rc == -2 and b"world 9" in lib.mlra_last_error()
-    rc = lib.mlra_outproj_sim(None, None, None, None, None, 16, 768, 3072, 2, None, 1, None, None)
+    rc = lib.mlra_outproj_sim(None, None, None, None, None, 16, 768, 3072, 2, None, None, None)
     assert rc == -2
     assert lib.mlra_ipc_handle(None, None) == -2
     assert lib.mlra_comm_alloc(0, None) == -2

@@ -55,11 +55,9 @@ for B, K, D in shapes:
         gates = [gate] * world
         ys = [torch.empty(B, D, device=dev) for _ in range(world)]
         comms = [torch.zeros(ops.outproj_comm_bytes(B, D, world), dtype=torch.uint8, device=dev) for _ in range(world)]
-        ep = [0]
 
         def sim():
-            ep[0] += 1
-            ops.outproj_sim(attns, gates, w_os[:world], resid, ys, comms, ep[0])
+            ops.outproj_sim(attns, gates, w_os[:world], resid, ys, comms)
 
         try:
             print(f"      sim world {world}: {gtime(sim):6.2f} us (all ranks on one GPU)")
