@@ -17,13 +17,21 @@ ctxs = [4096, 8192, 16384, 32768, 65536, 131072]
 batches = [1, 4, 16, 64]
 if len(sys.argv) > 1:
     ctxs = [int(x) for x in sys.argv[1].split(",")]
-for name, own, phi in (("tp4_rank", shard_ownership(cfg, 4, 0), 4), ("tp1", None, 1)):
+if len(sys.argv) > 2:
+    batches = [int(x) for x in sys.argv[2].split(",")]
+mla = trained_config("mla")
+layouts = {"tp4_rank": (cfg, shard_ownership(cfg, 4, 0), 4), "tp1": (cfg, None, 1),
+           "mla_tp4_rank": (mla, shard_ownership(mla, 4, 0), 4), "mla_tp1": (mla, None, 1)}
+names = sys.argv[3].split(",") if len(sys.argv) > 3 else ["tp4_rank", "tp1"]
+out_md = sys.argv[4] if len(sys.argv) > 4 else "gpurun_out/sweep.md"
+for name in names:
+    c, own, phi = layouts[name]
     for n in ctxs:
         for B in batches:
-            runner = bench.StepRunner(cfg, own, B, n, dev)
+            runner = bench.StepRunner(c, own, B, n, dev)
             step_ms = bench.time_graph_steps(runner, 20, 10, torch.cuda.synchronize)
             k2_ms = bench.time_k2_alone(runner.engines, 20)
-            nbytes = algorithmic_bytes(cfg, phi, [n] * B)
+            nbytes = algorithmic_bytes(c, phi, [n] * B)
             r = {"layout": name, "ctx": n, "batch": B, "nsplit": runner.engines[0][0].nsplit,
                  "step_us": round(step_ms * 1e3, 2), "step_gbs": round(nbytes / (step_ms * 1e-3) / 1e9, 1),
                  "k2_us": round(k2_ms * 1e3, 2), "k2_gbs": round(nbytes / (k2_ms * 1e-3) / 1e9, 1),
@@ -34,7 +42,7 @@ for name, own, phi in (("tp4_rank", shard_ownership(cfg, 4, 0), 4), ("tp1", None
             del runner
             torch.cuda.empty_cache()
 os.makedirs("gpurun_out", exist_ok=True)
-with open("gpurun_out/sweep.md", "w") as f:
+with open(out_md, "w") as f:
     f.write(f"peak (MEASURED_PEAKS hbm_gbs) = {peak} GB/s\n\n")
     f.write("| layout | ctx | B | nsplit | step µs | step GB/s | step frac | K2 µs | K2 GB/s | K2 frac |\n")
     f.write("|---|---|---|---|---|---|---|---|---|---|\n")
