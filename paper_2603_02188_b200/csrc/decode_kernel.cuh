@@ -184,7 +184,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   constexpr bool kSharedRope = NB > 1 && !GQA;
   const uint32_t S_COL = 0, SR_COL = 2 * NPAD, O_COL = (kSharedRope ? 4 : 2) * NPAD;
 
-  if (tid == 0) {
+  if (tid == 0) {  // the producer's first TMA needs both descriptors: fetch them first
+    tma_prefetch_desc(&lat_map);
+    tma_prefetch_desc(&rope_map);
+  }
+  if (tid == 32) {  // barrier init off the producer warp: it overlaps the page-id loads
     for (int i = 0; i < p.lat_slots; ++i) { mbar_init(&lat_full[i], 1); mbar_init(&lat_empty[i], 1); }
     for (int i = 0; i < p.rope_slots; ++i) { mbar_init(&rope_full[i], 1); mbar_init(&rope_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
@@ -196,20 +200,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int i = 0; i < 2; ++i) mbar_init(&sr_empty[i], kSoftThreads);
     tmem_base_sh[1] = 0;  // debug-trace check of the final CTA barrier
     fence_barrier_init();
-    tma_prefetch_desc(&lat_map);
-    tma_prefetch_desc(&rope_map);
   }
-  // The TMA producer (warp 0) only needs the mbarriers: it announces them (bar.arrive) and
-  // starts streaming without waiting for the TMEM allocation and the consumers' setup.
-  if (warp == 0) {
-    __syncwarp();
-    named_bar_arrive(6, kNumThreads);
-  } else {
-    if (warp == 1) tmem_alloc<kTmemCols>(tmem_base_sh);
+  // The TMA producer (warp 0) fetches its first page ids while warp 1 initialises the
+  // mbarriers; it waits for them (named barrier 7 with warp 1) only before its first mbarrier
+  // use, and never for the TMEM allocation or the consumers' setup (barrier 6, warps 1-10).
+  if (warp != 0) {
+    if (warp == 1) {
+      __syncwarp();
+      named_bar_arrive(7, 64);
+      tmem_alloc<kTmemCols>(tmem_base_sh);
+    }
     for (int i = tid - 32; i < 32 * NPAD; i += kNumThreads - 32) m_run[i] = 0.f;  // set exactly on tile 0
     fence_proxy_async_smem();
     tc_fence_before();
-    named_bar_sync(6, kNumThreads);
+    named_bar_sync(6, kNumThreads - 32);
     tc_fence_after();
   }
   const uint32_t tbase = warp == 0 ? 0u : *tmem_base_sh;
@@ -252,6 +256,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // DLS-wide sub-block of a T-token tile; rope_map: 2-D {64 cols, box_rows rows} view.
     // The page ids of the next 32/nbox tiles are fetched by the 32 lanes in one round trip
     // (no dependent block-table load per tile), then lane 0 issues the boxes.
+    if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 0);  // producer start (len known below)
+    if (R == 0) named_bar_sync(7, 64);
     if (R > 0) {
       const uint64_t policy = l2_policy_evict_first();
       const int rope_col = NB * DLAT;
@@ -273,6 +279,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         int rows[T / 64];
 #pragma unroll
         for (int i = 0; i < T / 64; ++i) rows[i] = __shfl_sync(0xffffffffu, my_row, tf * nbox + (i < nbox ? i : 0));
+        if (t == 0) {
+          if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 1);  // page ids of the first tiles in
+          named_bar_sync(7, 64);  // mbarriers initialised by warp 1
+        }
         if (!GQA) {
           const int slot = t % p.rope_slots;
           mbar_wait(&rope_empty[slot], ((t / p.rope_slots) & 1) ^ 1);

@@ -23,6 +23,9 @@ o2 = ops.decode_partials(*args2)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 def med(xs): return int(st.median(xs)) if xs else -1
 ctas = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 8, 40, 77, 100, 135, 143]
+print("prologue (cycles from CTA start): producer start, page ids in, first TMA")
+for cta in ctas[:1]:
+    pass
 print("cta  dur_us  rounds period tma_lat  hold  soft  Pdone->PV  QK->S | start->TMA0 TMA0->data0 data0->Pdone0 lastPV->softdone ->ofinal ->stored ->end (cycles)")
 for cta in ctas:
     os.environ["MLRA_DEBUG_TRACE_CTA"] = str(cta)
@@ -42,7 +45,8 @@ for cta in ctas:
           f"{med([(t[5, r] - t[6, r]).item() for r in rr]):5d} {med([(t[4, r] - t[3, r]).item() for r in rr]):5d} "
           f"{med([(t[2, r] - t[4, r]).item() for r in rr]):10d} {med([(t[3, r] - t[1, r]).item() for r in rr]):6d} | "
           f"{(t[0, 0] - tt[13824 + 2 * cta]).item():10d} {(arr[0] - t[0, 0]).item():11d} {(t[4, 0] - arr[0]).item():13d} "
-          f"{(ep[3] - t[5, n - 1]).item():16d} {(ep[4] - ep[3]).item():7d} {(ep[5] - ep[4]).item():7d} {(tt[13824 + 2 * cta + 1] - ep[5]).item():5d}")
+          f"{(ep[3] - t[5, n - 1]).item():16d} {(ep[4] - ep[3]).item():7d} {(ep[5] - ep[4]).item():7d} {(tt[13824 + 2 * cta + 1] - ep[5]).item():5d}"
+          f" | prod-start {(tt[13056] - tt[13824 + 2 * cta]).item()} pages-in {(tt[13057] - tt[13824 + 2 * cta]).item()}")
 n_cta = int((ce[:, 1] != 0).sum())
 s0 = ce[:n_cta, 0].double(); e0 = ce[:n_cta, 1].double()
 d = ((e0 - s0) / 1e3)
