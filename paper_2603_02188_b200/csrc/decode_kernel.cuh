@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (t == 0) {
           if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 1);  // page ids of the first tiles in
           named_bar_sync(7, 64);  // mbarriers initialised by warp 1
+          if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 2);
         }
         if (!GQA) {
           const int slot = t % p.rope_slots;
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             for (int i = 0; i < nbox; ++i)
               tma_load_2d_hint(&rope_map, &rope_full[slot], rope_ring + slot * L::kRopeBytes + i * box_bytes, rope_col,
                                rows[i], policy);
+            if (t == 0) trace_event(p.trace, p.trace_cta, 11, 3);
           }
         }
         // units of the tile: MLRA/MLA the NB*SUB latent sub-blocks; GQA K_b then V_b per KV head

@@ -46,7 +46,8 @@ for cta in ctas:
           f"{med([(t[2, r] - t[4, r]).item() for r in rr]):10d} {med([(t[3, r] - t[1, r]).item() for r in rr]):6d} | "
           f"{(t[0, 0] - tt[13824 + 2 * cta]).item():10d} {(arr[0] - t[0, 0]).item():11d} {(t[4, 0] - arr[0]).item():13d} "
           f"{(ep[3] - t[5, n - 1]).item():16d} {(ep[4] - ep[3]).item():7d} {(ep[5] - ep[4]).item():7d} {(tt[13824 + 2 * cta + 1] - ep[5]).item():5d}"
-          f" | prod-start {(tt[13056] - tt[13824 + 2 * cta]).item()} pages-in {(tt[13057] - tt[13824 + 2 * cta]).item()}")
+          f" | prod-start {(tt[13056] - tt[13824 + 2 * cta]).item()} pages-in {(tt[13057] - tt[13824 + 2 * cta]).item()}"
+          f" bar7 {(tt[13058] - tt[13824 + 2 * cta]).item()} rope-tma {(tt[13059] - tt[13824 + 2 * cta]).item()}")
 n_cta = int((ce[:, 1] != 0).sum())
 s0 = ce[:n_cta, 0].double(); e0 = ce[:n_cta, 1].double()
 d = ((e0 - s0) / 1e3)
