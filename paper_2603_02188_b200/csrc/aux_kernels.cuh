@@ -384,7 +384,14 @@ absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __
 template <int SEQS, int THREADS = 256>
 inline size_t combine4_smem(int DLAT, int DH, int nsplit) {
   return ((size_t(DLAT) * DH * 2 + 15) / 16) * 16 + size_t(DLAT) * SEQS * 4 + size_t(THREADS / kG4Cols) * SEQS * DH * 4 +
-         16;
+         16 + size_t(SEQS) * kMergeMaxSplits * 4;
+}
+
+// Non-volatile DSMEM load: independent loads after a cluster barrier may be issued together.
+__device__ __forceinline__ float ld_shared_cluster_f32_batched(uint32_t addr) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
 }
 
 constexpr int kMergeChunk = 12;  // split loads in flight per thread (B = 16 -> 9 splits: one pass)
@@ -404,6 +411,7 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   float* zs = reinterpret_cast<float*>(c4_smem + ((wbytes + 15) / 16) * 16);    // [DLAT][SEQS]
   float* ys = zs + DLAT * SEQS;                                                 // [Q][SEQS][DH]
   uint64_t* bar = reinterpret_cast<uint64_t*>(ys + kQ * SEQS * DH);
+  float* wts = reinterpret_cast<float*>(bar + 2);                                // [SEQS][kMergeMaxSplits]
   const int s0 = blockIdx.x * SEQS, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   MLRA_STAMP(0);
   if (tid == 0) {
@@ -420,43 +428,67 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   griddep_wait();  // partials of K2 (a no-op in plain stream order)
   MLRA_STAMP(1);
   const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
-  // merge: thread = (latent column c, sequence); the split weights are computed by every
-  // thread of a sequence redundantly (L2-resident lse loads) -- no extra barrier
-  for (int i = tid; i < DLAT * SEQS; i += THREADS) {
-    const int c = i / SEQS, sq = i % SEQS, s = s0 + sq;
-    float z = 0.f;
-    if (s < B) {
-      const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
+  // merge: thread = (latent column c, sequence), two items at a time with every split load of
+  // both in flight: Z[c] = sum_k w_k O_k[c]. The first pair's partial loads are issued before
+  // the split weights are formed, so the two L2 round trips overlap.
+  auto load_pair = [&](int i0, int k0, float (&v)[2][kMergeChunk]) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * THREADS, c = i / SEQS, sq = i % SEQS, s = s0 + sq;
+      const bool ok = i < DLAT * SEQS && s < B;
       const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
-      float m = -INFINITY, tot = 0.f;
-      for (int k0 = 0; k0 < nsplit; k0 += kMergeChunk) {
-        float lk[kMergeChunk], v[kMergeChunk];
 #pragma unroll
-        for (int j = 0; j < kMergeChunk; ++j) {
-          const int k = min(k0 + j, nsplit - 1);
-          lk[j] = __ldcg(l + size_t(k) * NB * H);
-          v[j] = __ldcg(o + size_t(k) * kstride);
-        }
-        // online rescale across chunks of splits (one chunk for nsplit <= kMergeChunk)
-        float mc = m;
-#pragma unroll
-        for (int j = 0; j < kMergeChunk; ++j) mc = (k0 + j < nsplit) ? fmaxf(mc, lk[j]) : mc;
-        if (mc != -INFINITY) {
-          const float a = (m == -INFINITY) ? 0.f : ex2(m - mc);
-          z *= a;
-          tot *= a;
-#pragma unroll
-          for (int j = 0; j < kMergeChunk; ++j) {
-            const float w = (k0 + j >= nsplit || lk[j] == -INFINITY) ? 0.f : ex2(lk[j] - mc);
-            tot += w;
-            z = fmaf(w, v[j], z);
-          }
-          m = mc;
-        }
-      }
-      z = tot > 0.f ? z / tot : 0.f;
+      for (int j = 0; j < kMergeChunk; ++j) v[u][j] = (ok && k0 + j < nsplit) ? __ldcg(o + size_t(k0 + j) * kstride) : 0.f;
     }
-    zs[i] = z;
+  };
+  float v[2][kMergeChunk];
+  load_pair(tid, 0, v);
+  // split weights w_k = 2^(lse_k - max) / sum_j 2^(lse_j - max), once per sequence: warp sq,
+  // lane k (+32j) -> wts[sq][k] (0 for empty splits / an empty sequence)
+  {
+    const int sq = tid / 32, lane = tid % 32, s = s0 + sq;
+    if (sq < SEQS) {
+      float lk[kMergeMaxSplits / 32];
+      float m = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
+        const int k = lane + 32 * j;
+        lk[j] = (s < B && k < nsplit) ? __ldcg(lse_part + (size_t(s) * nsplit * NB + b) * H + h + size_t(k) * NB * H)
+                                      : -INFINITY;
+        m = fmaxf(m, lk[j]);
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      float tot = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
+        lk[j] = (m == -INFINITY || lk[j] == -INFINITY) ? 0.f : ex2(lk[j] - m);
+        tot += lk[j];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+      const float inv = tot > 0.f ? 1.f / tot : 0.f;
+#pragma unroll
+      for (int j = 0; j < kMergeMaxSplits / 32; ++j)
+        if (lane + 32 * j < nsplit) wts[sq * kMergeMaxSplits + lane + 32 * j] = lk[j] * inv;
+    }
+  }
+  __syncthreads();
+  for (int i0 = tid; i0 < DLAT * SEQS; i0 += 2 * THREADS) {
+    float z[2] = {0.f, 0.f};
+    for (int k0 = 0; k0 < nsplit; k0 += kMergeChunk) {
+      if (i0 != tid || k0 != 0) load_pair(i0, k0, v);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int sq = (i0 + u * THREADS) % SEQS;
+#pragma unroll
+        for (int j = 0; j < kMergeChunk; ++j)
+          if (k0 + j < nsplit) z[u] = fmaf(wts[sq * kMergeMaxSplits + k0 + j], v[u][j], z[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (i0 + u * THREADS < DLAT * SEQS) zs[i0 + u * THREADS] = z[u];
   }
   __syncthreads();
   MLRA_STAMP(2);
@@ -523,8 +555,13 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
       const uint32_t ys_addr = smem_u32(ys);
       for (int i = tid; i < SEQS * DH; i += THREADS) {
         const int s = s0 + i / DH, d = i % DH;
+        float rv[4];
+#pragma unroll
+        for (int r = 1; r < 4; ++r) rv[r] = r < NB ? ld_shared_cluster_f32_batched(mapa_shared(ys_addr + i * 4, r)) : 0.f;
         float tot = ys[i];
-        for (int r = 1; r < NB; ++r) tot += ld_shared_cluster_f32(mapa_shared(ys_addr + i * 4, r));
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+          if (r < NB) tot += rv[r];  // ascending branch order
         if (s < B) out[(size_t(s) * H + h) * DH + d] = tot;
       }
     }
