@@ -419,11 +419,21 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     fence_barrier_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  // DH = 128: the up-projection runs on mma.sync and W^UV_b[h] is staged with cp.async, its
+  // 16-byte units XOR-swizzled by row (conflict-free ldmatrix.trans); otherwise one bulk copy.
+  const bool use_mma = DH == 128 && DLAT % 16 == 0;
+  const uint8_t* w_src = reinterpret_cast<const uint8_t*>(w_uv + (size_t(h) * NB + b) * DLAT * DH);
+  if (use_mma) {
+    const uint32_t wbase = smem_u32(c4_smem);
+    for (int i = tid; i < DLAT * 16; i += THREADS) {
+      const int r = i >> 4, q = i & 15;
+      cp_async16(wbase + r * 256 + ((q ^ (r & 7)) * 16), w_src + size_t(r) * 256 + q * 16, 16u);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else if (tid == 0) {
     mbar_arrive_expect_tx(bar, uint32_t(wbytes));
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(w_uv + (size_t(h) * NB + b) * DLAT * DH);
     for (size_t off = 0; off < wbytes; off += 32768)
-      bulk_copy_g2s(c4_smem + off, src + off, uint32_t(wbytes - off < 32768 ? wbytes - off : 32768), bar);
+      bulk_copy_g2s(c4_smem + off, w_src + off, uint32_t(wbytes - off < 32768 ? wbytes - off : 32768), bar);
   }
   griddep_wait();  // partials of K2 (a no-op in plain stream order)
   MLRA_STAMP(1);
@@ -490,54 +500,91 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     for (int u = 0; u < 2; ++u)
       if (i0 + u * THREADS < DLAT * SEQS) zs[i0 + u * THREADS] = z[u];
   }
+  if (use_mma) cp_async_wait_all();
   __syncthreads();
   MLRA_STAMP(2);
-  mbar_wait(bar, 0);
+  if (!use_mma) mbar_wait(bar, 0);
   MLRA_STAMP(3);
   const bool cluster_sum = NB > 1 && !per_branch;
-  const int cq = tid / kG4Cols;
-  const int q_len = (DLAT + kQ - 1) / kQ, cr0 = cq * q_len, cr1 = min(DLAT, cr0 + q_len);
-  for (int d0 = 0; d0 < DH; d0 += kG4Cols) {
-    const int d = d0 + tid % kG4Cols;
-    float acc[SEQS];
+  if (use_mma) {
+    // y[s][d] = alpha * sum_c Z[s][c] W[c][d]: rows = the SEQS sequences (of 16), warp w owns
+    // columns [16w, 16w+16); Z enters as bf16 hi + lo (two MMAs: ~16-bit mantissa), fp32 sums
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3, q = lane >> 3;
+    const uint32_t wbase = smem_u32(c4_smem);
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int kb = 0; kb < DLAT; kb += 16) {
+      uint32_t ahi[4] = {0u, 0u, 0u, 0u}, alo[4] = {0u, 0u, 0u, 0u};
+      if (g < SEQS) {
 #pragma unroll
-    for (int s = 0; s < SEQS; ++s) acc[s] = 0.f;
-    if (d < DH) {
-      const __nv_bfloat16* wc = wsm + d;
+        for (int hf = 0; hf < 2; ++hf) {
+          const int k = kb + 2 * t4 + 8 * hf;
+          const float z0 = zs[k * SEQS + g], z1 = zs[(k + 1) * SEQS + g];
+          const __nv_bfloat16 h0 = __float2bfloat16_rn(z0), h1 = __float2bfloat16_rn(z1);
+          ahi[2 * hf] = pack_bf16_raw(h0, h1);
+          alo[2 * hf] = pack_bf16(z0 - __bfloat162float(h0), z1 - __bfloat162float(h1));
+        }
+      }
+      uint32_t bfr[4];
+      const int k = kb + (q & 1) * 8 + (lane & 7);
+      ldmatrix_x4_trans(bfr, wbase + k * 256 + (((warp * 2 + (q >> 1)) ^ (k & 7)) * 16));
+      mma_m16n8k16_bf16(acc[0], ahi, bfr[0], bfr[1]);
+      mma_m16n8k16_bf16(acc[0], alo, bfr[0], bfr[1]);
+      mma_m16n8k16_bf16(acc[1], ahi, bfr[2], bfr[3]);
+      mma_m16n8k16_bf16(acc[1], alo, bfr[2], bfr[3]);
+    }
+    if (g < SEQS) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = warp * 16 + j * 8 + 2 * t4;
+        ys[g * DH + col] = acc[j][0] * alpha;
+        ys[g * DH + col + 1] = acc[j][1] * alpha;
+      }
+    }
+  } else {
+    const int cq = tid / kG4Cols;
+    const int q_len = (DLAT + kQ - 1) / kQ, cr0 = cq * q_len, cr1 = min(DLAT, cr0 + q_len);
+    for (int d0 = 0; d0 < DH; d0 += kG4Cols) {
+      const int d = d0 + tid % kG4Cols;
+      float acc[SEQS];
+#pragma unroll
+      for (int s = 0; s < SEQS; ++s) acc[s] = 0.f;
+      if (d < DH) {
+        const __nv_bfloat16* wc = wsm + d;
 #pragma unroll 4
-      for (int c = cr0; c < cr1; ++c) {
-        const float w = __bfloat162float(wc[size_t(c) * DH]);
+        for (int c = cr0; c < cr1; ++c) {
+          const float w = __bfloat162float(wc[size_t(c) * DH]);
 #pragma unroll
-        if constexpr (SEQS == 2) {
-          const float2 z = *reinterpret_cast<const float2*>(zs + c * SEQS);
-          acc[0] = fmaf(z.x, w, acc[0]);
-          acc[1] = fmaf(z.y, w, acc[1]);
-        } else {
+          if constexpr (SEQS == 2) {
+            const float2 z = *reinterpret_cast<const float2*>(zs + c * SEQS);
+            acc[0] = fmaf(z.x, w, acc[0]);
+            acc[1] = fmaf(z.y, w, acc[1]);
+          } else {
 #pragma unroll
-          for (int s4 = 0; s4 < SEQS; s4 += 4) {
-            const float4 z = *reinterpret_cast<const float4*>(zs + c * SEQS + s4);
-            acc[s4 + 0] = fmaf(z.x, w, acc[s4 + 0]);
-            acc[s4 + 1] = fmaf(z.y, w, acc[s4 + 1]);
-            acc[s4 + 2] = fmaf(z.z, w, acc[s4 + 2]);
-            acc[s4 + 3] = fmaf(z.w, w, acc[s4 + 3]);
+            for (int s4 = 0; s4 < SEQS; s4 += 4) {
+              const float4 z = *reinterpret_cast<const float4*>(zs + c * SEQS + s4);
+              acc[s4 + 0] = fmaf(z.x, w, acc[s4 + 0]);
+              acc[s4 + 1] = fmaf(z.y, w, acc[s4 + 1]);
+              acc[s4 + 2] = fmaf(z.z, w, acc[s4 + 2]);
+              acc[s4 + 3] = fmaf(z.w, w, acc[s4 + 3]);
+            }
           }
         }
       }
-    }
-    if (d0 > 0) __syncthreads();
-    if (d < DH) {
+      if (d0 > 0) __syncthreads();
+      if (d < DH) {
 #pragma unroll
-      for (int s = 0; s < SEQS; ++s) ys[(cq * SEQS + s) * DH + d] = acc[s];
+        for (int s = 0; s < SEQS; ++s) ys[(cq * SEQS + s) * DH + d] = acc[s];
+      }
     }
-  }
-  __syncthreads();
-  // quarters -> ys[0] (scaled); thread = (sequence, column)
-  for (int i = tid; i < SEQS * DH; i += THREADS) {
-    float v = ys[i];
+    __syncthreads();
+    // quarters -> ys[0] (scaled); thread = (sequence, column)
+    for (int i = tid; i < SEQS * DH; i += THREADS) {
+      float v = ys[i];
 #pragma unroll
-    for (int q = 1; q < kQ; ++q) v += ys[q * SEQS * DH + i];
-    ys[i] = v * alpha;
-  }
+      for (int q = 1; q < kQ; ++q) v += ys[q * SEQS * DH + i];
+      ys[i] = v * alpha;
+    }
+  }  // FMA up-projection
   MLRA_STAMP(4);
   if (!cluster_sum) {
     __syncthreads();
