@@ -371,6 +371,76 @@ absorb4_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __
   MLRA_STAMP(3);
 }
 
+// K1 on tensor cores (d_h % 16 == 0, d_h <= 256): CTA = (128 output columns, head, 16
+// sequences); the W^UK tile [d_h][128] (cp.async, row-XOR swizzled, issued before
+// griddepcontrol.wait) and the bf16 queries [16][d_h] (exact operands) meet in mma.sync
+// m16n8k16 with fp32 accumulation; warp w owns columns [16w, 16w+16). Grid (ceil(NCOL/128),
+// H, ceil(B/16)): W^UK is read once per 16 sequences.
+constexpr int kAmThreads = 256, kAmMaxDH = 256;
+inline size_t absorb_mma_smem(int DH) { return size_t(DH) * 256 + size_t(16) * (DH + 8) * 2; }
+
+__global__ void __launch_bounds__(kAmThreads)
+absorb_mma_kernel(const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __restrict__ w_uk,
+                  __nv_bfloat16* __restrict__ q_abs, int B, int H, int DH, int NB, int DLAT, float scale,
+                  const __nv_bfloat16* __restrict__ rope_in, __nv_bfloat16* __restrict__ rope_out, int DR) {
+  griddep_launch_dependents();
+  extern __shared__ __align__(128) uint8_t am_smem[];
+  const int NCOL = NB * DLAT, arow = (DH + 8) * 2;
+  const int c0 = blockIdx.x * 128, h = blockIdx.y, m0 = blockIdx.z * 16, tid = threadIdx.x;
+  const uint32_t wbase = smem_u32(am_smem), abase = wbase + uint32_t(DH) * 256;
+  for (int i = tid; i < DH * 16; i += kAmThreads) {  // W^UK[h][k][c0 + 8q ..] -> row k, unit q ^ (k & 7)
+    const int r = i >> 4, q = i & 15;
+    const bool ok = c0 + q * 8 < NCOL;
+    cp_async16(wbase + r * 256 + ((q ^ (r & 7)) * 16),
+               ok ? static_cast<const void*>(w_uk + (size_t(h) * DH + r) * NCOL + c0 + q * 8) : static_cast<const void*>(w_uk),
+               ok ? 16u : 0u);
+  }
+  griddep_wait();  // q_nope comes from the previous kernel on the stream
+  const int units = DH / 8;
+  for (int i = tid; i < 16 * units; i += kAmThreads) {
+    const int r = i / units, q = i % units, m = m0 + r;
+    const bool ok = m < B;
+    cp_async16(abase + r * arow + q * 16,
+               ok ? static_cast<const void*>(q_nope + (size_t(m) * H + h) * DH + q * 8) : static_cast<const void*>(q_nope),
+               ok ? 16u : 0u);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  cp_async_wait_all();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3, q = lane >> 3;
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  for (int kb = 0; kb < DH; kb += 16) {
+    uint32_t a[4], bfr[4];
+    ldmatrix_x4(a, abase + ((lane & 7) + (q & 1) * 8) * arow + (kb + (q >> 1) * 8) * 2);
+    const int k = kb + (q & 1) * 8 + (lane & 7);
+    ldmatrix_x4_trans(bfr, wbase + k * 256 + (((warp * 2 + (q >> 1)) ^ (k & 7)) * 16));
+    mma_m16n8k16_bf16(acc[0], a, bfr[0], bfr[1]);
+    mma_m16n8k16_bf16(acc[1], a, bfr[2], bfr[3]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int col = c0 + warp * 16 + j * 8 + 2 * t4;
+    if (col >= NCOL) continue;
+    const int bb = col / DLAT, cc = col % DLAT;  // DLAT even: the pair stays in one branch
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int m = m0 + g + 8 * hf;
+      if (m < B)
+        *reinterpret_cast<uint32_t*>(q_abs + ((size_t(m) * NB + bb) * H + h) * DLAT + cc) =
+            pack_bf16(acc[j][2 * hf] * scale, acc[j][2 * hf + 1] * scale);
+    }
+  }
+  if (blockIdx.x == 0 && rope_out != nullptr) {
+    for (int i = tid; i < 16 * DR; i += kAmThreads) {
+      const int m = m0 + i / DR;
+      if (m < B) {
+        const size_t off = (size_t(m) * H + h) * DR + i % DR;
+        rope_out[off] = __float2bfloat16(__bfloat162float(rope_in[off]) * scale);
+      }
+    }
+  }
+}
+
 // K3: split merge + W^UV up-projection + ascending branch sum + alpha
 // (attnkit/decode.py:228 per branch, then reduce_contributions :264-285).
 // Grid (ceil(B/SEQS), H, NB), SEQS (4) sequences per CTA; with NB > 1 and a summed output the NB CTAs of a (sequence group, head)

@@ -264,6 +264,23 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
   // CTA = (128 latent columns, head, 4 sequences): W^UK tile staged in smem, one column per thread
   const size_t smem = mlra::absorb4_smem();
   const int NCOL = NB * DLAT;
+  // tensor-core K1 when its grid (128 columns x head x 16 sequences per CTA) has >= 64 CTAs;
+  // below that (one branch per device: TP4 ranks) the 4-sequence FMA kernel spreads wider
+  const long am_ctas = long((NCOL + 127) / 128) * H * ((B + 15) / 16);
+  if (DH % 16 == 0 && DH <= mlra::kAmMaxDH && (reinterpret_cast<uintptr_t>(q_nope) & 15) == 0 && am_ctas >= 64 &&
+      getenv("MLRA_K1_FMA") == nullptr) {
+    const size_t asmem = mlra::absorb_mma_smem(DH);
+    static unsigned am_done = 0;
+    if (int rc = set_smem_once(mlra::absorb_mma_kernel, am_done, int(mlra::absorb_mma_smem(mlra::kAmMaxDH)))) return rc;
+    dim3 agrid((NCOL + 127) / 128, H, (B + 15) / 16);
+    if (launch_ex(mlra::absorb_mma_kernel, agrid, dim3(mlra::kAmThreads), asmem, st, false,
+                  static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(w_uk),
+                  static_cast<__nv_bfloat16*>(q_abs), B, H, DH, NB, DLAT, score_scale,
+                  static_cast<const __nv_bfloat16*>(q_rope), DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr,
+                  DR) != cudaSuccess)
+      return cuda_check("absorb_query launch");
+    return cuda_check("absorb_query launch");
+  }
   dim3 grid((NCOL + mlra::kG4Cols - 1) / mlra::kG4Cols, H, (B + mlra::kG4Seqs - 1) / mlra::kG4Seqs);
   if (launch_ex(mlra::absorb4_kernel, grid, dim3(mlra::kG4Threads), smem, st, false,
                 static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(w_uk),
