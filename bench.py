@@ -537,6 +537,16 @@ def run_ours(args):
     return 0
 
 
+def median_ms(runner, args, reps=3):
+    """Comparison rows: median of three timed loops (the SM clock moves under the power cap)."""
+    import statistics
+
+    import torch
+
+    return statistics.median(time_graph_steps(runner, args.steps, args.warmup, torch.cuda.synchronize)
+                             for _ in range(reps))
+
+
 def per_gpu_comparisons(cfg, device, args):
     """The headline per-GPU numbers on one device: one TP4 rank of MLRA-4 (block + rope) and
     the MLA baseline at the same shapes (TP4 heads-sharded rank: full latent, 6 heads; and TP1)."""
@@ -556,7 +566,7 @@ def per_gpu_comparisons(cfg, device, args):
     res = {}
     for name, (c, own, phi) in cases.items():
         r = StepRunner(c, own, BATCH_PER_GROUP, CTX, device)
-        ms = time_graph_steps(r, args.steps, args.warmup, torch.cuda.synchronize)
+        ms = median_ms(r, args)
         nbytes = algorithmic_bytes(c, phi, [CTX] * BATCH_PER_GROUP)
         res[name] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                      "algorithmic_bytes": nbytes}
@@ -575,7 +585,7 @@ def per_gpu_comparisons(cfg, device, args):
     g_res = {}
     for name, own, phi in (("gqa_tp1", None, 1), ("gqa_tp2_rank", shard_ownership(gqa, 2, 0), 2)):
         r = GqaStepRunner(gqa, own, BATCH_PER_GROUP, CTX, device)
-        ms = time_graph_steps(r, args.steps, args.warmup, torch.cuda.synchronize)
+        ms = median_ms(r, args)
         nbytes = algorithmic_bytes(gqa, phi, [CTX] * BATCH_PER_GROUP)
         g_res[name] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                        "algorithmic_bytes": nbytes}
@@ -586,7 +596,7 @@ def per_gpu_comparisons(cfg, device, args):
     for name, phi in (("mlra2", 4), ("gla2", 2)):
         c = trained_config(name)
         r = StepRunner(c, shard_ownership(c, phi, 0), BATCH_PER_GROUP, CTX, device)
-        ms = time_graph_steps(r, args.steps, args.warmup, torch.cuda.synchronize)
+        ms = median_ms(r, args)
         nbytes = algorithmic_bytes(c, phi, [CTX] * BATCH_PER_GROUP)
         v_res[f"{name}_tp{phi}_rank"] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                                          "algorithmic_bytes": nbytes}
