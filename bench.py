@@ -503,9 +503,9 @@ def run_ours(args):
                          "d2h_bytes_per_step": bout, "ms_per_step": round(e2e_s * 1e3, 4),
                          "serial_ms_per_step": round(ser_s * 1e3, 4),
                          "path": "host_loop.MicroBatchLoop: per step 1 H2D (pinned rows+queries), mlra_cache_append "
-                                 "(advance) + mlra_decode_step (C ABI), 1 D2H; 2 micro-batches, copies on side "
-                                 "streams overlapping the other micro-batch's kernels; serial_ms_per_step = same "
-                                 "calls on one stream, no overlap"
+                                 "(advance) + mlra_decode_step (C ABI), 1 D2H; 2 micro-batches, the copies and K0 on "
+                                 "side streams overlapping the other micro-batch's kernels; serial_ms_per_step = "
+                                 "same calls on one stream, no overlap"
                                  + ("" if world == 1 else "; rank 0 share (no collective)")}
         if n_gpus == 1 and not args.quick:
             extras.update(per_gpu_comparisons(cfg, device, args))

@@ -9,9 +9,10 @@ micro-batch's inputs are uploaded and the previous one's output is downloaded.
 Per step of micro-batch k:
 
 * upload stream: ONE host->device copy of k's pinned staging buffer ``[rows | q_nope | q_rope]``
-  (the new token's cache rows and its queries), after k's previous step has consumed it;
-* compute stream: K0 with ``advance=1`` (writes the token row and bumps ``seqlens``: no separate
-  length update), then K1 -> K2 -> K3 into the engine's output buffer;
+  (the new token's cache rows and its queries), after k's previous step has consumed it, then
+  K0 with ``advance=1`` (writes the token row and bumps ``seqlens``: no separate length
+  update) -- both under the other micro-batch's kernels;
+* compute stream: K1 -> K2 -> K3 into the engine's output buffer;
 * download stream: ONE device->host copy of the fp32 output into k's pinned result buffer.
 
 Host contract: ``wait(k)`` returns when k's last submitted step is fully done; after it,
@@ -89,13 +90,14 @@ class MicroBatchLoop:
         c.reserve_token()
         main = torch.cuda.current_stream(self.device)
         self.up.wait_event(s.step_done)  # k's previous step has read its staging buffer
+        rows, qn, qr = s.views(s.d_in)
         with torch.cuda.stream(self.up):
             s.d_in.copy_(s.h_in, non_blocking=True)
+            # K0 on the upload stream too: it runs under the other micro-batch's kernels
+            ops.cache_append(rows, c.block_table, c.seqlens, c.pool, c.page_size, advance=True)
             s.up_done.record(self.up)
         main.wait_event(s.up_done)
         main.wait_event(s.down_done)  # the output buffer has been drained
-        rows, qn, qr = s.views(s.d_in)
-        ops.cache_append(rows, c.block_table, c.seqlens, c.pool, c.page_size, advance=True)
         out = eng.decode_attention(qn, qr)
         s.step_done.record(main)
         self.down.wait_event(s.step_done)
