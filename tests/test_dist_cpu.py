@@ -99,3 +99,57 @@ def test_group_layout():
     assert group_ranks(8, 4) == [[0, 1, 2, 3], [4, 5, 6, 7]]
     assert group_ranks(4, 4) == [[0, 1, 2, 3]]
     assert group_ranks(2, 1) == [[0], [1]]
+
+
+def _reducer_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+
+        group = dist.new_group([0, 1])
+        red, kind = bench.make_reducer("nccl", group, 8, torch.device("cpu"))
+        res = [(red is None, kind)]
+        # no GPU here: K5's region allocation fails, the bench falls back to the collective
+        red, kind = bench.make_reducer("peer", group, 8, torch.device("cpu"))
+        res.append((red is None, kind))
+        # the TP group's reducer hook replaces its all_reduce
+        calls = []
+
+        def reducer(t):
+            calls.append(t.numel())
+            dist.all_reduce(t, group=group)
+            return t
+
+        cfg = AttnConfig("mla", h=4, d=32, d_h=8, d_h_rope=4, d_c=32, d_cq=16, scaling=True)
+        grp = TPDecodeGroup(cfg, 2, rank, world, group=group, reducer=reducer,
+                            compute=lambda qn, qr: torch.full((1, 2, 8), float(rank + 1), dtype=torch.float64))
+        full = torch.zeros((1, 4, 8), dtype=torch.float64)
+        grp.step(None, None, full)
+        res.append((calls, full[0, :, 0].tolist()))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_reducer_fallback_and_tp_group_hook():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reducer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in range(world):
+        (none_nccl, kind_nccl), (none_peer, kind_peer), (calls, col) = results[rank]
+        assert none_nccl and kind_nccl == "nccl all_reduce"
+        assert none_peer and kind_peer.startswith("nccl all_reduce (K5 unavailable")
+        assert calls == [32]
+        assert col == [1.0, 1.0, 2.0, 2.0]  # MLA: rank r owns heads 2r, 2r+1
