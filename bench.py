@@ -510,7 +510,7 @@ def run_ours(args):
         if n_gpus == 1 and not args.quick:
             extras.update(per_gpu_comparisons(cfg, device, args))
         if n_gpus == 1 and not args.no_cpu:
-            nseq = BATCH_PER_GROUP * 8  # the B=16 batch eight times over: ~10 s of host work
+            nseq = BATCH_PER_GROUP * 16  # the B=16 batch sixteen times over: ~10 s of host work
             gbs_cpu, dt = cpu_oracle_sample(1, CTX, nseq)
             extras["cpu_baseline"] = {"value": round(gbs_cpu, 3), "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
                                       "sample": f"{nseq} sequences x {CTX} tokens of the TP1 workload (numpy float64 "
