@@ -183,6 +183,9 @@ class StepRunner:
         torch.cuda.synchronize()
 
     def _step(self, eng, qn, qr):
+        if self.reducer is not None and len(self.heads) == self.cfg.h:
+            # every rank holds every head (MLRA-4 by latent block): the TP sum runs inside K3
+            return eng.decode_attention_tp(qn, qr, self.reducer, out=self.full)
         out = eng.decode_attention(qn, qr)
         if self.tp_group is not None:
             import torch.distributed as dist
@@ -527,7 +530,7 @@ def run_ours(args):
                        "graphs": "10 alternating steps per CUDA graph replay", "allreduce": allreduce_kind,
                        "algorithmic_bytes_per_gpu_per_step": bytes_rank, "page_size": 128,
                        "nsplit": runner.engines[0][0].nsplit},
-            "gpu_launches": (3 + (1 if reducer is not None else 0)) * args.steps,
+            "gpu_launches": (3 + (1 if reducer is not None and len(runner.heads) != cfg.h else 0)) * args.steps,
         }
         line.update(extras)
         print(json.dumps(line))
@@ -720,7 +723,8 @@ def make_reducer(kind, group, n, device):
         ok = torch.tensor([float(torch.allclose(a, b, rtol=1e-5, atol=1e-5))], device=device)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
         if ok.item() == 1.0:
-            return red, "peer (K5 mlra_allreduce: one-shot over NVLink IPC mappings, rank-order sum)"
+            return red, ("peer (one-shot over NVLink IPC mappings, rank-order sum: fused into K3 via "
+                         "mlra_decode_step_tp when every rank holds every head, else K5 mlra_allreduce)")
         red.close()
         return None, "nccl all_reduce (K5 self-check mismatch)"
     except Exception as e:  # IPC / peer access unavailable

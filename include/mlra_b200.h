@@ -197,6 +197,19 @@ int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, con
  * CUDA graph and replayed. All ranks must make the same sequence of calls.
  */
 size_t mlra_allreduce_comm_bytes(int n, int world);
+/*
+ * mlra_decode_step with the TP sum over ranks fused into K3's epilogue (K3 + K5 in one kernel):
+ * out [B, H, DH] = sum over the `world` ranks of each rank's alpha-scaled step output, in
+ * ascending rank order (bit-identical on every rank). For owners that hold every head (MLRA-4
+ * / MLRA-2 sharded by latent block). comm = the ranks' mlra_allreduce regions (n = B*H*DH).
+ * When the chosen K3 variant cannot fuse (split-K merge for many splits, a grid that cannot be
+ * resident), K5 runs after it on the same region.
+ */
+int mlra_decode_step_tp(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
+                        const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
+                        int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
+                        int nsplit, float score_scale, float alpha, int rank, int world, void* const* comm,
+                        void* stream);
 int mlra_allreduce(const float* x, float* y, int n, int rank, int world, void* const* comm, void* stream);
 int mlra_allreduce_sim(const float* const* x, float* const* y, int n, int world, void* const* comm, void* stream);
 

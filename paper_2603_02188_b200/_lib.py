@@ -44,6 +44,7 @@ SIGNATURES = {
     "mlra_outproj": (_I, [_P] * 5 + [_I] * 5 + [_P, _P, _P]),
     "mlra_outproj_sim": (_I, [_P] * 5 + [_I] * 4 + [_P, _P, _P]),
     "mlra_allreduce_comm_bytes": (ctypes.c_size_t, [_I, _I]),
+    "mlra_decode_step_tp": (_I, [_P] * 9 + [_I] * 11 + [_F, _F, _I, _I, _P, _P]),
     "mlra_allreduce": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "mlra_allreduce_sim": (_I, [_P, _P, _I, _I, _P, _P]),
     "mlra_comm_alloc": (_I, [ctypes.c_size_t, _P]),

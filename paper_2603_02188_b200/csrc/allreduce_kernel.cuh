@@ -14,7 +14,7 @@
 // pushed call e+1, i.e. after the peer finished reading call e).
 //
 // Region of a rank (mlra_allreduce_comm_bytes): fp32 recv [2][world][n rounded to 4], uint32 flags
-// [2][world][nchunks], uint32 {epoch counter, done counter}; zero-filled once.
+// [2][world][kArFlagSlots], uint32 {epoch counter, done counter}; zero-filled once.
 #pragma once
 #include <cstdint>
 #include "ptx.cuh"
@@ -22,6 +22,9 @@
 namespace mlra {
 
 constexpr int kArThreads = 256, kArChunk = kArThreads * 4, kArMaxRanks = 8;
+// Flag slots per (parity, source rank): shared layout with K3's fused TP sum (one region, one
+// epoch counter for both), so up to kArFlagSlots chunks / K3 CTAs.
+constexpr int kArFlagSlots = 4096;
 
 struct AllReduceParams {
   const float* x[kArMaxRanks];  // per local rank [n]
@@ -33,7 +36,16 @@ struct AllReduceParams {
 // per-rank slot stride: n rounded up to whole float4s
 __host__ __device__ inline size_t ar_stride(int n) { return (size_t(n) + 3) / 4 * 4; }
 __host__ __device__ inline size_t ar_recv_floats(int n, int world) { return size_t(2) * world * ar_stride(n); }
-__host__ __device__ inline size_t ar_flag_words(int nchunks, int world) { return size_t(2) * world * nchunks; }
+__host__ __device__ inline size_t ar_flag_words(int world) { return size_t(2) * world * kArFlagSlots; }
+__host__ __device__ inline size_t ar_region_bytes(int n, int world) {
+  return ar_recv_floats(n, world) * 4 + ar_flag_words(world) * 4 + 16;
+}
+
+// A rank's view of the TP group for a fused sum (K3 epilogue): world <= 1 means off.
+struct TpSum {
+  float* comm[kArMaxRanks];  // region of every GLOBAL rank, as mapped here
+  int world, rank;
+};
 
 __device__ __forceinline__ void ar_st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -55,7 +67,7 @@ __global__ void __launch_bounds__(kArThreads) allreduce_kernel(const __grid_cons
   const size_t ns = ar_stride(n);
   float* own = p.comm[rank];
   uint32_t* own_flags = reinterpret_cast<uint32_t*>(own + ar_recv_floats(n, W));
-  uint32_t* ctr = own_flags + ar_flag_words(p.nchunks, W);  // [0] epoch, [1] done CTAs
+  uint32_t* ctr = own_flags + ar_flag_words(W);  // [0] epoch, [1] done CTAs
   __shared__ uint32_t s_epoch;
   if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(ctr) + 1u;
   __syncthreads();
@@ -84,8 +96,8 @@ __global__ void __launch_bounds__(kArThreads) allreduce_kernel(const __grid_cons
   if (tid < W) {
     __threadfence_system();
     uint32_t* flags = reinterpret_cast<uint32_t*>(p.comm[tid] + ar_recv_floats(n, W));
-    ar_st_release_sys(flags + (size_t(par) * W + rank) * p.nchunks + c, epoch);
-    const uint32_t* f = own_flags + (size_t(par) * W + tid) * p.nchunks + c;
+    ar_st_release_sys(flags + (size_t(par) * W + rank) * kArFlagSlots + c, epoch);
+    const uint32_t* f = own_flags + (size_t(par) * W + tid) * kArFlagSlots + c;
     const unsigned long long t0 = ar_globaltimer();
     while (ar_ld_acquire_sys(f) != epoch) {
       if (ar_globaltimer() - t0 > 4000000000ull) __trap();

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cmath>
 #include "ptx.cuh"
+#include "allreduce_kernel.cuh"
 
 namespace mlra {
 
@@ -472,7 +473,7 @@ template <int SEQS, int THREADS = 256>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
-                int nsplit, float alpha, int per_branch) {
+                int nsplit, float alpha, int per_branch, const TpSum tp) {
   static_assert(SEQS == 2 || SEQS == 4 || SEQS == 8, "2, 4 or 8 sequences per CTA");
   constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
@@ -484,9 +485,16 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   float* wts = reinterpret_cast<float*>(bar + 2);                                // [SEQS][kMergeMaxSplits]
   const int s0 = blockIdx.x * SEQS, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   MLRA_STAMP(0);
+  // fused TP sum (tp.world > 1, summed output): this call's epoch from the rank's region
+  uint32_t& s_tp_epoch = *reinterpret_cast<uint32_t*>(bar + 1);  // (dynamic smem: no static carve-out)
+  const size_t tp_n = size_t(B) * H * DH, tp_ns = ar_stride(int(tp_n));
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
+    if (tp.world > 1)
+      s_tp_epoch = *reinterpret_cast<volatile uint32_t*>(
+                       reinterpret_cast<uint32_t*>(tp.comm[tp.rank] + ar_recv_floats(int(tp_n), tp.world)) +
+                       ar_flag_words(tp.world)) + 1u;
   }
   __syncthreads();
   // DH = 128: the up-projection runs on mma.sync and W^UV_b[h] is staged with cp.async, its
@@ -656,13 +664,16 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     }
   }  // FMA up-projection
   MLRA_STAMP(4);
+  const bool tp_sum = tp.world > 1 && !per_branch;
   if (!cluster_sum) {
     __syncthreads();
-    for (int i = tid; i < SEQS * DH; i += THREADS) {
-      const int s = s0 + i / DH, d = i % DH;
-      if (s >= B) continue;
-      if (per_branch) out[((size_t(s) * NB + b) * H + h) * DH + d] = ys[i];
-      else out[(size_t(s) * H + h) * DH + d] = ys[i];
+    if (!tp_sum) {
+      for (int i = tid; i < SEQS * DH; i += THREADS) {
+        const int s = s0 + i / DH, d = i % DH;
+        if (s >= B) continue;
+        if (per_branch) out[((size_t(s) * NB + b) * H + h) * DH + d] = ys[i];
+        else out[(size_t(s) * H + h) * DH + d] = ys[i];
+      }
     }
   } else {
     // branch sum over the cluster (ranks = branches along z), ascending order
@@ -679,12 +690,60 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
 #pragma unroll
         for (int r = 1; r < 4; ++r)
           if (r < NB) tot += rv[r];  // ascending branch order
-        if (s < B) out[(size_t(s) * H + h) * DH + d] = tot;
+        if (tp_sum) ys[i] = tot;  // own slot i only: the peers read their own smem, not ours
+        else if (s < B) out[(size_t(s) * H + h) * DH + d] = tot;
       }
     }
     // keep every rank's smem alive until rank 0 has read it
     cluster_arrive_release();
     cluster_wait_acquire();
+  }
+  if (tp_sum && b == 0) {
+    // one-shot sum over the TP ranks (the K5 protocol, fused): store this CTA's [SEQS][DH] tile
+    // into slot [parity][my rank] of every rank, release the epoch into that rank's flag for
+    // this CTA, wait for the world flags of this CTA in my region, add in ascending rank order
+    const int W = tp.world, par = int(s_tp_epoch & 1u);
+    const uint32_t epoch = s_tp_epoch;
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x, nct = gridDim.x * gridDim.y;
+    __syncthreads();
+    for (int r = 0; r < W; ++r) {
+      float* dst = tp.comm[r] + (size_t(par) * W + tp.rank) * tp_ns;
+      for (int i = tid; i < SEQS * DH; i += THREADS) {
+        const int s = s0 + i / DH;
+        if (s < B) dst[(size_t(s) * H + h) * DH + i % DH] = ys[i];
+      }
+    }
+    __syncthreads();
+    if (tid < W) {
+      __threadfence_system();
+      uint32_t* flags = reinterpret_cast<uint32_t*>(tp.comm[tid] + ar_recv_floats(int(tp_n), W));
+      ar_st_release_sys(flags + (size_t(par) * W + tp.rank) * kArFlagSlots + cta, epoch);
+      const uint32_t* f = reinterpret_cast<const uint32_t*>(tp.comm[tp.rank] + ar_recv_floats(int(tp_n), W)) +
+                          (size_t(par) * W + tid) * kArFlagSlots + cta;
+      const unsigned long long t0 = ar_globaltimer();
+      while (ar_ld_acquire_sys(f) != epoch) {
+        if (ar_globaltimer() - t0 > 4000000000ull) __trap();
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    const float* recv = tp.comm[tp.rank] + size_t(par) * W * tp_ns;
+    for (int i = tid; i < SEQS * DH; i += THREADS) {
+      const int s = s0 + i / DH;
+      if (s >= B) continue;
+      const size_t o = (size_t(s) * H + h) * DH + i % DH;
+      float sum = 0.f;
+      for (int r = 0; r < W; ++r) sum += __ldcv(recv + size_t(r) * tp_ns + o);
+      out[o] = sum;
+    }
+    if (tid == 0) {  // advance the rank's epoch once every CTA of the call has read it
+      uint32_t* ctr = reinterpret_cast<uint32_t*>(tp.comm[tp.rank] + ar_recv_floats(int(tp_n), W)) + ar_flag_words(W);
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1u) == uint32_t(nct) - 1u) {
+        ctr[1] = 0u;
+        atomicExch(ctr, epoch);
+      }
+    }
   }
   MLRA_STAMP(5);
 }

@@ -463,9 +463,36 @@ static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block
 // K3 needs a [B, H, NB*DLAT] fp32 scratch for the merged latent when it up-projects; the
 // standalone entry point allocates it from a per-thread cache (mlra_decode_step passes the
 // workspace slice instead).
+static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cudaStream_t st);
+static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
+                           int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
+                           bool pdl, const mlra::TpSum* tp);
+
+// After a K3 variant without the fused TP sum: K5 on the output, in place, same region.
+static int tp_sum_after(const mlra::TpSum* tp, float* out, int n, cudaStream_t st) {
+  if (tp == nullptr || tp->world <= 1) return MLRA_OK;
+  mlra::AllReduceParams p = {};
+  p.x[0] = out;
+  p.y[0] = out;
+  for (int r = 0; r < tp->world; ++r) p.comm[r] = tp->comm[r];
+  p.n = n, p.world = tp->world, p.rank0 = tp->rank;
+  return allreduce_launch(p, 1, false, st);
+}
+
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
                         int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                        bool pdl = false) {
+                        bool pdl = false, const mlra::TpSum* tp = nullptr) {
+  if (int rc = combine_variant(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, upproj, st, pdl, tp))
+    return rc == 1 ? tp_sum_after(tp, out, B * H * DH, st) : rc;
+  return MLRA_OK;
+}
+
+// Returns MLRA_OK when the output is complete (TP sum fused in K3 when requested), 1 when a
+// requested TP sum still has to run (the K3 variant has no fused sum), < 0 on error.
+static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
+                           int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
+                           bool pdl, const mlra::TpSum* tp) {
+  const int tp_pending = (tp != nullptr && tp->world > 1 && upproj == 1) ? 1 : 0;
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
   // summed output: split-K merge over a cluster of KP CTAs (KP = 8 once the splits are many)
@@ -499,7 +526,8 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
                            DH, nsplit, alpha) != cudaSuccess)
       return cuda_check("combine launch");
-    return cuda_check("combine launch");
+    if (int rc = cuda_check("combine launch")) return rc;
+    return tp_pending;
   }
   // 2 sequences per CTA (one merge item per thread) while the grid stays within one wave
   // (4 CTAs per SM), else 4
@@ -535,10 +563,23 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
     attr[1].val.clusterDim.z = (NB > 1 && !per_branch) ? NB : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
+    // TP sum fused into the epilogue when every CTA of the grid is resident (flag waits)
+    mlra::TpSum tps = {};
+    int fused = 0;
+    if (tp_pending) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, c4smem);
+      if (long(cfg.gridDim.x) * cfg.gridDim.y * cfg.gridDim.z <= long(sms) * per_sm &&
+          long(cfg.gridDim.x) * cfg.gridDim.y <= mlra::kArFlagSlots) {
+        tps = *tp;
+        fused = 1;
+      }
+    }
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha, per_branch) != cudaSuccess)
+                           DH, nsplit, alpha, per_branch, tps) != cudaSuccess)
       return cuda_check("combine launch");
-    return cuda_check("combine launch");
+    if (int rc = cuda_check("combine launch")) return rc;
+    return fused ? MLRA_OK : tp_pending;
   }
   if (upproj == 0) {
     mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
@@ -563,7 +604,8 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
   dim3 grid((DH + NT - 1) / NT, H, ((B + mlra::kHG_S - 1) / mlra::kHG_S) * kparts);
   kern<<<grid, mlra::kHG_THREADS, smem, st>>>(zbuf, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
                                               DH, kparts, alpha, 0, 0, nullptr, nullptr, 0);
-  return cuda_check("up-projection launch");
+  if (int rc = cuda_check("up-projection launch")) return rc;
+  return tp_pending;
 }
 
 int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
@@ -577,10 +619,43 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
                       static_cast<cudaStream_t>(stream));
 }
 
+static int decode_step_impl(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,
+                            const void* pool, const int32_t* block_table, const int32_t* seqlens, float* out,
+                            void* workspace, int B, int H, int DH, int NB, int SUB, int DLS, int DR, int page_size,
+                            int max_pages, int num_pages, int nsplit, float score_scale, float alpha, void* stream,
+                            const mlra::TpSum* tp);
+
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
                      const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
                      int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
                      int nsplit, float score_scale, float alpha, void* stream) {
+  return decode_step_impl(q_nope, q_rope, w_uk, w_uv, pool, block_table, seqlens, out, workspace, B, H, DH, NB, SUB,
+                          DLS, DR, page_size, max_pages, num_pages, nsplit, score_scale, alpha, stream, nullptr);
+}
+
+int mlra_decode_step_tp(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
+                        const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
+                        int DH, int NB, int SUB, int DLS, int DR, int page_size, int max_pages, int num_pages,
+                        int nsplit, float score_scale, float alpha, int rank, int world, void* const* comm,
+                        void* stream) {
+  if (world < 1 || world > mlra::kArMaxRanks || rank < 0 || rank >= world)
+    return fail(MLRA_ERR_CONFIG, "decode_step_tp: rank %d of %d", rank, world);
+  if (world > 1 && comm == nullptr) return fail(MLRA_ERR_CONFIG, "decode_step_tp: no communication regions");
+  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return fail(MLRA_ERR_CONFIG, "decode_step_tp: out not 16-byte aligned");
+  mlra::TpSum tp = {};
+  tp.world = world;
+  tp.rank = rank;
+  for (int r = 0; r < world && world > 1; ++r) tp.comm[r] = static_cast<float*>(comm[r]);
+  return decode_step_impl(q_nope, q_rope, w_uk, w_uv, pool, block_table, seqlens, out, workspace, B, H, DH, NB, SUB,
+                          DLS, DR, page_size, max_pages, num_pages, nsplit, score_scale, alpha, stream,
+                          world > 1 ? &tp : nullptr);
+}
+
+static int decode_step_impl(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,
+                            const void* pool, const int32_t* block_table, const int32_t* seqlens, float* out,
+                            void* workspace, int B, int H, int DH, int NB, int SUB, int DLS, int DR, int page_size,
+                            int max_pages, int num_pages, int nsplit, float score_scale, float alpha, void* stream,
+                            const mlra::TpSum* tp) {
   if (B <= 0) return MLRA_OK;
   const int DLAT = SUB * DLS;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -605,7 +680,7 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
                    max_pages, num_pages, nsplit, stream, pdl);
   if (rc) return rc;
   return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
-                      static_cast<cudaStream_t>(stream), false);
+                      static_cast<cudaStream_t>(stream), false, tp);
 }
 
 int mlra_gqa_default_splits(int B, int G, int max_seqlen) {
@@ -774,8 +849,7 @@ int mlra_outproj_sim(const float* const* attn, const float* const* gate_pre, con
 // ----------------------------------------------------------------------------- K5 (peer all-reduce)
 size_t mlra_allreduce_comm_bytes(int n, int world) {
   if (n <= 0 || world <= 0) return 0;
-  const int nchunks = (n + mlra::kArChunk - 1) / mlra::kArChunk;
-  return mlra::ar_recv_floats(n, world) * 4 + mlra::ar_flag_words(nchunks, world) * 4 + 16;
+  return mlra::ar_region_bytes(n, world);
 }
 
 static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cudaStream_t st) {
@@ -783,6 +857,7 @@ static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cuda
   if (p.world < 1 || p.world > mlra::kArMaxRanks)
     return fail(MLRA_ERR_CONFIG, "allreduce: world %d outside [1, %d]", p.world, mlra::kArMaxRanks);
   p.nchunks = (p.n + mlra::kArChunk - 1) / mlra::kArChunk;
+  if (p.nchunks > mlra::kArFlagSlots) return fail(MLRA_ERR_SHAPE, "allreduce: %d values exceed %d chunks", p.n, mlra::kArFlagSlots);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

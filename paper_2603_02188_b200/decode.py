@@ -505,6 +505,18 @@ class DecodeEngine:
         qr[..., :self.layout.dr] = qr_src.to(torch.bfloat16)
         return qn, qr
 
+    def decode_attention_tp(self, q_nope: torch.Tensor, q_rope: torch.Tensor, reducer, out: torch.Tensor | None = None):
+        """decode_attention plus the sum over the TP group fused into K3 (every local head must be
+        a global head: owners holding all heads, MLRA-4 / MLRA-2 by latent block). reducer:
+        collective.PeerAllReduce sized B*h*d_h (its regions and epoch are shared with K5)."""
+        if len(self.heads) != self.cfg.h:
+            raise RoutingError("fused TP sum needs owners holding every head; use K5 after the step")
+        c = self.cache
+        return ops.decode_step_tp(q_nope, q_rope, self.w_uk, self.w_uv, c.pool, c.block_table, c.seqlens,
+                                  c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
+                                  self.workspace, reducer.rank, reducer.world, reducer.ptrs,
+                                  out=self.out if out is None else out)
+
     def decode_attention(self, q_nope: torch.Tensor, q_rope: torch.Tensor, out: torch.Tensor | None = None):
         """One decode-attention step over the cache: bf16 [B, h_local, d_h] / [B, h_local, drp]
         queries on this device -> fp32 [B, h_local, d_h] (alpha-scaled, branch-summed)."""

@@ -191,6 +191,29 @@ def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seq
     return out
 
 
+def decode_step_tp(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
+                   sub: int, dls: int, nsplit: int, score_scale: float, alpha: float, workspace: DecodeWorkspace,
+                   rank: int, world: int, comm_ptrs, out: torch.Tensor | None = None) -> torch.Tensor:
+    """decode_step with the sum over the TP ranks fused into K3 (mlra_decode_step_tp): every rank
+    gets the device-order sum of all ranks' outputs. comm_ptrs: the ranks' allreduce regions
+    (collective.PeerAllReduce(group, B*H*DH).ptrs)."""
+    B, H, DH = q_nope.shape
+    DR = q_rope.shape[2]
+    dlat = sub * dls
+    if workspace.key != (B, H, nb, dlat, DR, nsplit):
+        raise ConfigError(f"workspace sized for {workspace.key}, call needs {(B, H, nb, dlat, DR, nsplit)}")
+    if out is None:
+        out = torch.empty((B, H, DH), dtype=torch.float32, device=q_nope.device)
+    rc = _lib.load().mlra_decode_step_tp(q_nope.data_ptr(), q_rope.data_ptr(), w_uk_packed.data_ptr(),
+                                         w_uv_packed.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
+                                         seqlens.data_ptr(), out.data_ptr(), workspace.buf.data_ptr(), B, H, DH, nb,
+                                         sub, dls, DR, page_size, block_table.shape[1], pool.shape[0] // page_size,
+                                         nsplit, float(score_scale), float(alpha), rank, world,
+                                         _ptr_array(comm_ptrs) if world > 1 else None, _stream())
+    _lib.check(rc, "mlra_decode_step_tp")
+    return out
+
+
 # ----------------------------------------------------------------------------- GQA variant
 def gqa_default_splits(batch: int, kv_heads: int, max_seqlen: int) -> int:
     return _lib.load().mlra_gqa_default_splits(batch, kv_heads, max_seqlen)

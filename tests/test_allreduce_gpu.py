@@ -183,3 +183,68 @@ def test_tp_decode_group_with_peer_reducer(tmp_path):
                 full[:, r * 12:(r + 1) * 12] = loc
             parts.append(full)
         np.testing.assert_array_equal(r0, _fold(parts))
+
+
+_STEP_WORKER = r'''
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["REPO"])
+sys.path.insert(0, os.path.join(os.environ["REPO"], "tests"))
+import paper_2603_02188_b200 as mlra
+from paper_2603_02188_b200.collective import PeerAllReduce
+from paper_2603_02188_b200.tp import shard_ownership
+import bench
+rank = int(sys.argv[1]); world = int(sys.argv[3])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + sys.argv[2], rank=rank, world_size=world)
+dev = torch.device("cuda", 0)
+torch.cuda.set_device(dev)
+cfg = mlra.trained_config("mlra4")
+own = shard_ownership(cfg, world, rank)
+outs = {}
+for B, ctx in ((16, 2048), (3, 700), (1, 20000)):   # combine4 (fused) and split-K (K5 after) variants
+    eng, qn, qr = bench.make_engine(cfg, own, B, ctx, 1000, dev)
+    red = PeerAllReduce(None, B * cfg.h * cfg.d_h, dev)
+    local = eng.decode_attention(qn, qr).clone()
+    fused = [eng.decode_attention_tp(qn, qr, red).clone() for _ in range(3)]
+    torch.cuda.synchronize()
+    outs[f"local_{B}"] = local.cpu().numpy()
+    for i, f in enumerate(fused):
+        outs[f"fused_{B}_{i}"] = f.cpu().numpy()
+    dist.barrier()
+    red.close()
+np.savez(os.path.join(os.environ["OUTDIR"], f"step{rank}.npz"), **outs)
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_decode_step_with_fused_tp_sum(tmp_path, world):
+    """mlra_decode_step_tp in `world` processes on the one GPU (MLRA-4 sharded by latent block,
+    every rank holds every head): each rank's fused result equals the float32 rank-order sum of
+    the ranks' plain decode outputs, bit-identical across ranks and repeated calls; B = 16 uses
+    the fused K3 epilogue, B = 1 long context the split-K K3 followed by K5."""
+    import socket
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "step_worker.py"
+    script.write_text(_STEP_WORKER)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = str(s.getsockname()[1])
+    env = dict(os.environ, REPO=repo, OUTDIR=str(tmp_path))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), port, str(world)], env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT) for r in range(world)]
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=300)[0].decode(errors="replace"))
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            pytest.fail("step worker timed out")
+    assert all(p.returncode == 0 for p in procs), "\n".join(outs)
+    res = [dict(np.load(tmp_path / f"step{r}.npz")) for r in range(world)]
+    for B in (16, 3, 1):
+        want = _fold([res[r][f"local_{B}"] for r in range(world)])
+        for r in range(world):
+            for i in range(3):
+                np.testing.assert_array_equal(res[r][f"fused_{B}_{i}"], want)

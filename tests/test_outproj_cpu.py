@@ -73,7 +73,7 @@ def test_allreduce_c_abi_validation():
 
     lib = _lib.load()
     n, world = 49152, 4
-    assert lib.mlra_allreduce_comm_bytes(n, world) == 2 * world * n * 4 + 2 * world * 48 * 4 + 16
+    assert lib.mlra_allreduce_comm_bytes(n, world) == 2 * world * n * 4 + 2 * world * 4096 * 4 + 16
     assert lib.mlra_allreduce(None, None, n, 0, 2, None, None) == -2
     assert lib.mlra_allreduce(None, None, n, 2, 2, None, None) == -2
     assert lib.mlra_allreduce_sim(None, None, n, 9, None, None) == -2

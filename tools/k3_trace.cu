@@ -25,9 +25,9 @@ int main() {
   attr[0].id = cudaLaunchAttributeClusterDimension; attr[0].val.clusterDim.x = 1; attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = NB; cfg.attrs = attr; cfg.numAttrs = 1;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int i = 0; i < 5; ++i) cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0);
+  for (int i = 0; i < 5; ++i) cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{});
   cudaEventRecord(e0);
-  cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0);
+  cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{});
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   const int n = ((B + 3) / 4) * H * NB;

@@ -83,7 +83,7 @@ int main() {
           cfg.attrs = attr;
           cfg.numAttrs = 1;
           cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB,
-                             DLAT, DH, nsplit, 0.5f, cl ? 0 : 1);
+                             DLAT, DH, nsplit, 0.5f, cl ? 0 : 1, TpSum{});
         });
       }
     }
