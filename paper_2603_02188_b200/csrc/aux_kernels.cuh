@@ -847,12 +847,16 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
     const uint32_t pz_a = smem_u32(pz), pml_a = smem_u32(pml);
     for (int it = tid; it < 4 * rows; it += kSkThreads) {
       const int q = it / rows, r = it % rows, b = r / DLAT;
+      if (s0 + q >= B) {  // padding sequence of the group: nothing to combine
+        reinterpret_cast<float*>(zf)[r * 4 + q] = 0.f;
+        continue;
+      }
       float mk[KP], lk[KP], zk[KP];
 #pragma unroll
-      for (int j = 0; j < KP; ++j) {
-        mk[j] = ld_shared_cluster_f32(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2) * 4), j));
-        lk[j] = ld_shared_cluster_f32(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2 + 1) * 4), j));
-        zk[j] = ld_shared_cluster_f32(mapa_shared(pz_a + uint32_t((q * rows + r) * 4), j));
+      for (int j = 0; j < KP; ++j) {  // all 3*KP remote loads in flight together
+        mk[j] = ld_shared_cluster_f32_batched(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2) * 4), j));
+        lk[j] = ld_shared_cluster_f32_batched(mapa_shared(pml_a + uint32_t(((q * NB + b) * 2 + 1) * 4), j));
+        zk[j] = ld_shared_cluster_f32_batched(mapa_shared(pz_a + uint32_t((q * rows + r) * 4), j));
       }
       float M = -INFINITY;
 #pragma unroll
