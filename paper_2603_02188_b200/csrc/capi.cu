@@ -538,17 +538,21 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const bool seq2 = long((B + 1) / 2) * H * NB <= 4L * sms && getenv("MLRA_K3_SEQ4") == nullptr;
-  const size_t c4smem = seq2 ? mlra::combine4_smem<2>(DLAT, DH, nsplit) : mlra::combine4_smem<4>(DLAT, DH, nsplit);
+  // many sequences (prefill's pseudo-sequences): 8 per CTA halves the W^UV re-reads
+  const bool seq8 = !seq2 && B >= 256;
+  const size_t c4smem = seq2   ? mlra::combine4_smem<2>(DLAT, DH, nsplit)
+                        : seq8 ? mlra::combine4_smem<8>(DLAT, DH, nsplit)
+                               : mlra::combine4_smem<4>(DLAT, DH, nsplit);
   if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
     // CTA = (2 or 4 sequences, head, branch); with a summed output the NB branch CTAs of a
     // (sequence group, head) form a cluster and add their results through DSMEM.
     // (8 sequences per CTA measured slower even where 4 needs 1.3 waves.)
-    auto kern = seq2 ? mlra::combine4_kernel<2> : mlra::combine4_kernel<4>;
-    static unsigned attr_done2 = 0, attr_done4 = 0;
-    if (int rc = set_smem_once(kern, seq2 ? attr_done2 : attr_done4, kSmemBudget)) return rc;
+    auto kern = seq2 ? mlra::combine4_kernel<2> : seq8 ? mlra::combine4_kernel<8> : mlra::combine4_kernel<4>;
+    static unsigned attr_done2 = 0, attr_done4 = 0, attr_done8 = 0;
+    if (int rc = set_smem_once(kern, seq2 ? attr_done2 : seq8 ? attr_done8 : attr_done4, kSmemBudget)) return rc;
     const int per_branch = upproj == 2 ? 1 : 0;
-    const int seqs = seq2 ? 2 : 4;
+    const int seqs = seq2 ? 2 : seq8 ? 8 : 4;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((B + seqs - 1) / seqs, H, NB);
     cfg.blockDim = dim3(256);
