@@ -267,8 +267,8 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
   // tensor-core K1 when its grid (128 columns x head x 16 sequences per CTA) has >= 64 CTAs;
   // below that (one branch per device: TP4 ranks) the 4-sequence FMA kernel spreads wider
   const long am_ctas = long((NCOL + 127) / 128) * H * ((B + 15) / 16);
-  if (DH % 16 == 0 && DH <= mlra::kAmMaxDH && (reinterpret_cast<uintptr_t>(q_nope) & 15) == 0 && am_ctas >= 64 &&
-      getenv("MLRA_K1_FMA") == nullptr) {
+  if (DH % 16 == 0 && DH <= mlra::kAmMaxDH && (reinterpret_cast<uintptr_t>(q_nope) & 15) == 0 &&
+      (am_ctas >= 64 || getenv("MLRA_K1_MMA") != nullptr) && getenv("MLRA_K1_FMA") == nullptr) {
     const size_t asmem = mlra::absorb_mma_smem(DH);
     static unsigned am_done = 0;
     if (int rc = set_smem_once(mlra::absorb_mma_kernel, am_done, int(mlra::absorb_mma_smem(mlra::kAmMaxDH)))) return rc;
