@@ -170,6 +170,18 @@ class StepRunner:
         for eng, qn, qr in self.engines:  # warm (attributes, tensor maps), then capture
             eng.decode_attention(qn, qr)
         torch.cuda.synchronize()
+        self.fused_tp = reducer is not None and len(self.heads) == cfg.h
+        if self.fused_tp:  # once: the K3-fused TP sum against NCCL on the same step
+            import torch.distributed as dist
+
+            eng, qn, qr = self.engines[0]
+            ref = eng.decode_attention(qn, qr).clone()
+            dist.all_reduce(ref, group=tp_group)
+            got = eng.decode_attention_tp(qn, qr, reducer, out=self.full).clone()
+            torch.cuda.synchronize()
+            ok = torch.tensor([float(torch.allclose(got, ref, rtol=1e-5, atol=1e-6))], device=device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=tp_group)
+            self.fused_tp = ok.item() == 1.0
         self.single = []
         for eng, qn, qr in self.engines:
             gr = torch.cuda.CUDAGraph()
@@ -183,7 +195,7 @@ class StepRunner:
         torch.cuda.synchronize()
 
     def _step(self, eng, qn, qr):
-        if self.reducer is not None and len(self.heads) == self.cfg.h:
+        if self.fused_tp:
             # every rank holds every head (MLRA-4 by latent block): the TP sum runs inside K3
             return eng.decode_attention_tp(qn, qr, self.reducer, out=self.full)
         out = eng.decode_attention(qn, qr)
@@ -527,10 +539,12 @@ def run_ours(args):
                        "d_c=512, d_h^R=64)", "global_batch": BATCH_PER_GROUP * max(1, n_gpus // 4), "seq_len": CTX,
                        "parallelism": f"tp{tp}" + (f"xdp{n_gpus // tp}" if n_gpus > tp else ""),
                        "l2": "2 distinct caches alternated; per-step working set > 126 MB L2",
-                       "graphs": "10 alternating steps per CUDA graph replay", "allreduce": allreduce_kind,
+                       "graphs": "10 alternating steps per CUDA graph replay",
+                       "allreduce": allreduce_kind + ("; fused into K3 (checked against NCCL)" if runner.fused_tp
+                                                      else ""),
                        "algorithmic_bytes_per_gpu_per_step": bytes_rank, "page_size": 128,
                        "nsplit": runner.engines[0][0].nsplit},
-            "gpu_launches": (3 + (1 if reducer is not None and len(runner.heads) != cfg.h else 0)) * args.steps,
+            "gpu_launches": (3 + (1 if reducer is not None and not runner.fused_tp else 0)) * args.steps,
         }
         line.update(extras)
         print(json.dumps(line))
