@@ -464,10 +464,17 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n_gpus = world if world > 1 else args.gpus
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    # test hook: MLRA_BENCH_SHARED_GPU=1 runs every rank on cuda:0 over gloo (the multi-rank
+    # path exercised on a one-GPU box; time-sliced contexts, not a performance measurement)
+    shared = os.environ.get("MLRA_BENCH_SHARED_GPU") == "1"
+    dev_index = 0 if shared else local_rank
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     tp = 1 if n_gpus == 1 else min(n_gpus, 4)
     groups = None
     if world > 1:
@@ -485,7 +492,7 @@ def run_ours(args):
     if tp_group is not None:
         reducer, allreduce_kind = make_reducer(args.allreduce, tp_group, BATCH_PER_GROUP * cfg.h * cfg.d_h, device)
     runner = StepRunner(cfg, own, BATCH_PER_GROUP, CTX, device, tp_group=tp_group, reducer=reducer)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         ms = time_graph_steps(runner, args.steps, args.warmup, rank_sync)
         t = torch.tensor([ms], device=device)
         if world > 1:
