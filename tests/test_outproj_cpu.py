@@ -77,3 +77,16 @@ def test_allreduce_c_abi_validation():
     assert lib.mlra_allreduce(None, None, n, 0, 2, None, None) == -2
     assert lib.mlra_allreduce(None, None, n, 2, 2, None, None) == -2
     assert lib.mlra_allreduce_sim(None, None, n, 9, None, None) == -2
+
+
+def test_decode_step_tp_c_abi_validation():
+    from paper_2603_02188_b200 import _lib
+
+    lib = _lib.load()
+    args = [None] * 9 + [16, 24, 128, 1, 1, 128, 64, 128, 257, 4112, 9, 0.1, 0.5]
+    rc = lib.mlra_decode_step_tp(*args, 2, 2, None, None)
+    assert rc == -2 and b"rank 2 of 2" in lib.mlra_last_error()
+    rc = lib.mlra_decode_step_tp(*args, 0, 9, None, None)
+    assert rc == -2 and b"rank 0 of 9" in lib.mlra_last_error()
+    rc = lib.mlra_decode_step_tp(*args, 0, 2, None, None)
+    assert rc == -2 and b"communication regions" in lib.mlra_last_error()
