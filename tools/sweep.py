@@ -20,8 +20,12 @@ if len(sys.argv) > 1:
 if len(sys.argv) > 2:
     batches = [int(x) for x in sys.argv[2].split(",")]
 mla = trained_config("mla")
+from paper_2603_02188_b200.config import table_context
+tc = table_context()  # the paper's decode benchmark shape: 64 heads, d_h 128, d_h^R 64
 layouts = {"tp4_rank": (cfg, shard_ownership(cfg, 4, 0), 4), "tp1": (cfg, None, 1),
-           "mla_tp4_rank": (mla, shard_ownership(mla, 4, 0), 4), "mla_tp1": (mla, None, 1)}
+           "mla_tp4_rank": (mla, shard_ownership(mla, 4, 0), 4), "mla_tp1": (mla, None, 1),
+           "h64_tp4_rank": (tc["mlra4"], shard_ownership(tc["mlra4"], 4, 0), 4),
+           "h64_mla_tp4_rank": (tc["mla"], shard_ownership(tc["mla"], 4, 0), 4)}
 names = sys.argv[3].split(",") if len(sys.argv) > 3 else ["tp4_rank", "tp1"]
 out_md = sys.argv[4] if len(sys.argv) > 4 else "gpurun_out/sweep.md"
 for name in names:
