@@ -7,8 +7,8 @@ trace = torch.zeros(13824 + 2048, dtype=torch.int64, device="cuda")
 os.environ["MLRA_DEBUG_TRACE_PTR"] = str(trace.data_ptr())
 from paper_2603_02188_b200 import ops
 which = sys.argv[1]
-NB, DLAT = {"tp4": (1, 128), "tp1": (4, 128), "mla": (1, 512)}[which]
-B, H, DH, DR = 16, 24, 128, 64
+NB, DLAT = {"tp4": (1, 128), "tp1": (4, 128), "mla": (1, 512), "h64": (1, 128)}[which]
+B, H, DH, DR = 16, 64 if which == "h64" else 24, 128, 64
 B = int(os.environ.get("TRACE_B", B)); L = int(os.environ.get("TRACE_L", 32768))
 c = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128)
 c2 = make_case(B, H, DH, NB, DLAT, DR, [L] * B, page_size=128, seed=1)  # the bench alternates two caches
