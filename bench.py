@@ -141,6 +141,7 @@ def make_engine(cfg, own, batch, ctx, seed, device, page_size=128):
         pool[s:e] = blk.to(torch.bfloat16)
     eng.cache.seqlens.fill_(ctx)
     eng.cache._host_lens = [ctx] * batch
+    eng.src_weights = w  # the float64 W^UK / W^UV the packs came from (parity tests' oracle input)
     hl = len(eng.heads)
     qn = (torch.randn((batch, hl, cfg.d_h), generator=g, device=device) * 2.0).to(torch.bfloat16)
     qr = torch.zeros((batch, hl, lay.drp), dtype=torch.bfloat16, device=device)
@@ -224,6 +225,24 @@ class StepRunner:
         self.single[i % 2].replay()
 
 
+def make_gqa_engine(cfg, own, batch, ctx, seed, device):
+    """GqaDecodeEngine over a synthetic random bf16 cache (K and V heads ~ N(0, 1))."""
+    import torch
+
+    from paper_2603_02188_b200.gqa import GqaDecodeEngine
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    eng = GqaDecodeEngine(cfg, own, batch=batch, max_tokens=ctx + 64, page_size=128, device=device)
+    pool = eng.cache.pool
+    for s0 in range(0, pool.shape[0], 1 << 20):
+        e = min(pool.shape[0], s0 + (1 << 20))
+        pool[s0:e] = torch.randn((e - s0, pool.shape[1]), generator=g, device=device).to(torch.bfloat16)
+    eng.cache.seqlens.fill_(ctx)
+    eng.cache._host_lens = [ctx] * batch
+    q = eng.prepare_queries(torch.randn((batch, cfg.h, cfg.d_h), generator=g, device=device))
+    return eng, q
+
+
 class GqaStepRunner:
     """GQA comparison variant (2.9B: h=24, g=6, d_h=128): two engines over distinct random
     caches, alternated, one CUDA graph each (K2 GQA + split merge)."""
@@ -231,20 +250,9 @@ class GqaStepRunner:
     def __init__(self, cfg, own, batch, ctx, device):
         import torch
 
-        from paper_2603_02188_b200.gqa import GqaDecodeEngine
-
         self.engines, self.graphs = [], []
         for i in range(2):
-            g = torch.Generator(device=device).manual_seed(2000 + i)
-            eng = GqaDecodeEngine(cfg, own, batch=batch, max_tokens=ctx + 64, page_size=128, device=device)
-            pool = eng.cache.pool
-            for s0 in range(0, pool.shape[0], 1 << 20):
-                e = min(pool.shape[0], s0 + (1 << 20))
-                pool[s0:e] = torch.randn((e - s0, pool.shape[1]), generator=g, device=device).to(torch.bfloat16)
-            eng.cache.seqlens.fill_(ctx)
-            eng.cache._host_lens = [ctx] * batch
-            q = eng.prepare_queries(torch.randn((batch, cfg.h, cfg.d_h), generator=g, device=device))
-            self.engines.append((eng, q))
+            self.engines.append(make_gqa_engine(cfg, own, batch, ctx, 2000 + i, device))
         stream = torch.cuda.Stream(device=device)
         for eng, q in self.engines:
             eng.decode_attention(q)

@@ -515,7 +515,7 @@ class DecodeEngine:
         return ops.decode_step_tp(q_nope, q_rope, self.w_uk, self.w_uv, c.pool, c.block_table, c.seqlens,
                                   c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
                                   self.workspace, reducer.rank, reducer.world, reducer.ptrs,
-                                  out=self.out if out is None else out)
+                                  out=self.out if out is None else out, comm_n=reducer.n)
 
     def decode_attention(self, q_nope: torch.Tensor, q_rope: torch.Tensor, out: torch.Tensor | None = None):
         """One decode-attention step over the cache: bf16 [B, h_local, d_h] / [B, h_local, drp]

@@ -193,7 +193,8 @@ def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seq
 
 def decode_step_tp(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
                    sub: int, dls: int, nsplit: int, score_scale: float, alpha: float, workspace: DecodeWorkspace,
-                   rank: int, world: int, comm_ptrs, out: torch.Tensor | None = None) -> torch.Tensor:
+                   rank: int, world: int, comm_ptrs, out: torch.Tensor | None = None,
+                   comm_n: int | None = None) -> torch.Tensor:
     """decode_step with the sum over the TP ranks fused into K3 (mlra_decode_step_tp): every rank
     gets the device-order sum of all ranks' outputs. comm_ptrs: the ranks' allreduce regions
     (collective.PeerAllReduce(group, B*H*DH).ptrs)."""
@@ -202,8 +203,14 @@ def decode_step_tp(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, 
     dlat = sub * dls
     if workspace.key != (B, H, nb, dlat, DR, nsplit):
         raise ConfigError(f"workspace sized for {workspace.key}, call needs {(B, H, nb, dlat, DR, nsplit)}")
+    if world > 1 and comm_n is not None and comm_n != B * H * DH:
+        # the fused epilogue derives the receive stride, flag array and epoch counter of the
+        # regions from B*H*DH: a region sized for another n would be read and written off-layout
+        raise ConfigError(f"peer regions sized for {comm_n} values, the step reduces {B * H * DH}")
     if out is None:
         out = torch.empty((B, H, DH), dtype=torch.float32, device=q_nope.device)
+    elif out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != (B, H, DH):
+        raise ShapeMismatchError(f"out must be a contiguous float32 [{B}, {H}, {DH}] tensor")
     rc = _lib.load().mlra_decode_step_tp(q_nope.data_ptr(), q_rope.data_ptr(), w_uk_packed.data_ptr(),
                                          w_uv_packed.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
                                          seqlens.data_ptr(), out.data_ptr(), workspace.buf.data_ptr(), B, H, DH, nb,

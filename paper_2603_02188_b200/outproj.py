@@ -68,7 +68,7 @@ class OutputProjection:
             self.w_g = torch.tensor(np.asarray(tensors["w_g"])[:, cols], dtype=torch.float32, device=self.device)
         self.batch = int(batch)
         self.comm = comm
-        if comm is not None and (comm.batch < self.batch or comm.d != cfg.d):
+        if comm is not None and (comm.batch != self.batch or comm.d != cfg.d):
             raise ConfigError("TpComm was sized for another batch / model width")
         self.y = torch.empty((self.batch, cfg.d), dtype=torch.float32, device=self.device)
         self.workspace = ops.outproj_workspace(self.batch, self.width, self.device)
@@ -85,6 +85,10 @@ class OutputProjection:
                  residual: bool = True, out: torch.Tensor | None = None) -> torch.Tensor:
         """attn [B, h_local, d_h] (or [B, h_local*d_h]) fp32, hidden [B, d] fp32 -> y [B, d]."""
         B = attn.shape[0]
+        if self.comm is not None and self.comm.world > 1 and B != self.comm.batch:
+            # K4 lays out the receive slots, flags and epoch counter of the region from the
+            # call's batch: a call of another batch would read the counters at the wrong place
+            raise ConfigError(f"multi-rank output projection sized for batch {self.comm.batch}, called with {B}")
         a = attn.reshape(B, -1)
         if a.shape[1] != self.width:
             raise ShapeMismatchError(f"attention width {a.shape[1]} != {self.width} ({len(self.heads)} heads)")

@@ -96,7 +96,7 @@ def shard_ownership(cfg: AttnConfig, phi: int, device_id: int) -> Ownership:  # 
 
 def _resource_keys(own: Ownership) -> list[str]:  # tpsim.py:134-144 (latent family + gqa)
     if not own.units:
-        return [f"k{s}" for s in own.kv_slots] + [f"v{s}" for s in own.kv_slots]
+        return [f"{s}[{slot}]" for s in ("k", "v") for slot in own.kv_slots]
     return [unit.stream for unit in own.units] + ["rope"]
 
 
