@@ -319,18 +319,21 @@ def time_k2_alone(eng_qs, iters):
     return e0.elapsed_time(e1) / (reps * per)
 
 
-def e2e_steps(engines, steps, warmup):
+def e2e_steps(engines, steps, warmup, reducer=None, rank_sync=None):
     """The plugin calls a user makes, with HOST buffers, every step: one H2D of the new token's
     cache rows + queries from pinned memory, K0 (append, advancing seqlens) + K1..K3 through
-    the C ABI, one D2H of the fp32 output. Two micro-batches (the two caches) are stepped in
-    turn by host_loop.MicroBatchLoop: micro-batch k+1's upload and k-1's download overlap k's
-    kernels. Also returns the serial time (one micro-batch, copies in line on one stream)."""
+    the C ABI (with reducer: mlra_decode_step_tp, the TP group's sum fused into K3), one D2H of
+    the fp32 output. Two micro-batches (the two caches) are stepped in turn by
+    host_loop.MicroBatchLoop: micro-batch k+1's upload and k-1's download overlap k's kernels.
+    Also returns the serial time (one micro-batch, copies in line on one stream). Under torchrun
+    every rank runs it (same call sequence); the caller takes the max over ranks."""
     import torch
 
     from paper_2603_02188_b200 import ops
     from paper_2603_02188_b200.host_loop import MicroBatchLoop
 
-    loop = MicroBatchLoop(engines)
+    sync = rank_sync or torch.cuda.synchronize
+    loop = MicroBatchLoop(engines, reducer=reducer)
     g = torch.Generator().manual_seed(7)
     for k in range(len(loop)):
         for t in loop.host_inputs(k):
@@ -342,7 +345,7 @@ def e2e_steps(engines, steps, warmup):
             loop.submit(i % len(loop))
 
     run(warmup * len(loop))
-    torch.cuda.synchronize()
+    sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     loop.start()
     t0 = time.perf_counter()
@@ -352,6 +355,7 @@ def e2e_steps(engines, steps, warmup):
     e1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    sync()
     piped = max(e0.elapsed_time(e1) / 1e3, wall) / steps
 
     # serial reference point: same calls, one micro-batch, every copy in line
@@ -366,12 +370,14 @@ def e2e_steps(engines, steps, warmup):
             d.copy_(h, non_blocking=True)
         c.reserve_token()
         ops.cache_append(d_in[0], c.block_table, c.seqlens, c.pool, c.page_size, advance=True)
-        h_out.copy_(eng.decode_attention(d_in[1], d_in[2]), non_blocking=True)
+        out = eng.decode_attention_tp(d_in[1], d_in[2], reducer) if reducer is not None else \
+            eng.decode_attention(d_in[1], d_in[2])
+        h_out.copy_(out, non_blocking=True)
 
     nser = max(3, steps // 2)
     for _ in range(warmup):
         one()
-    torch.cuda.synchronize()
+    sync()
     t0 = time.perf_counter()
     e0.record()
     for _ in range(nser):
@@ -379,6 +385,7 @@ def e2e_steps(engines, steps, warmup):
     e1.record()
     torch.cuda.synchronize()
     serial = max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0) / nser
+    sync()
     for e, lens in zip(engines, start_lens):  # back to the benchmark context
         e.cache.seqlens.copy_(torch.tensor(lens, dtype=torch.int32))
         e.cache._host_lens = list(lens)
@@ -395,7 +402,8 @@ def cpu_cores():
 
 
 def cpu_oracle_sample(phi: int, n: int, seqs: int, seed: int = 0):
-    """Time the oracle's attention (attend_local + reduce) over `seqs` sequences of n tokens."""
+    """Time the oracle port's attention (attend_local + reduce) over `seqs` sequences of n tokens
+    (the fallback CPU baseline when the reference is not installed in baseline/_ref)."""
     from oracle import attnkit_port as ak
 
     cfg = ak.Cfg("mlra", 24, 3072, 128, 64, 512, 1024, branches=4, scaling=True)
@@ -415,49 +423,160 @@ def cpu_oracle_sample(phi: int, n: int, seqs: int, seed: int = 0):
     return seqs * n * per_tok_bytes / dt / 1e9, dt
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The unmodified reference package (attnkit), installed into baseline/_ref by
+    `pip install --no-index --no-build-isolation --no-deps --target baseline/_ref <copy of
+    /root/reference/pkg>`; None when absent."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import attnkit
+        from attnkit import cache as ak_cache
+        from attnkit import decode as ak_decode
+        from attnkit import tpsim as ak_tpsim
+    except Exception:
+        return None
+    return attnkit, ak_cache, ak_decode, ak_tpsim
+
+
+class ReferenceWorkload:
+    """The reference's own decode attention (attnkit/decode.py:204-285) over a batch of
+    sequences of one TP group: per sequence and per logical device of the group, attnkit's
+    ``attend_local`` on that device's ``KvCache`` (built once with ``cache_from_streams``,
+    attnkit/cache.py:95-102; random rows with the RMS of the reference's latents), then one
+    ``reduce_contributions`` over the devices' contributions in device-id order -- the body of
+    ``sim_decode`` (attnkit/tpsim.py:269-276) without the token append. Sequences run one after
+    the other on the reference's stock path (its ATTNKIT_THREADS default is 1 worker; numpy's
+    BLAS uses every host thread)."""
+
+    def __init__(self, ref, phi: int, seqs: int, n: int, seed: int = 0):
+        attnkit, ak_cache, ak_decode, ak_tpsim = ref
+        self.ak_decode = ak_decode
+        self.cfg = attnkit.trained_config("mlra4")
+        cfg = self.cfg
+        rng = np.random.default_rng(seed)
+        w = {"w_uk": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02,
+             "w_uv": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02}
+        self.devices = []
+        for k in range(phi):
+            own = ak_tpsim.shard_ownership(cfg, phi, k) if phi > 1 else ak_decode.full_ownership(cfg)
+            self.devices.append((own, ak_decode.local_weights(cfg, w, own)))
+        akv = (4 * cfg.d / cfg.d_c) ** 0.5  # alpha_kv: the cached latent's per-element RMS
+        self.caches = []
+        for _ in range(seqs):
+            rope = rng.standard_normal((n, cfg.d_h_rope)) * 1.1
+            per_dev = []
+            for own, _lw in self.devices:
+                streams = {u.stream: rng.standard_normal((n, cfg.block_dim)) * akv for u in own.units}
+                streams["rope"] = rope
+                per_dev.append(ak_cache.cache_from_streams(cfg, streams))
+            self.caches.append(per_dev)
+        self.queries = {"q_nope": rng.standard_normal((cfg.h, cfg.d_h)),
+                        "q_rope": rng.standard_normal((cfg.h, cfg.d_h_rope))}
+        self.bytes_per_step = seqs * n * sum((len(own.units) * cfg.block_dim + cfg.d_h_rope) * 2
+                                             for own, _ in self.devices)
+
+    def step(self):
+        d = self.ak_decode
+        for per_dev in self.caches:
+            contribs = []
+            for (own, lw), cache in zip(self.devices, per_dev):
+                contribs.extend(d.attend_local(self.cfg, lw, own, cache, self.queries))
+            d.reduce_contributions(self.cfg, contribs)
+
+
+def cpu_baseline():
+    """The reference's own CPU path (attnkit, baseline/_ref) on a bounded sample of the N = 1
+    workload: 6 sequences x 32K (TP1), attended twice (~5-10 s of host work); the oracle port
+    when the reference is not installed."""
+    ref = import_reference()
+    if ref is None:
+        nseq = BATCH_PER_GROUP * 16
+        gbs_cpu, dt = cpu_oracle_sample(1, CTX, nseq)
+        return {"value": round(gbs_cpu, 3), "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
+                "sample": f"{nseq} sequences x {CTX} tokens of the TP1 workload (numpy float64 oracle "
+                          f"attend_local+reduce, BLAS on all host threads), {dt:.1f} s"}
+    work = ReferenceWorkload(ref, 1, 6, CTX, seed=1)
+    work.step()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        work.step()
+    dt = time.perf_counter() - t0
+    return {"value": round(2 * work.bytes_per_step / dt / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(),
+            "kind": "reference", "sample": f"2 x 6 sequences x {CTX} tokens of the TP1 workload: attnkit "
+                                           f"attend_local + reduce_contributions (baseline/_ref, float64, BLAS on "
+                                           f"all host threads), {dt:.1f} s"}
+
+
 # ----------------------------------------------------------------------------- main
 def run_reference(args):
-    from paper_2603_02188_b200.config import trained_config
-
+    """--impl reference: the reference's own CPU path (attnkit from baseline/_ref, unmodified)
+    on this arm's workload, rank 0 only. N = 1: the whole configs[1] batch (16 sequences x 32K,
+    TP1) every step. N > 1: each step a bounded sample of the TP-group workload (4 sequences x
+    32K on all phi logical devices; the full group would take minutes per step on the host)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n_gpus = args.gpus
+    ref = import_reference()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n_gpus = world if world > 1 else args.gpus
     phi = 1 if n_gpus == 1 else min(n_gpus, 4)
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "attnkit not installed in baseline/_ref"}))
+        return 0
+    seqs = BATCH_PER_GROUP if n_gpus == 1 else 4
+    ctx = context_for(n_gpus)
+    t_build = time.perf_counter()
+    work = ReferenceWorkload(ref, phi, seqs, ctx)
+    t_build = time.perf_counter() - t_build
     for _ in range(args.warmup):
-        cpu_oracle_sample(phi, CTX, 1)
-    vals = []
+        work.step()
+    times = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, _ = cpu_oracle_sample(phi, CTX, 1)
-        vals.append(v)
+        ts = time.perf_counter()
+        work.step()
+        times.append(time.perf_counter() - ts)
     total = time.perf_counter() - t0
-    gbs = float(np.median(vals))
-    cfg = trained_config("mlra4")
-    seqs = BATCH_PER_GROUP * max(1, n_gpus // 4)
-    per_gpu_bytes = seqs * CTX * (int(4 // phi) * 128 + 64) * 2
+    ms = total / args.steps * 1e3
+    gbs = work.bytes_per_step / (ms * 1e-3) / 1e9
+    sample = (f"{seqs} sequences x {ctx} tokens per step on {phi} logical device(s): attnkit attend_local per "
+              f"(sequence, device) + reduce_contributions (float64 numpy, BLAS on all host threads); "
+              f"{'the whole batch' if n_gpus == 1 else 'a bounded sample of the group batch'}; caches built "
+              f"once with cache_from_streams ({t_build:.1f} s, untimed)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_gpu_bytes / (gbs * 1e9) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _workload_name(n_gpus), "global_batch": seqs, "seq_len": CTX, "tp": phi,
-                   "model": f"2.9B MLRA-4 attention layer h={cfg.h} d_h={cfg.d_h} d_c={cfg.d_c}"},
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
-                         "sample": f"1 sequence x {CTX} tokens per step (TP{phi} device share), numpy float64 "
-                                   f"oracle/attnkit_port.py attend_local+reduce; ms_per_step extrapolates to the "
-                                   f"full batch"},
-        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": total,
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong" if n_gpus <= 4 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (random rows with the reference latents' RMS)",
+        "config": {"workload": _workload_name(n_gpus), "model": "2.9B MLRA-4 attention layer (h=24, d_h=128, "
+                   "d_c=512, d_h^R=64)", "global_batch": seqs, "seq_len": ctx,
+                   "parallelism": f"tp{phi} (simulated devices, attnkit/tpsim.py)" if phi > 1 else "tp1",
+                   "reference": "attnkit 0.1.0, unmodified (baseline/_ref)"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms_min_median": [round(min(times) * 1e3, 3), round(float(np.median(times)) * 1e3, 3)],
+        "wall_s": round(total, 2),
     }
     print(json.dumps(line))
     return 0
 
 
+def context_for(n_gpus: int) -> int:
+    """configs[2] (TP4 on 4 GPUs) is quoted at 64K; every other N runs the 32K metric context."""
+    return 65536 if n_gpus == 4 else CTX
+
+
 def _workload_name(n):
     return {1: "configs[1]: MLRA-4 2.9B layer, B=16, 32K ctx, TP1 on 1 GPU",
-            2: "MLRA-4 2.9B layer, B=16, 32K ctx, TP2",
-            4: "configs[2]-shape: MLRA-4 2.9B layer, B=16, 32K ctx, TP4 (NCCL all-reduce)",
-            8: "configs[4]: 2 x TP4 over B=32 (16 per group), 32K ctx"}.get(n, f"{n} GPUs")
+            2: "MLRA-4 2.9B layer, B=16, 32K ctx, TP2 (rank sum fused into K3 over NVLink peer memory)",
+            4: "configs[2]: MLRA-4 2.9B layer, B=16, 64K ctx, TP4 (rank sum fused into K3 over NVLink peer "
+               "memory; NCCL all-reduce only as the fallback)",
+            8: "configs[4]: 2 x TP4 over B=32 (16 per group), 32K ctx (rank sum fused into K3)"}.get(n, f"{n} GPUs")
 
 
 def run_ours(args):
@@ -499,7 +618,8 @@ def run_ours(args):
     reducer, allreduce_kind = None, "none (tp1)"
     if tp_group is not None:
         reducer, allreduce_kind = make_reducer(args.allreduce, tp_group, BATCH_PER_GROUP * cfg.h * cfg.d_h, device)
-    runner = StepRunner(cfg, own, BATCH_PER_GROUP, CTX, device, tp_group=tp_group, reducer=reducer)
+    ctx = context_for(n_gpus)
+    runner = StepRunner(cfg, own, BATCH_PER_GROUP, ctx, device, tp_group=tp_group, reducer=reducer)
     with ClockSampler(dev_index) as clk:
         ms = time_graph_steps(runner, args.steps, args.warmup, rank_sync)
         t = torch.tensor([ms], device=device)
@@ -510,9 +630,19 @@ def run_ours(args):
         # (untimed, same count on every rank) for ~0.6 s so the clock record sees real load.
         runner.run(max(50, int(600.0 / max(ms, 1e-3))))
         rank_sync()
-    bytes_rank = algorithmic_bytes(cfg, tp, [CTX] * BATCH_PER_GROUP)
+    bytes_rank = algorithmic_bytes(cfg, tp, [ctx] * BATCH_PER_GROUP)
     total_bytes = bytes_rank * n_gpus
     value = total_bytes / (ms * 1e-3) / 1e9
+
+    # end to end through the C ABI from pinned host buffers, on every rank (the TP sum fused
+    # into K3 when the group has one); whole-job bytes over the slowest rank's time
+    e2e_red = reducer if runner.fused_tp else None
+    e2e_s, ser_s, bin_, bout = e2e_steps([e for e, _, _ in runner.engines], max(4, args.steps), args.warmup,
+                                         reducer=e2e_red, rank_sync=rank_sync)
+    tt = torch.tensor([e2e_s, ser_s], device=device)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s, ser_s = float(tt[0]), float(tt[1])
 
     extras = {}
     if rank == 0:
@@ -520,38 +650,32 @@ def run_ours(args):
         k2_ms = time_k2_alone(runner.engines, 20)
         k2_bytes = bytes_rank
         achieved = k2_bytes / (k2_ms * 1e-3) / 1e9
-        workload = f"mlra4_tp{tp}_b{BATCH_PER_GROUP}_n{CTX}"
+        workload = f"mlra4_tp{tp}_b{BATCH_PER_GROUP}_n{ctx}"
         extras["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                               "frac": round(achieved / hbm_peak, 4), "traffic": ncu_traffic(workload),
                               "kernel": "mlra_decode_kernel (K2)", "kernel_us": round(k2_ms * 1e3, 2),
                               "algorithmic_bytes_per_launch": k2_bytes, "peak_kind": f"{peak_kind} copy (burst)"}
         extras["clocks"] = clk.summary()
-        e2e_s, ser_s, bin_, bout = e2e_steps([e for e, _, _ in runner.engines], max(4, args.steps), args.warmup)
-        # e2e is a single-GPU call through the C ABI; at N>1 it measures this rank's share
-        e2e_bytes = bytes_rank * (n_gpus if world == 1 else 1)
-        extras["e2e"] = {"value": round(e2e_bytes / e2e_s / 1e9, 1), "unit": "GB/s", "h2d_bytes_per_step": bin_,
-                         "d2h_bytes_per_step": bout, "ms_per_step": round(e2e_s * 1e3, 4),
-                         "serial_ms_per_step": round(ser_s * 1e3, 4),
-                         "path": "host_loop.MicroBatchLoop: per step 1 H2D (pinned rows+queries), mlra_cache_append "
-                                 "(advance) + mlra_decode_step (C ABI), 1 D2H; 2 micro-batches, the copies and K0 on "
-                                 "side streams overlapping the other micro-batch's kernels; serial_ms_per_step = "
-                                 "same calls on one stream, no overlap"
-                                 + ("" if world == 1 else "; rank 0 share (no collective)")}
         if n_gpus == 1 and not args.quick:
             extras.update(per_gpu_comparisons(cfg, device, args))
         if n_gpus == 1 and not args.no_cpu:
-            nseq = BATCH_PER_GROUP * 16  # the B=16 batch sixteen times over: ~10 s of host work
-            gbs_cpu, dt = cpu_oracle_sample(1, CTX, nseq)
-            extras["cpu_baseline"] = {"value": round(gbs_cpu, 3), "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
-                                      "sample": f"{nseq} sequences x {CTX} tokens of the TP1 workload (numpy float64 "
-                                                f"oracle attend_local+reduce, BLAS on all host threads), {dt:.1f} s"}
+            extras["cpu_baseline"] = cpu_baseline()
+        extras["e2e"] = {"value": round(total_bytes / e2e_s / 1e9, 1), "unit": "GB/s", "h2d_bytes_per_step": bin_,
+                         "d2h_bytes_per_step": bout, "ms_per_step": round(e2e_s * 1e3, 4),
+                         "serial_ms_per_step": round(ser_s * 1e3, 4),
+                         "path": "host_loop.MicroBatchLoop: per step 1 H2D (pinned rows+queries), mlra_cache_append "
+                                 "(advance) + " + ("mlra_decode_step_tp (C ABI; the TP sum over the group fused into K3)"
+                                                   if e2e_red is not None else "mlra_decode_step (C ABI)") +
+                                 ", 1 D2H; 2 micro-batches, the copies and K0 on side streams overlapping the other "
+                                 "micro-batch's kernels; serial_ms_per_step = same calls on one stream, no overlap; "
+                                 "per-rank bytes/step and Bi/Bo, time = max over ranks"}
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "strong" if n_gpus <= 4 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 caches with the reference's latent RMS; random W^UK/W^UV)",
             "config": {"workload": _workload_name(n_gpus), "model": "2.9B MLRA-4 attention layer (h=24, d_h=128, "
-                       "d_c=512, d_h^R=64)", "global_batch": BATCH_PER_GROUP * max(1, n_gpus // 4), "seq_len": CTX,
+                       "d_c=512, d_h^R=64)", "global_batch": BATCH_PER_GROUP * max(1, n_gpus // 4), "seq_len": ctx,
                        "parallelism": f"tp{tp}" + (f"xdp{n_gpus // tp}" if n_gpus > tp else ""),
                        "l2": "2 distinct caches alternated; per-step working set > 126 MB L2",
                        "graphs": "10 alternating steps per CUDA graph replay",

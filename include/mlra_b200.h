@@ -35,7 +35,7 @@ extern "C" {
 #define MLRA_ERR_CUDA (-4)    /* launch / runtime failure          */
 
 /* ABI version (major*100 + minor). */
-int mlra_version(void);
+int mlra_version(void);  /* 200: fused single-launch step, status word */
 
 /* Message of the last failed call on this thread ("" if none). */
 const char* mlra_last_error(void);
@@ -87,10 +87,24 @@ int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int
 int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, void* q_abs, void* q_rope_out, int B,
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream);
 
-/* Bytes of device workspace mlra_decode_step needs (split-KV partials, absorbed queries,
- * merge scratch and per-sequence completion counters). Zero-initialise it once before first
- * use; K1 resets the counters every step afterwards. */
+/* Bytes of device workspace mlra_decode_step / mlra_decode_step_tp need: the numeric status word,
+ * the absorbed queries, the split-KV partials, the merge / per-chunk scratch and the fused step's
+ * completion counters. Zero-fill it once before first use; every launch leaves the counters at
+ * zero again (the last CTA of the fused step resets them). */
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit);
+
+/*
+ * Numeric status (attnkit/tensors.py:74-78 softmax_rows: NaN in the logits, or a row with no
+ * finite logit -> NumericError). The FIRST 4 BYTES of every decode workspace are an int32
+ * status word that the merge (K3, or the fused step's epilogue) ORs with MLRA_STATUS_NAN /
+ * MLRA_STATUS_NO_FINITE; mlra_combine takes the word explicitly (or NULL). Kernels never stop
+ * on a bad value (a serving loop keeps its CUDA graph); the caller checks when it wants to:
+ * mlra_check_status synchronises `stream` (the one ABI call that does), reads the word, resets
+ * it when `reset` != 0 and returns MLRA_ERR_NUMERIC if any flag was set.
+ */
+#define MLRA_STATUS_NAN 1
+#define MLRA_STATUS_NO_FINITE 2
+int mlra_check_status(int32_t* status, int reset, void* stream);
 
 /* Split count used when the caller passes nsplit <= 0 (fills the SMs for this batch). */
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB);
@@ -121,16 +135,18 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
  *   alpha = alpha_attn (latent.py:56-61: 1/sqrt(branches) for mlra, 1 otherwise)
  */
 int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
-                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream);
+                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, int32_t* status, void* stream);
 
 /*
- * K1 + K2 + K3 in one stream-ordered call: one decode-attention step for a batch.
- * Replaces decode.py:304-305 (attend_local + reduce_contributions inside
- * absorbed_decode_step) for every unit a device owns.
- * K1, K2, K3 are launched in turn on `stream`; K2 and K3 with programmatic dependent launch
- * (K2's TMA producer streams the cache while K1 drains; K3 loads W^UV early and waits only
- * for the K2 CTAs of its own sequences through per-sequence counters in the workspace, which
- * K1 resets every step). Environment MLRA_NO_PDL=1 falls back to plain stream order.
+ * One decode-attention step for a batch: K1 (absorb) + K2 (split-KV decode) + K3 (merge, W^UV,
+ * ascending branch sum, alpha). Replaces decode.py:304-305 (attend_local + reduce_contributions
+ * inside absorbed_decode_step) for every unit a device owns.
+ * When the K2 grid (nsplit x B x head groups) is co-resident (one CTA per SM, grid <= #SMs) it
+ * is ONE launch: the absorption runs in K2's prologue while the TMA producer already streams the
+ * cache, and the merge / up-projection in its epilogue, gated per sequence by completion
+ * counters in the workspace (fused_step.cuh). Otherwise K1, K2 and K3 run as three kernels in
+ * stream order (K2 programmatically dependent on K1). MLRA_NO_FUSE=1 forces the three-kernel
+ * path, MLRA_NO_PDL=1 plain stream order for it.
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  *   nsplit in [1, 160] (mlra_default_splits: one wave of the SMs for this batch)
  */
@@ -150,6 +166,7 @@ int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, c
  *   score_scale = tau * log2(e), tau = 1/sqrt(d_h) (config.py:112), applied in fp32
  *   o_part [B, nsplit, G, R, DH] fp32, lse_part [B, nsplit, G, R] fp32
  *   out    [B, G*R, DH] fp32 (mlra_gqa_decode_step: K2 + split merge)
+ * mlra_gqa_workspace_bytes includes the int32 status word (first 4 bytes, see mlra_check_status).
  */
 int mlra_gqa_default_splits(int B, int G, int max_seqlen);
 size_t mlra_gqa_workspace_bytes(int B, int G, int R, int DH, int nsplit);

@@ -33,7 +33,8 @@ SIGNATURES = {
     "mlra_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "mlra_default_splits": (_I, [_I, _I, _I, _I]),
     "mlra_decode_partials": (_I, [_P] * 7 + [_I] * 10 + [_P]),
-    "mlra_combine": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _I, _P]),
+    "mlra_combine": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _I, _P, _P]),
+    "mlra_check_status": (_I, [_P, _I, _P]),
     "mlra_decode_step": (_I, [_P] * 9 + [_I] * 11 + [_F, _F, _P]),
     "mlra_gqa_default_splits": (_I, [_I, _I, _I]),
     "mlra_gqa_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I, _I, _I]),

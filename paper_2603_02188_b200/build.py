@@ -14,10 +14,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmlra_b200.so")
-SOURCES = ["capi.cu"]
-HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cuh", "allreduce_kernel.cuh"]
+SOURCES = ["capi.cu", "decode_inst_a.cu", "decode_inst_b.cu", "decode_inst_c.cu", "decode_inst_d.cu"]
+HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cuh", "allreduce_kernel.cuh",
+           "fused_step.cuh", "host_common.cuh", "peer_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 STAMP = LIB + ".srchash"  # source hash of the shipped library (travels with it)
 
 
@@ -50,17 +51,32 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit (in parallel) and link libmlra_b200.so in-tree."""
     if not force and not _stale():
         return LIB
-    cmd = [nvcc(), *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    cmd += ["-lcudart"]
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", "-o", obj, os.path.join(CSRC, src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(obj)}")
+        if verbose:
+            sys.stderr.write(res.stderr)
+    cmd = [nvcc(), *ARCH, "--shared", "-o", LIB + ".tmp", *[o for o, _ in results], "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libmlra_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libmlra_b200.so")
     os.replace(LIB + ".tmp", LIB)
     with open(STAMP, "w") as f:
         f.write(source_hash() + "\n")

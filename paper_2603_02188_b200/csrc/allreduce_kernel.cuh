@@ -15,51 +15,11 @@
 //
 // Region of a rank (mlra_allreduce_comm_bytes): fp32 recv [2][world][n rounded to 4], uint32 flags
 // [2][world][kArFlagSlots], uint32 {epoch counter, done counter}; zero-filled once.
+// K5 kernel (region layout and the protocol: peer_common.cuh).
 #pragma once
-#include <cstdint>
-#include "ptx.cuh"
+#include "peer_common.cuh"
 
 namespace mlra {
-
-constexpr int kArThreads = 256, kArChunk = kArThreads * 4, kArMaxRanks = 8;
-// Flag slots per (parity, source rank): shared layout with K3's fused TP sum (one region, one
-// epoch counter for both), so up to kArFlagSlots chunks / K3 CTAs.
-constexpr int kArFlagSlots = 4096;
-
-struct AllReduceParams {
-  const float* x[kArMaxRanks];  // per local rank [n]
-  float* y[kArMaxRanks];        // per local rank [n]
-  float* comm[kArMaxRanks];     // region of every GLOBAL rank, as mapped here
-  int n, world, rank0, nchunks;
-};
-
-// per-rank slot stride: n rounded up to whole float4s
-__host__ __device__ inline size_t ar_stride(int n) { return (size_t(n) + 3) / 4 * 4; }
-__host__ __device__ inline size_t ar_recv_floats(int n, int world) { return size_t(2) * world * ar_stride(n); }
-__host__ __device__ inline size_t ar_flag_words(int world) { return size_t(2) * world * kArFlagSlots; }
-__host__ __device__ inline size_t ar_region_bytes(int n, int world) {
-  return ar_recv_floats(n, world) * 4 + ar_flag_words(world) * 4 + 16;
-}
-
-// A rank's view of the TP group for a fused sum (K3 epilogue): world <= 1 means off.
-struct TpSum {
-  float* comm[kArMaxRanks];  // region of every GLOBAL rank, as mapped here
-  int world, rank;
-};
-
-__device__ __forceinline__ void ar_st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ar_ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ar_globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
-  return t;
-}
 
 __global__ void __launch_bounds__(kArThreads) allreduce_kernel(const __grid_constant__ AllReduceParams p) {
   const int c = blockIdx.x, li = blockIdx.y, rank = p.rank0 + li, tid = threadIdx.x, W = p.world;

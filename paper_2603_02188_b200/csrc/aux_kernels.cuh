@@ -6,6 +6,7 @@
 #include <cmath>
 #include "ptx.cuh"
 #include "allreduce_kernel.cuh"
+#include "fused_step.cuh"
 
 namespace mlra {
 
@@ -223,7 +224,7 @@ inline size_t head_gemm_smem(int kp) {
 constexpr int kMergeMaxSplits = 160;  // 5 per lane
 __global__ void merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                     float* __restrict__ z, int B, int NB, int H, int DLAT, int nsplit, float alpha,
-                                    int zout_bnh) {
+                                    int zout_bnh, int* __restrict__ status) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= B * NB * H) return;
@@ -239,6 +240,14 @@ __global__ void merge_splits_kernel(const float* __restrict__ o_part, const floa
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  {  // numeric status (attnkit/tensors.py:74-78): a NaN logit, or no finite logit in the row
+    bool nan = false;
+#pragma unroll
+    for (int j = 0; j < kMergeMaxSplits / 32; ++j) nan |= lk[j] != lk[j];
+    const bool any_nan = __any_sync(0xffffffffu, nan);
+    if (status != nullptr && lane == 0 && (any_nan || m == -INFINITY))
+      atomicOr(status, (any_nan ? kStatusNaN : 0) | (m == -INFINITY ? kStatusNoFinite : 0));
+  }
   float wk[kMergeMaxSplits / 32], tot = 0.f;
 #pragma unroll
   for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
@@ -473,7 +482,7 @@ template <int SEQS, int THREADS = 256>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
-                int nsplit, float alpha, int per_branch, const TpSum tp) {
+                int nsplit, float alpha, int per_branch, const TpSum tp, int* __restrict__ status) {
   static_assert(SEQS == 2 || SEQS == 4 || SEQS == 8, "2, 4 or 8 sequences per CTA");
   constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
@@ -547,6 +556,14 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
       }
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      {  // numeric status (attnkit/tensors.py:74-78)
+        bool nan = false;
+#pragma unroll
+        for (int j = 0; j < kMergeMaxSplits / 32; ++j) nan |= lk[j] != lk[j];
+        const bool any_nan = __any_sync(0xffffffffu, nan);
+        if (status != nullptr && lane == 0 && s < B && (any_nan || m == -INFINITY))
+          atomicOr(status, (any_nan ? kStatusNaN : 0) | (m == -INFINITY ? kStatusNoFinite : 0));
+      }
       float tot = 0.f;
 #pragma unroll
       for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
@@ -776,7 +793,7 @@ template <int KP>
 __global__ void __launch_bounds__(kSkThreads)
 combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                       const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT,
-                      int DH, int nsplit, float alpha) {
+                      int DH, int nsplit, float alpha, int* __restrict__ status) {
   extern __shared__ __align__(128) uint8_t sk_smem[];
   const int rows = NB * DLAT, DSL = DH / KP;
   __nv_bfloat16* wsl = reinterpret_cast<__nv_bfloat16*>(sk_smem);  // [rows][DSL]
@@ -804,6 +821,7 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
   for (int it = tid; it < 4 * rows; it += kSkThreads) {
     const int q = it / rows, r = it % rows, b = r / DLAT, c = r % DLAT, s = s0 + q;
     float m = -INFINITY, l = 0.f, z = 0.f;
+    bool nan = false;
     if (s < B) {
       const float* lp = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
       const float* op = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
@@ -814,6 +832,7 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
           const int k = min(kb + j, k1 - 1);
           lk[j] = __ldcg(lp + size_t(k) * NB * H);
           v[j] = __ldcg(op + size_t(k) * kstride);
+          nan |= lk[j] != lk[j];
         }
         float mc = m;
 #pragma unroll
@@ -833,6 +852,7 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
       }
     }
     pz[q * rows + r] = z;
+    if (nan && c == 0 && status != nullptr) atomicOr(status, kStatusNaN);  // attnkit/tensors.py:74-75
     if (c == 0) {
       pml[(q * NB + b) * 2] = m;
       pml[(q * NB + b) * 2 + 1] = l;
@@ -861,6 +881,8 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
       float M = -INFINITY;
 #pragma unroll
       for (int j = 0; j < KP; ++j) M = fmaxf(M, mk[j]);
+      if (M == -INFINITY && kp == 0 && r % DLAT == 0 && status != nullptr)
+        atomicOr(status, kStatusNoFinite);  // no finite logit in the row (attnkit/tensors.py:76-77)
       float L = 0.f, Z = 0.f;
       if (M != -INFINITY) {
 #pragma unroll

@@ -1,5 +1,6 @@
 // C ABI of libmlra_b200.so (include/mlra_b200.h): argument validation, TMA descriptor
-// encoding, kernel selection and launch. No allocation, no synchronisation.
+// encoding, kernel selection and launch. No allocation; no synchronisation except in
+// mlra_check_status (which exists to read the status word).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -9,29 +10,19 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
-#include "../../include/mlra_b200.h"
+#include "host_common.cuh"
 #include "aux_kernels.cuh"
-#include "decode_kernel.cuh"
 #include "outproj_kernel.cuh"
 #include "allreduce_kernel.cuh"
 
-namespace {
-
+namespace mlra_host {
 thread_local char g_err[512] = "";
+MLRA_DECODE_INSTANCES(MLRA_EXTERN_DECODE)
+}  // namespace mlra_host
 
-int fail(int code, const char* fmt, ...) {
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(g_err, sizeof(g_err), fmt, ap);
-  va_end(ap);
-  return code;
-}
+using namespace mlra_host;
 
-int cuda_check(const char* what) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(MLRA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
-  return MLRA_OK;
-}
+namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -44,106 +35,6 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   });
   return fn;
-}
-
-// Launch with (pdl = true) programmatic stream serialization: the kernel may start before its
-// predecessor on the stream finishes and must griddepcontrol.wait before consuming its output.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
-                      Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
-template <typename K>
-int set_smem_once(K kern, unsigned& done_mask, int bytes) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 32 && (done_mask & (1u << dev))) return MLRA_OK;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
-    return cuda_check("cudaFuncSetAttribute");
-  if (dev < 32) done_mask |= 1u << dev;
-  return MLRA_OK;
-}
-
-constexpr int kSmemBudget = 232448;  // 227 KB opt-in dynamic smem (the kernel has no static smem)
-
-template <int T, int NPAD, int DLS, int NB, bool GQA = false>
-int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra::DecodeParams p, int head_groups,
-                  cudaStream_t stream) {
-  using L = mlra::DecodeLayout<T, NPAD, DLS>;
-  const int q_chunks = NB * p.SUB * (DLS / 64) + 1;
-  auto fixed = [&](int p_slots) { return q_chunks * L::kQChunkBytes + p_slots * L::kPBytes + L::kScratchBytes; };
-  auto fits = [&](int lat, int rope, int ps) { return L::smem_bytes(NB, p.SUB, lat, rope, ps) <= kSmemBudget; };
-  int rope_slots = 0, lat_slots = 0, p_slots = 2;
-  if (GQA) {
-    // K and V sub-blocks share one ring; no rope part
-    lat_slots = (kSmemBudget - fixed(2)) / L::kLatBytes;
-    if (lat_slots < 3) return fail(MLRA_ERR_CONFIG, "gqa decode: ring of %d slots < 3", lat_slots);
-  } else if (NB > 1) {
-    // Several branches per tile share one rope tile (consumed by the tile's first QK): one
-    // rope slot suffices; latent depth is what keeps HBM busy (5 slots with a single P
-    // buffer beat 4 with two).
-    if (fits(5, 1, 1)) { lat_slots = 5; rope_slots = 1; p_slots = 1; }
-    else { rope_slots = 2; lat_slots = (kSmemBudget - fixed(2) - 2 * L::kRopeBytes) / L::kLatBytes; }
-  } else if (p.SUB == 1) {
-    // one branch: every round consumes a latent and a rope sub-block -> equal ring depths
-    for (int d = 6; d >= 2; --d)
-      if (fits(d, d, 2)) { lat_slots = rope_slots = d; break; }
-  } else {
-    // multi-block latent (MLA, 64-token tiles): 2*SUB resident + 1 in flight at least
-    rope_slots = T == 64 ? 3 : 2;
-    for (;; --rope_slots) {
-      lat_slots = (kSmemBudget - fixed(2) - rope_slots * L::kRopeBytes) / L::kLatBytes;
-      if (lat_slots >= 2 * p.SUB + 2 || rope_slots == 2) break;
-    }
-  }
-  if (!GQA && lat_slots < 2 * p.SUB + 1)
-    return fail(MLRA_ERR_CONFIG, "decode: latent ring of %d slots cannot hold 2*SUB+1=%d sub-blocks", lat_slots,
-                2 * p.SUB + 1);
-  if (lat_slots > mlra::kMaxLat) lat_slots = mlra::kMaxLat;
-  if (rope_slots > mlra::kMaxRope) rope_slots = mlra::kMaxRope;
-  if (const char* e = getenv("MLRA_DEBUG_RING")) {  // dev: "lat,rope,p"
-    int a = 0, b = 0, c = 0;
-    if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && fits(a, b, c)) { lat_slots = a; rope_slots = b; p_slots = c; }
-  }
-  p.lat_slots = lat_slots;
-  p.rope_slots = rope_slots;
-  p.p_slots = p_slots;
-  const int smem = L::smem_bytes(NB, p.SUB, lat_slots, rope_slots, p_slots);
-  if (smem > kSmemBudget) return fail(MLRA_ERR_CONFIG, "decode: smem %d exceeds budget", smem);
-  auto kern = mlra::mlra_decode_kernel<T, NPAD, DLS, NB, GQA>;
-  static unsigned attr_done = 0;  // per instantiation, one bit per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 32 || !(attr_done & (1u << dev))) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) != cudaSuccess)
-      return cuda_check("cudaFuncSetAttribute(decode)");
-    if (dev < 32) attr_done |= 1u << dev;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.nsplit, p.B, head_groups);
-  cfg.blockDim = dim3(mlra::kNumThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, lat_map, rope_map, p) != cudaSuccess)
-    return cuda_check("mlra_decode_kernel launch");
-  return cuda_check("mlra_decode_kernel launch");
 }
 
 // TMA views of a pool [rows, W] bf16 (pure host descriptors, cached per thread so a decode
@@ -213,7 +104,7 @@ int pick_npad(int H, int NB, int SUB) {
 
 extern "C" {
 
-int mlra_version(void) { return 100; }
+int mlra_version(void) { return 200; }
 
 const char* mlra_last_error(void) { return g_err; }
 
@@ -318,11 +209,45 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
   return absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_out, B, H, DH, NB, DLAT, DR, score_scale, stream);
 }
 
-size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
+// Workspace of mlra_decode_step: [status word | q~ | scaled q_rope | o_part | lse_part | merge /
+// per-chunk scratch | fused-step counters], each 256-byte aligned. The status word (int32, the
+// first 4 bytes of every workspace) collects the kernels' numeric flags (mlra_check_status).
+struct WsLayout {
+  size_t q_abs, q_rope, o_part, lse, zbuf, sync, total;
+};
+
+static WsLayout ws_layout(int B, int H, int NB, int DLAT, int DR, int nsplit) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return al(size_t(B) * NB * H * DLAT * 2) + al(size_t(B) * H * (DR > 0 ? DR : 1) * 2) +
-         al(size_t(B) * nsplit * NB * H * DLAT * 4) + al(size_t(B) * nsplit * NB * H * 4) +
-         al(size_t(B) * NB * H * DLAT * 4);
+  WsLayout w;
+  size_t o = 256;  // status word
+  w.q_abs = o; o += al(size_t(B) * NB * H * DLAT * 2);
+  w.q_rope = o; o += al(size_t(B) * H * (DR > 0 ? DR : 1) * 2);
+  w.o_part = o; o += al(size_t(B) * nsplit * NB * H * DLAT * 4);
+  w.lse = o; o += al(size_t(B) * nsplit * NB * H * 4);
+  w.zbuf = o; o += al(size_t(B) * NB * H * DLAT * 4);
+  // fused-step counters: head groups <= ceil(H / 16) (the smallest head group is 16)
+  w.sync = o; o += al(mlra::fuse_sync_words(B, H, (H + 15) / 16) * 4);
+  w.total = o;
+  return w;
+}
+
+size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit) {
+  return ws_layout(B, H, NB, DLAT, DR, nsplit).total;
+}
+
+int mlra_check_status(int32_t* status, int reset, void* stream) {
+  if (status == nullptr) return fail(MLRA_ERR_CONFIG, "check_status: null status word");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t v = 0;
+  if (cudaMemcpyAsync(&v, status, sizeof v, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return cuda_check("check_status copy");
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("check_status sync");
+  if (v != 0 && reset) {
+    if (cudaMemsetAsync(status, 0, sizeof v, st) != cudaSuccess) return cuda_check("check_status reset");
+  }
+  if (v & mlra::kStatusNaN) return fail(MLRA_ERR_NUMERIC, "softmax_rows: NaN in input (status 0x%x)", v);
+  if (v & mlra::kStatusNoFinite) return fail(MLRA_ERR_NUMERIC, "softmax_rows: row with no finite entry (status 0x%x)", v);
+  return MLRA_OK;
 }
 
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
@@ -340,7 +265,7 @@ int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       bool pdl = false);
+                       bool pdl = false, const mlra::FuseArgs* fz = nullptr, int fuse_mode = 1);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
@@ -352,7 +277,7 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       bool pdl) {
+                       bool pdl, const mlra::FuseArgs* fz, int fuse_mode) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -383,6 +308,11 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
   p.pdl = pdl ? 1 : 0;
+  if (fz != nullptr) {
+    p.fused = fuse_mode;
+    p.fz = *fz;
+    p.pdl = 0;  // the fused step reads the cache and the raw queries from its first instruction
+  }
   p.rescale_threshold = mlra::kRescaleThreshold;
   if (const char* e = getenv("MLRA_DEBUG_RESCALE_THRESHOLD")) p.rescale_threshold = float(atof(e));
   if (const char* e = getenv("MLRA_DEBUG_TRACE_PTR")) p.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
@@ -466,7 +396,7 @@ static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block
 static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cudaStream_t st);
 static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
                            int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                           bool pdl, const mlra::TpSum* tp);
+                           bool pdl, const mlra::TpSum* tp, int32_t* status);
 
 // After a K3 variant without the fused TP sum: K5 on the output, in place, same region.
 static int tp_sum_after(const mlra::TpSum* tp, float* out, int n, cudaStream_t st) {
@@ -481,8 +411,9 @@ static int tp_sum_after(const mlra::TpSum* tp, float* out, int n, cudaStream_t s
 
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
                         int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                        bool pdl = false, const mlra::TpSum* tp = nullptr) {
-  if (int rc = combine_variant(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, upproj, st, pdl, tp))
+                        bool pdl = false, const mlra::TpSum* tp = nullptr, int32_t* status = nullptr) {
+  if (int rc = combine_variant(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, upproj, st, pdl, tp,
+                               status))
     return rc == 1 ? tp_sum_after(tp, out, B * H * DH, st) : rc;
   return MLRA_OK;
 }
@@ -491,7 +422,7 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
 // requested TP sum still has to run (the K3 variant has no fused sum), < 0 on error.
 static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
                            int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                           bool pdl, const mlra::TpSum* tp) {
+                           bool pdl, const mlra::TpSum* tp, int32_t* status) {
   const int tp_pending = (tp != nullptr && tp->world > 1 && upproj == 1) ? 1 : 0;
   const int rows = B * NB * H;
   const int warps_per_cta = 8;
@@ -524,7 +455,7 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha) != cudaSuccess)
+                           DH, nsplit, alpha, status) != cudaSuccess)
       return cuda_check("combine launch");
     if (int rc = cuda_check("combine launch")) return rc;
     return tp_pending;
@@ -580,18 +511,18 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
       }
     }
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha, per_branch, tps) != cudaSuccess)
+                           DH, nsplit, alpha, per_branch, tps, status) != cudaSuccess)
       return cuda_check("combine launch");
     if (int rc = cuda_check("combine launch")) return rc;
     return fused ? MLRA_OK : tp_pending;
   }
   if (upproj == 0) {
     mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
-        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1);
+        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status);
     return cuda_check("merge launch");
   }
   mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
-      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0);
+      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;
   const int kp = NB * DLAT / kparts;
@@ -613,14 +544,14 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
 }
 
 int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* scratch, int B,
-                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, void* stream) {
+                 int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, int32_t* status, void* stream) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4 || nsplit < 1 || nsplit > mlra::kMergeMaxSplits) return fail(MLRA_ERR_CONFIG, "combine: NB=%d nsplit=%d", NB, nsplit);
   if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
   if (upproj && (DH % 8 != 0)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not a multiple of 8", DH);
   if (upproj && scratch == nullptr) return fail(MLRA_ERR_CONFIG, "combine: up-projection needs a scratch buffer");
   return combine_impl(o_part, lse_part, w_uv, out, scratch, B, H, NB, DLAT, DH, nsplit, alpha, upproj,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream), false, nullptr, status);
 }
 
 static int decode_step_impl(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,
@@ -662,17 +593,105 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
                             const mlra::TpSum* tp) {
   if (B <= 0) return MLRA_OK;
   const int DLAT = SUB * DLS;
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const WsLayout wl = ws_layout(B, H, NB, DLAT, DR, nsplit);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  void* q_abs = ws;
-  ws += al(size_t(B) * NB * H * DLAT * 2);
-  void* q_rope_s = ws;
-  ws += al(size_t(B) * H * DR * 2);
-  float* o_part = reinterpret_cast<float*>(ws);
-  ws += al(size_t(B) * nsplit * NB * H * DLAT * 4);
-  float* lse_part = reinterpret_cast<float*>(ws);
-  ws += al(size_t(B) * nsplit * NB * H * 4);
-  float* zbuf = reinterpret_cast<float*>(ws);
+  int32_t* status = reinterpret_cast<int32_t*>(ws);
+  void* q_abs = ws + wl.q_abs;
+  void* q_rope_s = ws + wl.q_rope;
+  float* o_part = reinterpret_cast<float*>(ws + wl.o_part);
+  float* lse_part = reinterpret_cast<float*>(ws + wl.lse);
+  float* zbuf = reinterpret_cast<float*>(ws + wl.zbuf);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // One launch per step when the whole grid is co-resident (fused_step.cuh): K1 in K2's prologue,
+  // K3 (+ the TP sum) in its epilogue. Otherwise (or with MLRA_NO_FUSE) the three kernels below.
+  const int CW = mlra::combine_chunk_width(DLAT);
+  const bool fusable = getenv("MLRA_NO_FUSE") == nullptr && DH % 16 == 0 && DLAT % 16 == 0 && NB * DLAT % CW == 0 &&
+                       (NB * DLAT == CW || DH <= CW) && DR % 2 == 0 && (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(q_nope) & 3) == 0 &&
+                       (tp == nullptr || long(mlra::fuse_groups(B)) * H <= mlra::kArFlagSlots);
+  // Cluster step (one branch per device: an MLRA-4 / MLA TP rank): K1 and K3 inside the cluster of
+  // a sequence's split CTAs, hand-offs through DSMEM (fused_step.cuh).
+  if (getenv("MLRA_FUSE_CLUSTER") != nullptr && NB == 1 &&
+      (DH == 64 || DH == 128 || DH == 256) && DR % 2 == 0 && DR <= 64 && nsplit >= 2 && nsplit <= 16 &&
+      (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0 &&
+      (tp == nullptr || long(B) * nsplit <= mlra::kArFlagSlots)) {
+    mlra::FuseArgs f = {};
+    f.q_nope = static_cast<const __nv_bfloat16*>(q_nope);
+    f.q_rope = static_cast<const __nv_bfloat16*>(q_rope);
+    f.w_uk = static_cast<const __nv_bfloat16*>(w_uk);
+    f.w_uv = static_cast<const __nv_bfloat16*>(w_uv);
+    f.out = out;
+    f.status = status;
+    if (tp != nullptr) f.tp = *tp;
+    f.score_scale = score_scale;
+    f.alpha = alpha;
+    f.DH = DH, f.NB = NB, f.DLAT = DLAT;
+    // The cluster size is the split count of the step; the largest one <= nsplit whose B clusters
+    // are all resident at once (e.g. 16 x 9 CTAs do not fit the GPCs, 16 x 8 do). The choice
+    // depends only on the shape: cached per thread.
+    struct Pick { int B, H, DLAT, DR, nsplit, dev, ns; };
+    thread_local Pick picks[8];
+    thread_local int pick_next = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int ns = 0;
+    for (auto& e : picks)
+      if (e.nsplit == nsplit && e.B == B && e.H == H && e.DLAT == DLAT && e.DR == DR && e.dev == dev && e.ns != 0) ns = e.ns;
+    if (ns == 0) {
+      ns = -1;
+      for (int c = std::min(nsplit, 16); c >= 2 && 2 * c >= nsplit; --c) {
+        const int rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS,
+                                   DR, page_size, max_pages, num_pages, c, stream, false, &f, 2);
+        if (rc == kNotFusable) continue;
+        if (rc != MLRA_OK) return rc;
+        ns = c;
+        break;
+      }
+      picks[pick_next] = {B, H, DLAT, DR, nsplit, dev, ns};
+      pick_next = (pick_next + 1) % 8;
+      if (ns > 0) return MLRA_OK;  // launched while probing
+    } else if (ns > 0) {
+      const int rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                                 page_size, max_pages, num_pages, ns, stream, false, &f, 2);
+      if (rc != kNotFusable) return rc;
+    }
+  }
+  if (fusable && getenv("MLRA_FUSE_GRID") != nullptr) {  // dev: the grid-wide fused step
+    mlra::FuseArgs f = {};
+    f.q_nope = static_cast<const __nv_bfloat16*>(q_nope);
+    f.q_rope = static_cast<const __nv_bfloat16*>(q_rope);
+    f.w_uk = static_cast<const __nv_bfloat16*>(w_uk);
+    f.w_uv = static_cast<const __nv_bfloat16*>(w_uv);
+    f.q_abs = static_cast<__nv_bfloat16*>(q_abs);
+    f.q_rope_s = static_cast<__nv_bfloat16*>(q_rope_s);
+    f.out = out;
+    f.ybuf = zbuf;
+    f.sync = reinterpret_cast<uint32_t*>(ws + wl.sync);
+    f.status = status;
+    if (tp != nullptr) f.tp = *tp;
+    f.score_scale = score_scale;
+    f.alpha = alpha;
+    f.DH = DH, f.NB = NB, f.DLAT = DLAT;
+    f.absorb = 1;
+    f.combine = 1;
+    f.debug_reps = 1;
+    if (const char* e = getenv("MLRA_DEBUG_FUSE_REPS")) f.debug_reps = std::max(1, atoi(e));
+    f.debug_producer_wait = getenv("MLRA_DEBUG_PRODUCER_WAIT") != nullptr;
+    if (const char* e = getenv("MLRA_FUSE_PARTS")) {  // dev: "absorb" or "combine" alone
+      f.absorb = strstr(e, "absorb") != nullptr;
+      f.combine = strstr(e, "combine") != nullptr;
+    }
+    if (!f.absorb) {
+      if (int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream))
+        return rc;
+    }
+    int rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                         page_size, max_pages, num_pages, nsplit, stream, false, &f);
+    if (rc == MLRA_OK && !f.combine)
+      rc = combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, false, tp, status);
+    if (rc != kNotFusable) return rc;
+    if (!f.absorb) return fail(MLRA_ERR_CONFIG, "MLRA_FUSE_PARTS: grid not fusable");
+  }
   // K1 then K2 with programmatic dependent launch (K2's TMA producer streams the cache while
   // K1 drains -- the cache was written before K1 started -- and waits on K1 only before
   // reading the queries), then K3 in plain stream order. (K3 launched dependent on K2 measured
@@ -683,8 +702,7 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
   rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
                    max_pages, num_pages, nsplit, stream, pdl);
   if (rc) return rc;
-  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1,
-                      static_cast<cudaStream_t>(stream), false, tp);
+  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, false, tp, status);
 }
 
 int mlra_gqa_default_splits(int B, int G, int max_seqlen) {
@@ -706,9 +724,10 @@ int mlra_gqa_decode_partials(const void* q, const void* pool, const int32_t* blo
                          nsplit, score_scale, stream);
 }
 
+// GQA workspace: [status word | o_part | lse_part], 256-byte aligned.
 size_t mlra_gqa_workspace_bytes(int B, int G, int R, int DH, int nsplit) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return al(size_t(B) * nsplit * G * R * DH * 4) + al(size_t(B) * nsplit * G * R * 4);
+  return 256 + al(size_t(B) * nsplit * G * R * DH * 4) + al(size_t(B) * nsplit * G * R * 4);
 }
 
 int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_table, const int32_t* seqlens,
@@ -717,6 +736,8 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
   if (B <= 0) return MLRA_OK;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int32_t* status = reinterpret_cast<int32_t*>(ws);
+  ws += 256;
   float* o_part = reinterpret_cast<float*>(ws);
   ws += al(size_t(B) * nsplit * G * R * DH * 4);
   float* lse_part = reinterpret_cast<float*>(ws);
@@ -725,7 +746,7 @@ int mlra_gqa_decode_step(const void* q, const void* pool, const int32_t* block_t
   if (rc) return rc;
   // split merge; KV head b's query head j is output head b*R + j (out [B, G*R, DH])
   return combine_impl(o_part, lse_part, nullptr, out, nullptr, B, R, G, DH, DH, nsplit, 1.f, 0,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream), false, nullptr, status);
 }
 
 // ----------------------------------------------------------------------------- K4 (output side)

@@ -34,6 +34,7 @@
 #include <cstdint>
 #include <cmath>
 #include "ptx.cuh"
+#include "fused_step.cuh"
 
 namespace mlra {
 
@@ -60,6 +61,10 @@ struct DecodeParams {
   int nb_total;
   float qk_scale;
   int pdl;                      // host side: launch with programmatic stream serialization
+  // ---- fused step (fused_step.cuh): K1 in the prologue, K3 (+ TP sum) in the epilogue -------
+  int fused;                    // 0: partials only (K1 / K3 run as separate kernels)
+  int hgroups;                  // head groups (gridDim.z) -- completion-counter stride
+  FuseArgs fz;
 };
 
 constexpr int kNumThreads = 352;  // TMA warp, QK warp, 2 x 4 softmax warps, PV warp
@@ -83,7 +88,7 @@ struct DecodeLayout {
   static_assert(20 * NPAD * 4 <= kPBytes, "epilogue scratch must fit in one P buffer");
   static constexpr int kBarOff = ((kScratchFloats * 4 + 127) / 128) * 128;
   static constexpr int kNumBars = 2 * kMaxLat + 2 * kMaxRope + 8 + 4 + 1 + 2;
-  static constexpr int kScratchBytes = kBarOff + kNumBars * 8 + 8;
+  static constexpr int kScratchBytes = kBarOff + kNumBars * 8 + 16;  // + tmem base, debug word, TP epoch
   static int smem_bytes(int NB, int SUB, int lat_slots, int rope_slots, int p_slots) {
     const int q_chunks = NB * SUB * (DLS / 64) + 1;
     return lat_slots * kLatBytes + rope_slots * kRopeBytes + q_chunks * kQChunkBytes + p_slots * kPBytes +
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   griddep_launch_dependents();  // a dependent launch may start its prologue
+  if (p.fused == 2) cluster_arrive_relaxed();  // cluster step, phase 0: this CTA has started
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
     p.trace[13824 + 2 * cta_lin] = clock64();
@@ -217,13 +223,48 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tc_fence_after();
   }
   const uint32_t tbase = warp == 0 ? 0u : *tmem_base_sh;
+  const int ncta = gridDim.x * gridDim.y * gridDim.z;
+  const bool cm = p.fused == 2;  // cluster step (fused_step.cuh): the split CTAs of a sequence are one cluster
   if (warp != 0) {
-    // Under PDL this kernel overlaps K1's tail: the TMA producer is already streaming the
-    // cache (written before K1 started); the queries are K1's output.
-    griddep_wait();
+    if (cm) {
+      cluster_wait_acquire();  // phase 0: every CTA of the cluster runs (its shared memory may be written)
+      if (warp >= 2 && warp < 2 + kSoftThreads / 32)
+        cluster_absorb(p.fz, p.H, p.DR, DLAT, NPAD, seq, split, p.nsplit, smem_u32(q_smem), L::kQChunkBytes,
+                       NB * SUB * (DLS / 64), reinterpret_cast<float*>(p_smem), tid - 64);
+      if (tid == 64 && p.fz.tp.world > 1)  // this call's TP epoch (advanced after every CTA read it)
+        tmem_base_sh[2] = *reinterpret_cast<volatile uint32_t*>(
+                              reinterpret_cast<uint32_t*>(p.fz.tp.comm[p.fz.tp.rank] +
+                                                          ar_recv_floats(p.B * p.H * p.fz.DH, p.fz.tp.world)) +
+                              ar_flag_words(p.fz.tp.world)) + 1u;
+      cluster_arrive_release();  // phase A: the cluster's absorbed query rows are in every q buffer
+      cluster_wait_acquire();
+      fence_proxy_async_smem();  // generic-proxy (DSMEM) stores -> visible to the tensor-core reads
+    } else if (p.fused) {
+      // Fused step: the softmax warps run this CTA's share of the absorb units (K1) while the
+      // producer streams; every consumer then waits for the grid's absorbed queries.
+      if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 0] = (long long)global_ns();
+      if (p.fz.absorb) {
+        if (warp >= 2 && warp < 2 + kSoftThreads / 32)
+          fused_absorb(p.fz, p.B, p.H, p.DR, cta_lin, ncta, tid - 64, q_smem);  // stages in q / P buffers
+        if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 1] = (long long)global_ns();
+        if (tid == 64) wait_counter(p.fz.sync + kSyncAbsorb, uint32_t(absorb_units(p.B, p.H, p.fz.NB, p.fz.DLAT)));
+        if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 2] = (long long)global_ns();
+      }
+      if (tid == 64 && p.fz.tp.world > 1)  // this call's TP epoch (advanced after every final tile read it)
+        tmem_base_sh[2] = *reinterpret_cast<volatile uint32_t*>(
+                              reinterpret_cast<uint32_t*>(p.fz.tp.comm[p.fz.tp.rank] +
+                                                          ar_recv_floats(p.B * p.H * p.fz.DH, p.fz.tp.world)) +
+                              ar_flag_words(p.fz.tp.world)) + 1u;
+      named_bar_sync(5, kNumThreads - 32);
+    } else {
+      // Under PDL this kernel overlaps K1's tail: the TMA producer is already streaming the
+      // cache (written before K1 started); the queries are K1's output.
+      griddep_wait();
+    }
     // ---- absorbed + rotary queries of this (sequence, head group) -> K-major SW128 chunks.
     //      Chunk (b, c) holds latent columns [c*64, c*64+64) of branch b; the last is rope.
-    {
+    //      (cluster step: already written by the cluster's absorb)
+    if (!cm) {
       const int nlat_chunks = NB * SUB * (DLS / 64);
       const int total = q_chunks * NPAD * 8;  // 16-byte units
       for (int idx = tid - 32; idx < total; idx += kNumThreads - 32) {
@@ -257,7 +298,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // The page ids of the next 32/nbox tiles are fetched by the 32 lanes in one round trip
     // (no dependent block-table load per tile), then lane 0 issues the boxes.
     if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 0);  // producer start (len known below)
-    if (R == 0) named_bar_sync(7, 64);
+    if (R == 0) {
+      named_bar_sync(7, 64);
+      if (cm) { cluster_wait_acquire(); cluster_arrive_relaxed(); }  // phase 0 done; phase A: nothing to publish
+    }
+    if (p.fused && p.fz.debug_producer_wait && lane == 0)  // dev: no streaming until q~ is ready
+      wait_counter(p.fz.sync + kSyncAbsorb, uint32_t(absorb_units(p.B, p.H, p.fz.NB, p.fz.DLAT)));
+    __syncwarp();
     if (R > 0) {
       const uint64_t policy = l2_policy_evict_first();
       const int rope_col = NB * DLAT;
@@ -282,6 +329,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (t == 0) {
           if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 1);  // page ids of the first tiles in
           named_bar_sync(7, 64);  // mbarriers initialised by warp 1
+          if (cm) { cluster_wait_acquire(); cluster_arrive_relaxed(); }  // phase 0 done; phase A: nothing to publish
           if (lane == 0) trace_event(p.trace, p.trace_cta, 11, 2);
         }
         if (!GQA) {
@@ -649,6 +697,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_wait(o_final, 0);  // every PV done: the P buffer (lred/invl) and TMEM O are final
       tc_fence_after();
     }
+    // cluster step: O / lse of this split stay in the (now idle) ring for the cluster's merge; the
+    // W^UV rows of this CTA's heads are prefetched meanwhile
+    const int cm_heads = cm ? cluster_heads_per_cta(p.H, p.nsplit) : 0;
+    float* cm_o = reinterpret_cast<float*>(smem);                   // [NPAD][DLAT]
+    float* cm_lse = cm_o + NPAD * DLAT;                               // [NPAD]
+    __nv_bfloat16* cm_w = reinterpret_cast<__nv_bfloat16*>(cm_lse + ((NPAD + 15) / 16) * 16);  // [heads][DLAT][DH]
+    float* cm_z = reinterpret_cast<float*>(cm_w + size_t(cm_heads) * DLAT * p.fz.DH);           // [DLAT]
+    float* cm_wts = cm_z + DLAT;                                      // [16]
+    float* cm_ysum = cm_wts + 16;                                     // [256]
+    float* cm_y = cm_ysum + 256;                                      // [heads][DH]
+    if (cm) {
+      const int DH = p.fz.DH, per_head = DLAT * DH / 8;  // 16-byte chunks per head's W^UV rows
+      const uint32_t wb = smem_u32(cm_w);
+      for (int i = tid - 64; i < cm_heads * per_head; i += kSoftThreads) {
+        const int hi = i / per_head, ch = i % per_head, h = split + hi * p.nsplit;
+        if (h < p.H)
+          cp_async16(wb + uint32_t(i) * 16, p.fz.w_uv + size_t(h) * DLAT * DH + size_t(ch) * 8, 16u);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     {
       constexpr int kLive = (V >> 5) >= 1 ? (V >> 5) : 1;
 #pragma unroll
@@ -668,7 +736,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                          lred[(bb * 4 + 2) * NPAD + h] + lred[(bb * 4 + 3) * NPAD + h];
         const float m = m_run[(ws * 4 + bb) * NPAD + h];
         invl[bb * NPAD + h] = lt > 0.f ? 1.f / lt : 0.f;
-        p.lse_part[(part_row0 + bb) * p.H + hg * NPAD + h] = lt > 0.f ? m + log2f(lt) : -INFINITY;
+        // empty split (no tile, or every probability 0) -> -inf; a NaN logit leaves lt = NaN and
+        // the NaN is passed on so the merge can flag it (attnkit/tensors.py:74-75)
+        const float lse = lt > 0.f ? m + log2f(lt) : (lt == 0.f ? -INFINITY : __int_as_float(0x7fc00000));
+        if (cm) cm_lse[h] = lse;
+        else p.lse_part[(part_row0 + bb) * p.H + hg * NPAD + h] = lse;
       }
     }
     named_bar_sync(1, kSoftThreads);
@@ -720,7 +792,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int c = 0; c < kHG; ++c) o[c] = 0.f;
         }
         if (row_ok) {
-          float* dst = p.o_part + ((part_row0 + bb) * p.H + hg * NPAD + h_lo) * size_t(DLAT) + sb * DLS + row;
+          float* dst = cm ? cm_o + size_t(h_lo) * DLAT + sb * DLS + row
+                          : p.o_part + ((part_row0 + bb) * p.H + hg * NPAD + h_lo) * size_t(DLAT) + sb * DLS + row;
 #pragma unroll
           for (int c = 0; c < kHG; ++c)
             if (c < h_cnt) dst[size_t(c) * DLAT] = o[c];
@@ -728,6 +801,36 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
     }
     if (p.trace != nullptr && tid == 64 && cta_lin < 1024) p.trace[7 * 256 + 2048 + 8 * cta_lin + 5] = clock64();
+    if (cm) {
+      cluster_arrive_release();  // phase B: every split's O / lse of the sequence is in place
+      cluster_wait_acquire();
+      cp_async_wait_all();
+      named_bar_sync(1, kSoftThreads);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 3] = (long long)global_ns();
+      cluster_combine(p.fz, p.B, p.H, DLAT, NPAD, seq, split, p.nsplit, cm_o, cm_lse, cm_w, cm_z, cm_wts, cm_ysum, cm_y,
+                      tid - 64, tmem_base_sh[2]);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 4] = (long long)global_ns();
+      cluster_arrive_release();  // phase C: the cluster's DSMEM reads of this CTA are done
+      cluster_wait_acquire();
+    } else if (p.fused) {
+      // publish this split's partials (barrier + one cumulative release), then this CTA's share
+      // of the K3 units
+      named_bar_sync(1, kSoftThreads);
+      if (tid == 64) red_release_add(p.fz.sync + kSyncSeq + size_t(seq) * p.hgroups + hg, 1u);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 3] = (long long)global_ns();
+      if (p.fz.combine)
+        fused_combine(p.fz, p.o_part, p.lse_part, p.B, p.H, p.nsplit, smem, cta_lin, ncta, tid - 64, tmem_base_sh[2],
+                      cta_lin == p.trace_cta ? p.trace : nullptr);
+      if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 4] = (long long)global_ns();
+    }
+  }
+  if (cm && (warp < 2 || warp == kPvWarp)) {
+    // the producer and MMA warps take part in every cluster phase (barrier.cluster counts all threads)
+    if (warp == 0) cluster_wait_acquire();  // phase A (arrived at its start)
+    cluster_arrive_release();               // phase B
+    cluster_wait_acquire();
+    cluster_arrive_release();               // phase C
+    cluster_wait_acquire();
   }
   tc_fence_before();
   if (p.trace != nullptr && warp >= 2) atomicAdd(&tmem_base_sh[1], 1u);
@@ -739,6 +842,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tbase);
+  }
+  if (p.fused == 1 && tid == 0) {
+    // the last CTA out resets the step's counters for the next stream-ordered launch (visible to
+    // it at the kernel boundary)
+    if (atom_acq_rel_add(p.fz.sync + kSyncExit, 1u) == uint32_t(ncta - 1)) {
+      const size_t nw = fuse_sync_words(p.B, p.H, p.hgroups);
+      for (size_t i = 0; i < nw; ++i) p.fz.sync[i] = 0u;
+    }
   }
 }
 

@@ -233,7 +233,10 @@ def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, own: 
     q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, nb, dlat, ops.score_scale(cfg.tau))
     o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, pc.block_table, pc.seqlens, pc.page_size, nb, sub, dls,
                                       nsplit)
-    return ops.combine(o_part, lse, w_uv, alpha, per_branch=(upproj == 2))
+    status = ops.status_word(dev)
+    out = ops.combine(o_part, lse, w_uv, alpha, per_branch=(upproj == 2), status=status)
+    ops.check_status(status, "softmax_rows")  # NaN / no finite logit -> NumericError (tensors.py:74-78)
+    return out
 
 
 def attend_local(cfg: AttnConfig, local_w, own: Ownership, cache: PagedLatentCache, queries: dict) -> list:
@@ -516,6 +519,12 @@ class DecodeEngine:
                                   c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
                                   self.workspace, reducer.rank, reducer.world, reducer.ptrs,
                                   out=self.out if out is None else out, comm_n=reducer.n)
+
+    def check_numeric(self) -> None:
+        """Synchronise, read and reset the workspace's status word: NumericError when any step since
+        the last check saw a NaN logit or a row with no finite logit (attnkit/tensors.py:74-78). The
+        decode call itself never synchronises (serving loops replay it from CUDA graphs)."""
+        ops.check_status(self.workspace.status, "softmax_rows")
 
     def decode_attention(self, q_nope: torch.Tensor, q_rope: torch.Tensor, out: torch.Tensor | None = None):
         """One decode-attention step over the cache: bf16 [B, h_local, d_h] / [B, h_local, drp]

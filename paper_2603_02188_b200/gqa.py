@@ -78,6 +78,7 @@ def attend_local_gqa(cfg: AttnConfig, own, cache: PagedLatentCache, queries: dic
     nsplit = ops.gqa_default_splits(1, G, max(cache.n, 1))
     ws = ops.GqaWorkspace(1, G, R, layout.dhp, nsplit, pc.device)
     out = ops.gqa_decode_step(q, pc.pool, pc.block_table, pc.seqlens, pc.page_size, nsplit, score_scale(cfg), ws)
+    ops.check_status(ws.status, "softmax_rows")  # NaN / no finite logit -> NumericError (tensors.py:74-78)
     cache.reads += cache.n * cache.row_elements()
     vecs = out[0, :, :cfg.d_h].double().cpu().numpy()
     return [(head, vecs[j]) for j, head in enumerate(own.heads)]
@@ -114,6 +115,10 @@ class GqaDecodeEngine:
     def prepare_queries(self, q) -> torch.Tensor:
         """[B, h, d_h] (any float, host or device) -> this device's [B, G, R, dhp] bf16."""
         return queries_to_device(self.cfg, self.layout, q, self.heads, self.G, self.R, self.device)
+
+    def check_numeric(self) -> None:
+        """NumericError if any step since the last check flagged a NaN / non-finite softmax row."""
+        ops.check_status(self.workspace.status, "softmax_rows")
 
     def decode_attention(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """One decode-attention step: [B, G, R, dhp] bf16 -> fp32 [B, h_local, d_h] (a view

@@ -57,7 +57,10 @@ class _Slot:
 class MicroBatchLoop:
     """Micro-batches of one device stepped in turn with overlapped host<->device copies."""
 
-    def __init__(self, engines):
+    def __init__(self, engines, reducer=None):
+        """reducer: collective.PeerAllReduce of the engines' TP group (B*h*d_h values): every step
+        then runs ``decode_attention_tp`` (the sum over the group fused into K3), so the result
+        downloaded is the full TP output. All ranks must submit the same micro-batch sequence."""
         if not engines:
             raise ConfigError("MicroBatchLoop needs at least one engine")
         dev = engines[0].device
@@ -67,6 +70,7 @@ class MicroBatchLoop:
         self.slots = [_Slot(e) for e in engines]
         self.up = torch.cuda.Stream(device=dev)
         self.down = torch.cuda.Stream(device=dev)
+        self.reducer = reducer
 
     def __len__(self) -> int:
         return len(self.slots)
@@ -98,7 +102,10 @@ class MicroBatchLoop:
             s.up_done.record(self.up)
         main.wait_event(s.up_done)
         main.wait_event(s.down_done)  # the output buffer has been drained
-        out = eng.decode_attention(qn, qr)
+        if self.reducer is not None:
+            out = eng.decode_attention_tp(qn, qr, self.reducer)
+        else:
+            out = eng.decode_attention(qn, qr)
         s.step_done.record(main)
         self.down.wait_event(s.step_done)
         with torch.cuda.stream(self.down):

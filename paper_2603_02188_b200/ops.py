@@ -132,10 +132,30 @@ def decode_partials(q_abs: torch.Tensor, q_rope: torch.Tensor, pool: torch.Tenso
     return o_part, lse_part
 
 
+_STATUS: dict = {}
+
+
+def status_word(device) -> torch.Tensor:
+    """Per-device int32 numeric status word for the stand-alone K3 calls (``combine``)."""
+    key = str(torch.device(device))
+    if key not in _STATUS:
+        _STATUS[key] = torch.zeros(1, dtype=torch.int32, device=device)
+    return _STATUS[key]
+
+
+def check_status(status: torch.Tensor, what: str = "decode") -> None:
+    """Synchronise the current stream, read and reset a status word; NumericError if the merge
+    flagged a NaN logit or a row with no finite logit (attnkit/tensors.py:74-78)."""
+    rc = _lib.load().mlra_check_status(status.data_ptr(), 1, _stream())
+    _lib.check(rc, what)
+
+
 def combine(o_part: torch.Tensor, lse_part: torch.Tensor, w_uv_packed: torch.Tensor | None, alpha: float,
-            out: torch.Tensor | None = None, per_branch: bool = False, scratch: torch.Tensor | None = None):
+            out: torch.Tensor | None = None, per_branch: bool = False, scratch: torch.Tensor | None = None,
+            status: torch.Tensor | None = None):
     """K3: merge splits; with w_uv_packed [H, NB*DLAT, DH] also up-project (summing branches,
-    or per branch when ``per_branch``)."""
+    or per branch when ``per_branch``). Numeric flags go to ``status`` (default: the device's
+    status word, see ``check_status``)."""
     _need(o_part, torch.float32, "o_part", 5)
     _need(lse_part, torch.float32, "lse_part", 4)
     B, nsplit, NB, H, DLAT = o_part.shape
@@ -157,7 +177,8 @@ def combine(o_part: torch.Tensor, lse_part: torch.Tensor, w_uv_packed: torch.Ten
     rc = _lib.load().mlra_combine(o_part.data_ptr(), lse_part.data_ptr(),
                                   w_uv_packed.data_ptr() if mode else None, out.data_ptr(),
                                   scratch.data_ptr() if mode else None, B, H, NB, DLAT, DH, nsplit, float(alpha),
-                                  mode, _stream())
+                                  mode, (status if status is not None else status_word(o_part.device)).data_ptr(),
+                                  _stream())
     _lib.check(rc, "mlra_combine")
     return out
 
@@ -168,7 +189,8 @@ class DecodeWorkspace:
     def __init__(self, batch: int, heads: int, nb: int, dlat: int, dr: int, nsplit: int, device):
         nbytes = _lib.load().mlra_workspace_bytes(batch, heads, nb, dlat, dr, nsplit)
         self.key = (batch, heads, nb, dlat, dr, nsplit)
-        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # barrier state must start at 0
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # counters and status start at 0
+        self.status = self.buf[:4].view(torch.int32)  # numeric status word (include/mlra_b200.h)
 
 
 def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
@@ -256,7 +278,8 @@ class GqaWorkspace:
     def __init__(self, batch: int, kv_heads: int, reps: int, dh: int, nsplit: int, device):
         nbytes = _lib.load().mlra_gqa_workspace_bytes(batch, kv_heads, reps, dh, nsplit)
         self.key = (batch, kv_heads, reps, dh, nsplit)
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        self.status = self.buf[:4].view(torch.int32)  # numeric status word
 
 
 def gqa_decode_step(q: torch.Tensor, pool: torch.Tensor, block_table: torch.Tensor, seqlens: torch.Tensor,

@@ -52,7 +52,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_cpu_safe_calls(lib):
-    assert lib.mlra_version() == 100
+    assert lib.mlra_version() == 200
     assert lib.mlra_workspace_bytes(16, 24, 4, 128, 64, 9) > 16 * 9 * 4 * 24 * 128 * 4
     # argument validation happens before any CUDA call
     rc = lib.mlra_decode_partials(None, None, None, None, None, None, None, 1, 24, 3, 1, 128, 64, 128, 1, 1, 1, None)
@@ -63,8 +63,10 @@ def test_cpu_safe_calls(lib):
     assert rc == -2 and b"page_size" in lib.mlra_last_error()
     rc = lib.mlra_cache_append(None, None, None, 1, 7, 64, 1, 1, None, None)
     assert rc == -1 and b"row width" in lib.mlra_last_error()
-    rc = lib.mlra_combine(None, None, None, None, None, 1, 1, 1, 128, 128, 1, 1.0, 3, None)
+    rc = lib.mlra_combine(None, None, None, None, None, 1, 1, 1, 128, 128, 1, 1.0, 3, None, None)
     assert rc == -2
+    rc = lib.mlra_check_status(None, 1, None)
+    assert rc == -2 and b"null status" in lib.mlra_last_error()
     with pytest.raises(_lib.ConfigError):
         _lib.check(-2, "probe")
 

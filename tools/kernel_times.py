@@ -37,4 +37,15 @@ for name, cfg, own in cases:
     t2 = gtime(lambda: ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub, eng.dls, eng.nsplit, out=parts))
     t3 = gtime(lambda: ops.combine(*parts, eng.w_uv, eng.alpha, out=out, scratch=scratch))
     tstep = gtime(lambda: eng.decode_attention(qn, qr))
-    print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  step {tstep:.1f} us  (graph replay, K2 back-to-back on one cache: L2-warm)", flush=True)
+    import os
+    os.environ["MLRA_NO_FUSE"] = "1"
+    tstep3 = gtime(lambda: eng.decode_attention(qn, qr))
+    del os.environ["MLRA_NO_FUSE"]
+    parts = {}
+    for part in ("absorb", "combine"):
+        os.environ["MLRA_FUSE_PARTS"] = part
+        parts[part] = gtime(lambda: eng.decode_attention(qn, qr))
+        del os.environ["MLRA_FUSE_PARTS"]
+    print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  fused step {tstep:.1f} us  "
+          f"3-kernel step {tstep3:.1f} us  fused absorb only (+K3) {parts['absorb']:.1f}  fused combine only (K1+) "
+          f"{parts['combine']:.1f}  (graph replay, one cache: L2-warm)", flush=True)
