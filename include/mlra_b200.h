@@ -88,9 +88,8 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
                       int H, int DH, int NB, int DLAT, int DR, float score_scale, void* stream);
 
 /* Bytes of device workspace mlra_decode_step / mlra_decode_step_tp need: the numeric status word,
- * the absorbed queries, the split-KV partials, the merge / per-chunk scratch and the fused step's
- * completion counters. Zero-fill it once before first use; every launch leaves the counters at
- * zero again (the last CTA of the fused step resets them). */
+ * the absorbed queries, the split-KV partials, the merge scratch (and the counters of the
+ * dev-only fused experiments). Zero-fill it once before first use. */
 size_t mlra_workspace_bytes(int B, int H, int NB, int DLAT, int DR, int nsplit);
 
 /*
@@ -141,12 +140,13 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * One decode-attention step for a batch: K1 (absorb) + K2 (split-KV decode) + K3 (merge, W^UV,
  * ascending branch sum, alpha). Replaces decode.py:304-305 (attend_local + reduce_contributions
  * inside absorbed_decode_step) for every unit a device owns.
- * When the K2 grid (nsplit x B x head groups) is co-resident (one CTA per SM, grid <= #SMs) it
- * is ONE launch: the absorption runs in K2's prologue while the TMA producer already streams the
- * cache, and the merge / up-projection in its epilogue, gated per sequence by completion
- * counters in the workspace (fused_step.cuh). Otherwise K1, K2 and K3 run as three kernels in
- * stream order (K2 programmatically dependent on K1). MLRA_NO_FUSE=1 forces the three-kernel
- * path, MLRA_NO_PDL=1 plain stream order for it.
+ * Launches: K1, then K2 as a programmatic dependent of K1 (K2's TMA producer streams the cache
+ * while K1 drains; its consumers wait for the absorbed queries), then K3 in plain stream order.
+ * No completion counters are used on this path. MLRA_NO_PDL=1 launches K2 in plain stream order.
+ * (Dev experiments, off unless their environment switch is set, both measured slower:
+ * MLRA_FUSE_GRID -- one launch with K1 / K3 inside K2 behind grid-wide counters in the
+ * workspace; MLRA_FUSE_CLUSTER -- one launch with K1 / K3 inside the cluster of a sequence's
+ * split CTAs, DSMEM hand-offs; fused_step.cuh.)
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  *   nsplit in [1, 160] (mlra_default_splits: one wave of the SMs for this batch)
  */

@@ -290,8 +290,12 @@ def unit_weights(cfg: Cfg, w: dict, group: int, block: int, heads) -> tuple:  # 
     return (w_uk.reshape(d_lat, -1, cfg.d_h)[:, local], w_uv.reshape(d_lat, -1, cfg.d_h)[:, local])
 
 
-def attend_latent(cfg: Cfg, w: dict, cache: Cache, q_nope, q_rope, unit_list) -> list:
-    """attend_local, latent branch (attnkit/decode.py:217-230)."""
+def attend_latent(cfg: Cfg, w: dict, cache: Cache, q_nope, q_rope, unit_list, q_operand_scale=None) -> list:
+    """attend_local, latent branch (attnkit/decode.py:217-230).
+
+    q_operand_scale (test emulation only, default off): when set to s, the absorbed query and
+    the rotary query enter the logits as bf16(q * s) / s -- the bf16 operands the B200 K1 hands
+    K2 (the score scale s = tau*log2(e) folded in before the bf16 rounding)."""
     rope_hist = cache.read("rope")
     contribs = []
     for stream, group, block, heads in unit_list:
@@ -299,7 +303,11 @@ def attend_latent(cfg: Cfg, w: dict, cache: Cache, q_nope, q_rope, unit_list) ->
         uk, uv = unit_weights(cfg, w, group, block, heads)
         hl = list(heads)
         q_tilde = absorb_query(q_nope[hl], uk)
-        logits = cfg.tau * (q_tilde @ latent_hist.T + q_rope[hl] @ rope_hist.T)
+        q_r = q_rope[hl]
+        if q_operand_scale is not None:
+            q_tilde = bf16_round(q_tilde * q_operand_scale) / q_operand_scale
+            q_r = bf16_round(q_r * q_operand_scale) / q_operand_scale
+        logits = cfg.tau * (q_tilde @ latent_hist.T + q_r @ rope_hist.T)
         probs = softmax_rows(logits)
         mixed = probs @ latent_hist
         out = np.einsum("mc,cmp->mp", mixed, uv)
@@ -334,11 +342,13 @@ def reduce_contributions(cfg: Cfg, contribs: list) -> tuple:  # attnkit/decode.p
     return out, kind
 
 
-def decode_attention(cfg: Cfg, w: dict, streams: dict, q_nope: np.ndarray, q_rope: np.ndarray) -> np.ndarray:
+def decode_attention(cfg: Cfg, w: dict, streams: dict, q_nope: np.ndarray, q_rope: np.ndarray,
+                     q_operand_scale=None) -> np.ndarray:
     """Steps 1-3 of absorbed decoding for one sequence over a complete cache (no append):
-    the quantity the B200 K1+K2+K3 path computes. streams: latent stream(s) + 'rope'."""
+    the quantity the B200 K1+K2+K3 path computes. streams: latent stream(s) + 'rope'.
+    q_operand_scale: see attend_latent (bf16 query operands, test emulation)."""
     cache = Cache(dict(streams))
-    out, _ = reduce_contributions(cfg, attend_latent(cfg, w, cache, q_nope, q_rope, units(cfg)))
+    out, _ = reduce_contributions(cfg, attend_latent(cfg, w, cache, q_nope, q_rope, units(cfg), q_operand_scale))
     return out
 
 

@@ -35,7 +35,7 @@ def __getattr__(name):
         "local_weights": ("decode", "local_weights"), "attend_local": ("decode", "attend_local"),
         "reduce_contributions": ("decode", "reduce_contributions"),
         "absorbed_decode_step": ("decode", "absorbed_decode_step"), "decode_step": ("decode", "decode_step"),
-        "DecodeEngine": ("decode", "DecodeEngine"),
+        "naive_decode_step": ("decode", "naive_decode_step"), "DecodeEngine": ("decode", "DecodeEngine"),
         "shard_ownership": ("tp", "shard_ownership"), "make_shards": ("tp", "make_shards"),
         "sim_decode": ("tp", "sim_decode"), "ShardSet": ("tp", "ShardSet"), "DeviceShard": ("tp", "DeviceShard"),
         "TrafficLedger": ("tp", "TrafficLedger"), "TPDecodeGroup": ("tp", "TPDecodeGroup"),

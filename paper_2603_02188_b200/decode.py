@@ -453,12 +453,25 @@ def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t
     return out
 
 
+def naive_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tuple[np.ndarray, PagedLatentCache]:
+    """The reference's materialising decode (decode.py:309-338), same contract: latent family
+    only (RoutingError otherwise), cache append, per-head softmax over the prefix, alpha_attn.
+
+    On the B200 the per-head keys/values C·W^UK_h, C·W^UV_h are never materialised: the logits
+    q_h·(C W^UK_h)^T equal (q_h W^UK_h^T)·C^T and the output P·(C W^UV_h) equals (P·C)·W^UV_h
+    exactly in real arithmetic, so this runs the absorbed K0-K3 path (in float64 the
+    reference's two forms agree to 1e-10; tests/test_oracle.py). Reads are accounted like the
+    reference (every owned latent stream and the rope once)."""
+    if cfg.variant not in LATENT_VARIANTS:
+        raise RoutingError(f"naive_decode_step covers the latent family; {cfg.variant!r} decodes directly")
+    return absorbed_decode_step(cfg, w, cache, h_t)
+
+
 def decode_step(cfg: AttnConfig, w, cache, h_t, mode: str = "absorbed"):  # decode.py:341-348
     if mode == "absorbed":
         return absorbed_decode_step(cfg, w, cache, h_t)
     if mode == "naive":
-        raise RoutingError("naive decode (per-head K/V materialisation) is the CPU oracle's job; "
-                           "the B200 path implements the absorbed form only")
+        return naive_decode_step(cfg, w, cache, h_t)
     raise RoutingError(f"unknown decode mode {mode!r}")
 
 

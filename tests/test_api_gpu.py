@@ -46,6 +46,28 @@ def test_decode_steps_track_reference(name):
     assert ak.max_rel_err(arrays["out_absorbed"], out) <= TOL
 
 
+@pytest.mark.parametrize("name", ["tiny_mlra4", "refdims_mla", "p_mlra4"])
+def test_decode_step_naive_mode(name):
+    """decode_step(mode="naive") (attnkit/decode.py:341-348 -> :309-338) returns the reference's
+    materialised-KV result: the GPU evaluates it through absorption (equal in exact
+    arithmetic), so it matches the golden out_naive within the bf16 tolerance, and the cache
+    grows and is accounted like the absorbed step's."""
+    mlra = _mlra()
+    meta, arrays = load(name)
+    ocfg, w, hidden = regen(meta)
+    cfg = mlra.AttnConfig(**meta["cfg"])
+    n = meta["n"]
+    cache = mlra.new_cache(cfg)
+    ocache = ak.Cache(ak.latent_streams(ocfg, w, hidden[: n - 1]))
+    rows = cache.layout.pack_rows(ocache.streams, device="cuda:0")
+    cache.paged.fill(rows[None], [n - 1])
+    out, cache = mlra.decode_step(cfg, w, cache, hidden[n - 1], mode="naive")
+    assert cache.n == n
+    assert ak.max_rel_err(arrays["out_naive"], out) <= TOL
+    with pytest.raises(mlra.errors.RoutingError):
+        mlra.decode_step(cfg, w, cache, hidden[n - 1], mode="fused")
+
+
 def test_read_accounting_and_append_only():
     """tests/test_decode.py:133-160: each step reads the whole state once; rows are frozen."""
     mlra = _mlra()
