@@ -112,7 +112,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workloads
-def make_engine(cfg, own, batch, ctx, seed, device, page_size=128):
+def make_engine(cfg, own, batch, ctx, seed, device, page_size=128, weights=None):
     """DecodeEngine with a synthetic cache filled on the device (RMS like the reference's rows)."""
     import torch
 
@@ -121,7 +121,9 @@ def make_engine(cfg, own, batch, ctx, seed, device, page_size=128):
 
     g = torch.Generator(device=device).manual_seed(seed)
     rng = np.random.default_rng(seed)
-    if cfg.variant == "gla" or (cfg.variant == "mlra" and cfg.branches == 2):  # per-group up-projections
+    if weights is not None:
+        w = weights
+    elif cfg.variant == "gla" or (cfg.variant == "mlra" and cfg.branches == 2):  # per-group up-projections
         r, dg = cfg.h // cfg.g, cfg.d_c // cfg.g
         w = {f"{n}_{j}": rng.standard_normal((dg, r * cfg.d_h)) * 0.02 for n in ("w_uk", "w_uv") for j in range(cfg.g)}
     else:
@@ -766,9 +768,125 @@ def per_gpu_comparisons(cfg, device, args):
                                                       res["mlra4_tp4_rank"]["us_per_step"], 3),
         "traffic_ratio_gqa_tp2_rank_vs_mlra4_tp4_rank": 4.0,
     }
+    out["layer"] = layer_times(device, args)
     out["output_side"] = output_side_times(device)
     out["prefill"] = prefill_times(device)
     return out
+
+
+def make_layer_engine(cfg, own, batch, ctx, seed, device, page_size=128):
+    """DecodeEngine with the FULL weight set of the layer (weights.py shapes, sigma 0.02: the
+    projections as well as W^UK / W^UV) and a synthetic cache of ctx tokens, plus the new
+    tokens' hidden rows [B, d] ~ N(0, 1) for decode_layer."""
+    import torch
+
+    from paper_2603_02188_b200.weights import weight_shapes
+
+    rng = np.random.default_rng(seed)
+    w = {name: rng.standard_normal(shape) * 0.02 for name, shape in weight_shapes(cfg).items()}
+    eng, _, _ = make_engine(cfg, own, batch, ctx, seed, device, page_size=page_size, weights=w)
+    g = torch.Generator(device=device).manual_seed(seed + 1)
+    hidden = torch.randn((batch, cfg.d), generator=g, device=device)
+    return eng, hidden
+
+
+def layer_times(device, args):
+    """The attention layer from the hidden rows (the paper's end-to-end decode scope: pre-attention
+    plus attention), B = 16, 32K, per GPU: K-1 down -> K0 -> K-1 query -> [K1] ->
+    K2 -> K3 (hand-written K-1; the TP4 rank's query kernel writes q~ with W^UQ.W^UK_b
+    pre-multiplied, so K1 is skipped), against the same step with the projections as torch
+    bf16 cuBLAS GEMMs + rmsnorm / rope ops (K0-K3 unchanged). Two engines alternate (L2-cold
+    caches and weights); the timing loop rewrites the appended slot (advance=False), so the
+    attended length stays ctx."""
+    import torch
+
+    from paper_2603_02188_b200 import ops
+    from paper_2603_02188_b200.config import trained_config
+    from paper_2603_02188_b200.projections import rope_rotate
+    from paper_2603_02188_b200.tp import shard_ownership
+
+    def gtime(fns, reps=20):
+        for f in fns:
+            f()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(10):
+                fns[i % len(fns)]()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / 10 * 1e3
+
+    cfg = trained_config("mlra4")
+    res = {}
+    for name, own in (("mlra4_tp4_rank", shard_ownership(cfg, 4, 0)), ("mlra4_tp1", None)):
+        engs = [make_layer_engine(cfg, own, BATCH_PER_GROUP, CTX, 11 + i, device) for i in range(2)]
+        for eng, _ in engs:
+            eng.kernel_projector(None)
+        kp = engs[0][0].kernel_projector(None)
+
+        def layer(i):
+            eng, hid = engs[i]
+            return lambda: eng.decode_layer(hid, advance=False)
+
+        def proj(i):
+            eng, hid = engs[i]
+            k = eng.kernel_projector(None)
+
+            def f():
+                k.down(hid)
+                k.query(hid.shape[0], eng.cache.seqlens)
+            return f
+
+        def attn(i):
+            eng, hid = engs[i]
+            qn = torch.randn((BATCH_PER_GROUP, len(eng.heads), cfg.d_h), device=device).to(torch.bfloat16)
+            qr = torch.zeros((BATCH_PER_GROUP, len(eng.heads), eng.layout.drp), dtype=torch.bfloat16, device=device)
+            return lambda: eng.decode_attention(qn, qr)
+
+        def torch_layer(i):
+            eng, hid = engs[i]
+            k = eng.kernel_projector(False)  # q_nope weights (W^UQ) for the cuBLAS query GEMM
+            c = eng.cache
+            from paper_2603_02188_b200.decode import _write_plan
+            _, blocks, block0, nblocks, ng = _write_plan(cfg, eng.own)
+            pos = c.seqlens.long()
+
+            def f():
+                y = torch.mm(hid.to(torch.bfloat16), k.w_down, out_dtype=torch.float32)
+                cq = y[:, :k.n_q]
+                kv, kr = y[:, k.n_q:k.n_q + k.n_kv].contiguous(), y[:, k.n_q + k.n_kv:k.n_q + k.n_kv + k.n_kr].contiguous()
+                ops.cache_append_latent(kv, kr, None, c.seqlens, c.block_table, c.pool, c.page_size, branches=blocks,
+                                        block0=block0, nblocks=nblocks, dlp=eng.layout.dlp, drp=eng.layout.drp,
+                                        alpha_kv=k.alpha_kv, norm_groups=ng, advance=False)
+                cq = k.alpha_q * cq * torch.rsqrt((cq * cq).mean(-1, keepdim=True) + 1e-6)
+                q = torch.mm(cq.to(torch.bfloat16), k.w_query, out_dtype=torch.float32)
+                qn = q[:, :k.nq].reshape(-1, k.H, cfg.d_h).to(torch.bfloat16)
+                qr = torch.zeros((qn.shape[0], k.H, eng.layout.drp), dtype=torch.bfloat16, device=device)
+                qr[..., :k.dr] = rope_rotate(q[:, k.nq:k.nq + k.H * k.dr].reshape(-1, k.H, k.dr), pos).to(torch.bfloat16)
+                eng.decode_attention(qn, qr)
+            return f
+
+        t_layer = gtime([layer(0), layer(1)])
+        t_proj = gtime([proj(0), proj(1)])
+        t_attn = gtime([attn(0), attn(1)])
+        t_torch = gtime([torch_layer(0), torch_layer(1)])
+        wbytes = (kp.w_down.numel() + kp.w_query.numel()) * 2  # algorithmic: the unpadded weights
+        res[name] = {"layer_us": round(t_layer, 2), "k_minus1_us": round(t_proj, 2),
+                     "k_minus1_weight_bytes": wbytes, "k_minus1_gbs": round(wbytes / (t_proj * 1e-6) / 1e9, 1),
+                     "attention_step_us": round(t_attn, 2), "layer_torch_projections_us": round(t_torch, 2),
+                     "query_preabsorbed": bool(kp.absorbed)}
+        del engs
+        torch.cuda.empty_cache()
+    return res
 
 
 def prefill_times(device):

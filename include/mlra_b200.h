@@ -68,7 +68,8 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* pos
  *   pool row [c_kv blocks | k_rope] bf16 written at slot slots[s] of sequence s.
  *   kv_raw [B, d_c] fp32 = h W^DKV (whole groups: the RMS spans a group's blocks), kr_raw
  *   [B, dr] fp32 = h W^KR. MLA: branches = 1. advance != 0: slots[s] += 1 after the write
- *   (slots are then the sequence lengths, as in mlra_cache_append).
+ *   (slots are then the sequence lengths, as in mlra_cache_append). rope_pos == NULL: the rope
+ *   position is the slot written (a cache holding positions 0..n-1).
  */
 int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, int32_t* slots,
                              const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
@@ -149,6 +150,10 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * split CTAs, DSMEM hand-offs; fused_step.cuh.)
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  *   nsplit in [1, 160] (mlra_default_splits: one wave of the SMs for this batch)
+ *   w_uk == NULL: the queries arrive absorbed -- q_nope is q~ [B, NB, H, DLAT] and q_rope the
+ *   rotary query, both already scaled by score_scale (mlra_proj_query with the pre-multiplied
+ *   W^UQ.W^UK_b weight) -- and the step is K2 (programmatic dependent of the caller's previous
+ *   kernel) + K3.
  */
 int mlra_decode_step(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv, const void* pool,
                      const int32_t* block_table, const int32_t* seqlens, float* out, void* workspace, int B, int H,
@@ -237,6 +242,41 @@ int mlra_comm_free(void* dev_ptr);
 int mlra_ipc_handle(const void* dev_ptr, void* handle_out);
 int mlra_ipc_open(const void* handle, void** dev_ptr_out);
 int mlra_ipc_close(void* dev_ptr);
+
+/*
+ * K-1 -- pre-attention projections: the GEMVs of latent.py:129-159
+ * (latent_projections) for a decode batch, as two weight-streaming GEMM launches (M <= 16
+ * rows per launch; larger M loops). Weights are bf16 and SLAB-PACKED once at load time: a
+ * weight W [K, N] (row-major (in, out) as weights.py stores it) is passed as
+ * [ceil(N/64)][round_up(K, 64)][64] with element [s][k][c] = W[k][64 s + c] (zero outside W), so
+ * each CTA's slice is one contiguous HBM run. Activations enter as fp32 (split into bf16 hi +
+ * lo operands: ~16-bit mantissa); fp32 accumulation; the K slices of an output slab are summed
+ * in a fixed order.
+ *
+ * mlra_proj_down: y = x . w, x [M, K] fp32 (the hidden rows h), w = slab pack of
+ *   [W^DQ | W^DKV (every latent group, concatenated) | W^KR]  (N = n_q + n_kv + n_kr columns)
+ *   c_q_raw [M, n_q] = h W^DQ, kv_raw [M, n_kv] = h W^DKV (mlra_cache_append_latent's input),
+ *   kr_raw [M, n_kr] = h W^KR  (fp32; any output may be NULL)
+ *   ssq [ceil(n_q/64)][M] fp32 (or NULL): partial sums of squares of c_q_raw's rows, per 64
+ *   columns -- the query rmsnorm's statistics for mlra_proj_query (M <= 16 when given).
+ * mlra_proj_query: c_q = alpha_q * c_q_raw / sqrt(mean(c_q_raw^2) + eps) (tensors.py:83-87; the
+ *   mean from ssq), then [q_x | q_r] = c_q . w with w = slab pack of [W^Q | W^QR] (nq + H*dr
+ *   columns):
+ *   q_out [M, nq] bf16 = q_scale * q_x. W^Q = W^UQ (q_nope, for K1) or, for a device holding
+ *     NB latent blocks of DLAT columns, the pre-multiplied W^UQ_(h) . W^UK_(b),(h)^T columns in
+ *     (b, h, c) order: q_out is then K1's q_abs [M, NB, H, DLAT] and K1 is skipped.
+ *   r_out [M, H, drp] bf16 = r_scale * rope(q_r, pos[m] + pos_delta) (rope.py:37-60: pairs (2l, 2l+1),
+ *     theta_l = rope_base^(-2l/dr)); columns [dr, drp) are not written (zero them once).
+ *     (pos_delta = -1 with pos = the sequence lengths after mlra_cache_append_latent advanced
+ *     them: the position of the token just appended.)
+ * Both launch as programmatic dependents of the previous kernel on the stream (the weight
+ * stream starts before it finishes) and release their own dependents only after that wait.
+ */
+int mlra_proj_down(const float* x, const void* w, int M, int K, int n_q, int n_kv, int n_kr, float* c_q_raw,
+                   float* kv_raw, float* kr_raw, float* ssq, void* stream);
+int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float eps, const void* w, int M, int K,
+                    int nq, int H, int dr, int drp, const int32_t* pos, int pos_delta, float rope_base, float q_scale, float r_scale,
+                    void* q_out, void* r_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,8 @@ SIGNATURES = {
     "mlra_ipc_handle": (_I, [_P, _P]),
     "mlra_ipc_open": (_I, [_P, _P]),
     "mlra_ipc_close": (_I, [_P]),
+    "mlra_proj_down": (_I, [_P, _P] + [_I] * 5 + [_P] * 5),
+    "mlra_proj_query": (_I, [_P, _P, _F, _F, _P] + [_I] * 6 + [_P, _I, _F, _F, _F, _P, _P, _P]),
 }
 
 _CODES = {-1: ShapeMismatchError, -2: ConfigError, -3: NumericError, -4: CudaError}

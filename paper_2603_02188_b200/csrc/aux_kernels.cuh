@@ -100,7 +100,7 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
     const float v = c < bs ? kv[col] * gscale[col / gw] : 0.f;
     dst[i] = __float2bfloat16(v);
   }
-  const double pos = double(rope_pos[s]);
+  const double pos = double(rope_pos != nullptr ? rope_pos[s] : slot);  // NULL: the slot written
   const float* kr = kr_raw + size_t(s) * dr;
   for (int l = tid; l < drp / 2; l += kK0Threads) {
     float e = 0.f, o = 0.f;

@@ -24,19 +24,6 @@ using namespace mlra_host;
 
 namespace {
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 // TMA views of a pool [rows, W] bf16 (pure host descriptors, cached per thread so a decode
 // loop over the same pool does not re-encode them every step):
 //   lat  = 3-D {64 columns, rows, nlat 64-column chunks} (chunk stride 128 B), box
@@ -602,6 +589,14 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
   float* lse_part = reinterpret_cast<float*>(ws + wl.lse);
   float* zbuf = reinterpret_cast<float*>(ws + wl.zbuf);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (w_uk == nullptr) {
+    // Pre-absorbed queries (mlra_proj_query with W^UQ.W^UK_b pre-multiplied wrote q~ and the
+    // scaled rotary query): K2 as a programmatic dependent of the projection, then K3.
+    int rc = decode_impl(q_nope, q_rope, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                         page_size, max_pages, num_pages, nsplit, stream, getenv("MLRA_NO_PDL") == nullptr);
+    if (rc) return rc;
+    return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, false, tp, status);
+  }
   // One launch per step when the whole grid is co-resident (fused_step.cuh): K1 in K2's prologue,
   // K3 (+ the TP sum) in its epilogue. Otherwise (or with MLRA_NO_FUSE) the three kernels below.
   const int CW = mlra::combine_chunk_width(DLAT);

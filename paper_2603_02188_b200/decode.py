@@ -157,6 +157,15 @@ class LocalWeights(dict):
     def packed(self, layout: RowLayout, device, own: Ownership | None = None) -> tuple[torch.Tensor, torch.Tensor]:
         key = ("__packed__", layout, str(device), None if own is None else (own.heads, own.units))
         if key not in self.__dict__:
+            uk, uv = self.packed_host(layout, own)
+            self.__dict__[key] = (torch.as_tensor(uk, device=device).to(torch.bfloat16).contiguous(),
+                                  torch.as_tensor(uv, device=device).to(torch.bfloat16).contiguous())
+        return self.__dict__[key]
+
+    def packed_host(self, layout: RowLayout, own: Ownership | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """The same packs in float32 on the host (before the bf16 rounding)."""
+        key = ("__packed_host__", layout, None if own is None else (own.heads, own.units))
+        if key not in self.__dict__:
             uks = [np.asarray(self[f"uk:{u}"]) for u in layout.units]
             uvs = [np.asarray(self[f"uv:{u}"]) for u in layout.units]
             dh = uks[0].shape[2]
@@ -170,8 +179,7 @@ class LocalWeights(dict):
                 rows = [heads.index(hd) for hd in unit_heads[i]]
                 uk[rows, :, i * dlp:i * dlp + dl] = np.transpose(a, (1, 2, 0))  # (lat, m, dh) -> (m, dh, lat)
                 uv[rows, i * dlp:i * dlp + dl, :] = np.transpose(b, (1, 0, 2))  # (lat, m, dh) -> (m, lat, dh)
-            self.__dict__[key] = (torch.as_tensor(uk, device=device).to(torch.bfloat16).contiguous(),
-                                  torch.as_tensor(uv, device=device).to(torch.bfloat16).contiguous())
+            self.__dict__[key] = (uk, uv)
         return self.__dict__[key]
 
 
@@ -219,6 +227,15 @@ def _queries_to_device(cfg: AttnConfig, layout: RowLayout, q_nope, q_rope, heads
     qr = torch.zeros((len(heads), layout.drp), dtype=torch.float32, device=device)
     qr[:, :layout.dr] = qr_src
     return qn.to(torch.bfloat16)[None].contiguous(), qr.to(torch.bfloat16)[None].contiguous()
+
+
+def _pad_rope(qn: torch.Tensor, qr: torch.Tensor, layout: RowLayout):
+    """K-1's rotary queries [M, h, dr] -> the cache layout's padded width drp (zero columns)."""
+    if qr.shape[-1] == layout.drp:
+        return qn.contiguous(), qr.contiguous()
+    out = torch.zeros(qr.shape[:-1] + (layout.drp,), dtype=qr.dtype, device=qr.device)
+    out[..., :qr.shape[-1]] = qr
+    return qn.contiguous(), out
 
 
 def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, own: Ownership, qn, qr, upproj: int,
@@ -298,6 +315,18 @@ class _StepState:
             self.projector = LatentProjector(cfg, w, device)
         self.own = full_ownership(cfg)
         self.lw = local_weights(cfg, w, self.own)
+        self.cfg, self.w, self.device = cfg, w, device
+        self._kproj = None
+
+    @property
+    def kproj(self):
+        """K-1 kernels for the drop-in single-token steps (full heads, q_nope for K1)."""
+        if self._kproj is None:
+            from .projections import KernelProjector
+
+            names = _write_plan(self.cfg, self.own)[0]
+            self._kproj = KernelProjector(self.cfg, self.w, self.device, range(self.cfg.h), names, absorbed=False)
+        return self._kproj
 
 
 _STATE: dict = {}
@@ -333,16 +362,22 @@ def _write_plan(cfg: AttnConfig, own: Ownership) -> tuple[list, int, int, int, i
     return [f"w_dkv_{j}" for j in groups], per_group * len(groups), idx[0], len(idx), len(groups)
 
 
-def append_token_latent(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, hidden: torch.Tensor,
-                        pos: int, own: Ownership | None = None) -> None:
-    """Write side of one decode step for a latent-family cache: the raw down-projections
-    (h W^DKV, h W^KR -- pre-attention GEMVs, torch) then the fused K0 kernel (rmsnorm*alpha_kv
-    per latent group, owned blocks, rope, padding, paged append)."""
+def append_token_latent(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, kv_raw: torch.Tensor,
+                        kr_raw: torch.Tensor, pos: int, own: Ownership | None = None) -> None:
+    """Write side of one decode step for a latent-family cache: the fused K0 kernel (rmsnorm*alpha_kv
+    per latent group, owned blocks, rope, padding, paged append) on the raw down-projections that
+    K-1 (``st.kproj.project``) produced for the token: kv_raw [1, all latent groups], kr_raw [1, dr]."""
     names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, own or st.own)
-    proj = st.projector
-    kv_raw = torch.cat([hidden @ proj.w[n] for n in names], dim=-1)
-    cache.append_latent(kv_raw, hidden @ proj.w_kr, pos, branches=blocks, block0=block0, nblocks=nblocks,
-                        alpha_kv=proj.alpha_kv, norm_groups=norm_groups)
+    cache.append_latent(st.kproj.kv_slice(kv_raw, names), kr_raw, pos, branches=blocks, block0=block0,
+                        nblocks=nblocks, alpha_kv=st.kproj.alpha_kv, norm_groups=norm_groups)
+
+
+def token_projections(cfg: AttnConfig, st: "_StepState", h_t, pos: int):
+    """K-1 for one token (latent.py:129-159 at one position): (kv_raw, kr_raw, q_nope [1, h, d_h]
+    bf16, q_rope [1, h, dr] bf16 with rope applied), all on the device."""
+    dev = st.device
+    hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
+    return st.kproj.project(hidden, torch.tensor([pos], dtype=torch.int32, device=dev))
 
 
 def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tuple[np.ndarray, PagedLatentCache]:
@@ -359,10 +394,9 @@ def absorbed_decode_step(cfg: AttnConfig, w, cache: PagedLatentCache, h_t) -> tu
         contribs = attend_local(cfg, {}, st.own, cache, {"q": q[0]})
         out, _ = reduce_contributions(cfg, contribs)
         return out, cache
-    hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32, device=dev)
-    append_token_latent(cfg, st, cache, hidden, pos)
-    q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
-    qn, qr = _queries_to_device(cfg, cache.layout, q_nope[0], q_rope[0], list(range(cfg.h)), dev)
+    kv_raw, kr_raw, qn, qr = token_projections(cfg, st, h_t, pos)  # K-1 (hand-written GEMMs)
+    append_token_latent(cfg, st, cache, kv_raw, kr_raw, pos)        # fused K0
+    qn, qr = _pad_rope(qn, qr, cache.layout)
     alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
     out = _run_units(cfg, cache, st.lw, st.own, qn, qr, upproj=1, alpha=alpha)
     cache.reads += cache.n * cache.row_elements()
@@ -420,22 +454,19 @@ def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t
     positions = torch.arange(cache.pos_offset, cache.pos_offset + n, dtype=torch.int32, device=dev)
     # ---- write side: one K0 launch for all n tokens
     names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, st.own)
-    proj = st.projector
-    kv_raw = torch.cat([h_t @ proj.w[nm] for nm in names], dim=-1).contiguous()
-    kr_raw = (h_t @ proj.w_kr).contiguous()
+    kp = st.kproj
+    kv_raw, kr_raw, qn, q_r = kp.project_gemm(h_t, positions)  # the n rows' projections (cuBLAS bf16)
+    kv_raw = kp.kv_slice(kv_raw, names)
     bt_rep = pc.block_table[:1].expand(n, -1).contiguous()
     slots = torch.arange(n, dtype=torch.int32, device=dev)
     ops.cache_append_latent(kv_raw, kr_raw, positions, slots, bt_rep, pc.pool, pc.page_size, branches=blocks,
                             block0=block0, nblocks=nblocks, dlp=layout.dlp, drp=layout.drp,
-                            alpha_kv=proj.alpha_kv, norm_groups=norm_groups)
+                            alpha_kv=kp.alpha_kv, norm_groups=norm_groups)
     pc.seqlens.fill_(n)
     pc._host_lens = [n]
     # ---- attention side: n pseudo-sequences of lengths 1..n over the same pages
-    q_nope, q_rope = proj.queries(h_t, positions.long())
     heads = list(range(cfg.h))
-    qn = q_nope.to(torch.bfloat16).contiguous()
-    qr = torch.zeros((n, cfg.h, layout.drp), dtype=torch.bfloat16, device=dev)
-    qr[..., :layout.dr] = q_rope.to(torch.bfloat16)
+    qn, qr = _pad_rope(qn, q_r, layout)
     w_uk, w_uv = st.lw.packed(layout, dev, st.own)
     nb, dlat = kernel_geometry(layout, st.own)
     sub, dls = ops.latent_geometry(dlat)
@@ -508,6 +539,44 @@ class DecodeEngine:
         hl = len(self.heads)
         self.workspace = ops.DecodeWorkspace(batch, hl, self.nb, self.dlat, self.layout.drp, self.nsplit, self.device)
         self.out = torch.empty((batch, hl, cfg.d_h), dtype=torch.float32, device=self.device)
+        self._w, self._lw, self._kp = w, lw, {}
+
+    def kernel_projector(self, absorbed: bool | None = None):
+        """K-1 for this device (its heads, its latent groups' raw down-projections). absorbed=None:
+        pre-multiply W^UQ.W^UK_b when that weight is no larger than W^UQ (one latent block per
+        device), so the query kernel writes K2's q~ and K1 is skipped."""
+        if absorbed not in self._kp:
+            from .projections import KernelProjector
+
+            uk, _ = self._lw.packed_host(self.layout, self.own)
+            self._kp[absorbed] = KernelProjector(self.cfg, self._w, self.device, self.heads,
+                                                 _write_plan(self.cfg, self.own)[0], uk_pack=uk, nb=self.nb,
+                                                 dlat=self.dlat, drp=self.layout.drp, absorbed=absorbed,
+                                                 score_scale=self.scale)
+        return self._kp[absorbed]
+
+    def decode_layer(self, hidden: torch.Tensor, out: torch.Tensor | None = None, absorbed: bool | None = None,
+                     advance: bool = True):
+        """One decode step of the attention layer from the new tokens' hidden rows (the paper's
+        end-to-end scope: the pre-attention stage plus the attention):
+        K-1 down (h W^DQ, h W^DKV, h W^KR) -> K0 (rmsnorm*alpha_kv, rope, paged append at the
+        sequence's length, advancing it) -> K-1 query (c_q rmsnorm, W^UQ [. W^UK_b], W^QR, rope)
+        -> [K1] -> K2 -> K3. hidden [B, d] fp32 on the device (B <= 16 per call); out [B, h_local,
+        d_h] fp32. ``advance=False`` rewrites the same slot every call (timing loops)."""
+        cfg, c = self.cfg, self.cache
+        kp = self.kernel_projector(absorbed)
+        names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, self.own)
+        B = hidden.shape[0]
+        kv_raw, kr_raw = kp.down(hidden)
+        ops.cache_append_latent(kv_raw, kr_raw, None, c.seqlens, c.block_table, c.pool, c.page_size,
+                                branches=blocks, block0=block0, nblocks=nblocks, dlp=self.layout.dlp,
+                                drp=self.layout.drp, alpha_kv=kp.alpha_kv, norm_groups=norm_groups, advance=advance)
+        q, qr = kp.query(B, c.seqlens, pos_delta=-1 if advance else 0)
+        if advance and getattr(c, "_host_lens", None) is not None:  # host mirror (eager calls)
+            c._host_lens = [n + 1 for n in c._host_lens]
+        return ops.decode_step(q, qr, None if kp.absorbed else self.w_uk, self.w_uv, c.pool, c.block_table,
+                               c.seqlens, c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale,
+                               self.alpha, self.workspace, out=self.out if out is None else out)
 
     @property
     def batch(self) -> int:

@@ -56,16 +56,17 @@ def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch
     _lib.check(rc, "mlra_cache_append")
 
 
-def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor, slots: torch.Tensor,
+def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor | None, slots: torch.Tensor,
                         block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
                         nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
                         eps: float = 1e-6, norm_groups: int = 1, advance: bool = False) -> None:
     """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
-    rope_pos, padded, appended as one bf16 pool row per sequence at slots[s] (then slots[s] += 1
-    with ``advance``)."""
+    rope_pos (None: at the slot written), padded, appended as one bf16 pool row per sequence at
+    slots[s] (then slots[s] += 1 with ``advance``)."""
     _need(kv_raw, torch.float32, "kv_raw", 2)
     _need(kr_raw, torch.float32, "kr_raw", 2)
-    _need(rope_pos, torch.int32, "rope_pos", 1)
+    if rope_pos is not None:
+        _need(rope_pos, torch.int32, "rope_pos", 1)
     _need(slots, torch.int32, "slots", 1)
     _need(block_table, torch.int32, "block_table", 2)
     _need(pool, torch.bfloat16, "pool", 2)
@@ -73,7 +74,8 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
     dr = kr_raw.shape[1]
     if pool.shape[1] != nblocks * dlp + drp:
         raise ShapeMismatchError(f"cache_append_latent: pool width {pool.shape[1]} != {nblocks * dlp + drp}")
-    rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(), rope_pos.data_ptr(),
+    rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(),
+                                              None if rope_pos is None else rope_pos.data_ptr(),
                                               slots.data_ptr(), block_table.data_ptr(), B, d_c, branches, block0,
                                               nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
                                               page_size, block_table.shape[1], norm_groups, int(advance),
@@ -196,15 +198,22 @@ class DecodeWorkspace:
 def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
                 sub: int, dls: int, nsplit: int, score_scale: float, alpha: float, workspace: DecodeWorkspace,
                 out: torch.Tensor | None = None) -> torch.Tensor:
-    """K1 + K2 + K3 through the single C-ABI entry point mlra_decode_step."""
-    B, H, DH = q_nope.shape
+    """K1 + K2 + K3 through the single C-ABI entry point mlra_decode_step. ``w_uk_packed=None``:
+    q_nope is the pre-absorbed, pre-scaled q~ [B, NB, H, DLAT] (K-1 with the pre-multiplied
+    weight) and q_rope is pre-scaled; the step is K2 + K3."""
+    if w_uk_packed is None:
+        B, _, H, _ = q_nope.shape
+        DH = w_uv_packed.shape[2]
+    else:
+        B, H, DH = q_nope.shape
     DR = q_rope.shape[2]
     dlat = sub * dls
     if workspace.key != (B, H, nb, dlat, DR, nsplit):
         raise ConfigError(f"workspace sized for {workspace.key}, call needs {(B, H, nb, dlat, DR, nsplit)}")
     if out is None:
         out = torch.empty((B, H, DH), dtype=torch.float32, device=q_nope.device)
-    rc = _lib.load().mlra_decode_step(q_nope.data_ptr(), q_rope.data_ptr(), w_uk_packed.data_ptr(),
+    rc = _lib.load().mlra_decode_step(q_nope.data_ptr(), q_rope.data_ptr(),
+                                      None if w_uk_packed is None else w_uk_packed.data_ptr(),
                                       w_uv_packed.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
                                       seqlens.data_ptr(), out.data_ptr(), workspace.buf.data_ptr(), B, H, DH, nb,
                                       sub, dls, DR, page_size, block_table.shape[1], pool.shape[0] // page_size,
@@ -459,3 +468,70 @@ def allreduce_sim(xs, ys, comms) -> None:
                                         n, world, _ptr_array([c.data_ptr() for c in comms]), _stream())
     _lib.check(rc, "mlra_allreduce_sim")
 
+
+
+# ----------------------------------------------------------------------------- K-1 projections
+def slab_shape(K: int, N: int) -> tuple[int, int, int]:
+    return (-(-N // 64), -(-K // 64) * 64, 64)
+
+
+def slab_pack(w: torch.Tensor) -> torch.Tensor:
+    """[K, N] weight -> the K-1 kernels' slab-packed bf16 [ceil(N/64)][round_up(K, 64)][64]:
+    element [s][k][c] = w[k][64 s + c] (zero outside w; include/mlra_b200.h)."""
+    K, N = w.shape
+    ns, kp, _ = slab_shape(K, N)
+    full = torch.zeros((kp, ns * 64), dtype=torch.bfloat16, device=w.device)
+    full[:K, :N] = w.to(torch.bfloat16)
+    return full.reshape(kp, ns, 64).permute(1, 0, 2).contiguous()
+
+
+def proj_down(x: torch.Tensor, w: torch.Tensor, n_q: int, n_kv: int, n_kr: int, c_q_raw: torch.Tensor | None,
+              kv_raw: torch.Tensor | None, kr_raw: torch.Tensor | None, ssq: torch.Tensor | None) -> None:
+    """K-1 down: [c_q_raw | kv_raw | kr_raw] = x . W  (x [M, K] fp32, w = ``slab_pack(W)`` of the
+    bf16 [K, n_q+n_kv+n_kr] weight), plus the per-64-column sums of squares of c_q_raw into ssq
+    [ceil(n_q/64), M]."""
+    _need(x, torch.float32, "x", 2)
+    _need(w, torch.bfloat16, "w", 3)
+    M, K = x.shape
+    if tuple(w.shape) != slab_shape(K, n_q + n_kv + n_kr):
+        raise ShapeMismatchError(f"proj_down: w {tuple(w.shape)} is not the slab pack of [{K}, {n_q}+{n_kv}+{n_kr}]")
+    outs = []
+    for t, width, name in ((c_q_raw, n_q, "c_q_raw"), (kv_raw, n_kv, "kv_raw"), (kr_raw, n_kr, "kr_raw")):
+        if t is not None:
+            _need(t, torch.float32, name, 2)
+            if tuple(t.shape) != (M, width):
+                raise ShapeMismatchError(f"proj_down: {name} {tuple(t.shape)} != {(M, width)}")
+        outs.append(0 if t is None else t.data_ptr())
+    if ssq is not None:
+        _need(ssq, torch.float32, "ssq", 2)
+        if tuple(ssq.shape) != (-(-n_q // 64), M):
+            raise ShapeMismatchError(f"proj_down: ssq {tuple(ssq.shape)} != {(-(-n_q // 64), M)}")
+    rc = _lib.load().mlra_proj_down(x.data_ptr(), w.data_ptr(), M, K, n_q, n_kv, n_kr, *outs,
+                                    0 if ssq is None else ssq.data_ptr(), _stream())
+    _lib.check(rc, "mlra_proj_down")
+
+
+def proj_query(c_q_raw: torch.Tensor, ssq: torch.Tensor | None, alpha_q: float, w: torch.Tensor, nq: int, heads: int,
+               dr: int, pos: torch.Tensor, q_out: torch.Tensor, r_out: torch.Tensor, *, q_scale: float = 1.0,
+               r_scale: float = 1.0, eps: float = 1e-6, rope_base: float = 10000.0, pos_delta: int = 0) -> None:
+    """K-1 query: c_q = alpha_q * rmsnorm(c_q_raw) (statistics from ssq), [q_x | q_r] = c_q . w;
+    q_out [M, nq] bf16 = q_scale * q_x, r_out [M, heads, drp] bf16 = r_scale * rope(q_r, pos + pos_delta)."""
+    _need(c_q_raw, torch.float32, "c_q_raw", 2)
+    _need(w, torch.bfloat16, "w", 3)
+    _need(pos, torch.int32, "pos", 1)
+    _need(q_out, torch.bfloat16, "q_out")
+    _need(r_out, torch.bfloat16, "r_out", 3)
+    M, K = c_q_raw.shape
+    if tuple(w.shape) != slab_shape(K, nq + heads * dr):
+        raise ShapeMismatchError(f"proj_query: w {tuple(w.shape)} is not the slab pack of [{K}, {nq}+{heads}*{dr}]")
+    if q_out.numel() != M * nq or r_out.shape[0] != M or r_out.shape[1] != heads or r_out.shape[2] < dr:
+        raise ShapeMismatchError("proj_query: output shapes do not match")
+    if pos.shape[0] < M:
+        raise ShapeMismatchError(f"proj_query: {pos.shape[0]} positions for {M} rows")
+    if ssq is not None:
+        _need(ssq, torch.float32, "ssq", 2)
+    rc = _lib.load().mlra_proj_query(c_q_raw.data_ptr(), 0 if ssq is None else ssq.data_ptr(), float(alpha_q),
+                                     float(eps), w.data_ptr(), M, K, nq, heads, dr, r_out.shape[2], pos.data_ptr(),
+                                     int(pos_delta), float(rope_base), float(q_scale), float(r_scale), q_out.data_ptr(),
+                                     r_out.data_ptr(), _stream())
+    _lib.check(rc, "mlra_proj_query")

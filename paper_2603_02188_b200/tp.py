@@ -28,8 +28,8 @@ from fractions import Fraction
 import numpy as np
 
 from .config import TP_DEGREES, AttnConfig
-from .decode import (LatentUnit, Ownership, _check_served, append_token_latent, attend_local, local_weights,
-                     new_cache, reduce_contributions, _state)
+from .decode import (LatentUnit, Ownership, _check_served, _state, append_token_latent, attend_local, local_weights,
+                     new_cache, reduce_contributions, token_projections)
 from .errors import ConfigError, IntegrityError
 
 
@@ -197,6 +197,7 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
     st = _state(cfg, w, dev)
     before = [s.cache.reads for s in shards.shards]
     by_device: dict = {}
+    proj = None
     import torch
 
     if cfg.variant == "gqa":
@@ -212,11 +213,10 @@ def sim_decode(shards: ShardSet, h_t, order=None):  # tpsim.py:253-286
             by_device[shard.device_id] = attend_local(cfg, {}, shard.own, shard.cache,
                                                       {"q": q[0].double().cpu().numpy()})
             continue
-        hidden = torch.as_tensor(np.asarray(h_t, dtype=np.float64).reshape(1, cfg.d), dtype=torch.float32,
-                                 device=dev)
-        append_token_latent(cfg, st, shard.cache, hidden, pos, shard.own)  # fused K0 (owned blocks)
-        q_nope, q_rope = st.projector.queries(hidden, torch.tensor([pos], device=dev))
-        queries = {"q_nope": q_nope[0].double().cpu().numpy(), "q_rope": q_rope[0].double().cpu().numpy()}
+        if proj is None:  # K-1 once per step (the ranks' replicated projections)
+            proj = token_projections(cfg, st, h_t, pos)
+            queries = {"q_nope": proj[2][0].double().cpu().numpy(), "q_rope": proj[3][0].double().cpu().numpy()}
+        append_token_latent(cfg, st, shard.cache, proj[0], proj[1], pos, shard.own)  # fused K0 (owned blocks)
         by_device[shard.device_id] = attend_local(cfg, shard.attn_weights, shard.own, shard.cache, queries)
     contribs = [c for did in sorted(by_device) for c in by_device[did]]
     out, kind = reduce_contributions(cfg, contribs)

@@ -220,5 +220,5 @@ def test_decode_routing_errors():
         full_ownership(trained_config("mla").with_(variant="tpa"))
     with pytest.raises(RoutingError):
         decode_step(trained_config("mlra4"), None, None, None, mode="turbo")
-    with pytest.raises(RoutingError):
-        decode_step(trained_config("mlra4"), None, None, None, mode="naive")
+    with pytest.raises(RoutingError):  # naive covers the latent family only (decode.py:313-316)
+        decode_step(trained_config("gqa"), None, None, None, mode="naive")

@@ -57,7 +57,10 @@ def test_prefill_matches_reference_and_continues_decoding(name):
 
 def test_prefill_is_chunked_and_matches_decode_steps():
     """More queries than one kernel pass (PREFILL_CHUNK patched small) and a position offset:
-    the prefill outputs equal the per-token decode outputs of the same tokens."""
+    the prefill outputs equal the per-token decode outputs of the same tokens (the reference's
+    tests/test_decode.py:83-94). Same kernels and bf16 weights on both sides; the prefill's n-row
+    projections run as cuBLAS bf16 GEMMs (bf16 activations) and the decode's through K-1
+    (fp32-split activations), so the two agree to the bf16 level, not bit for bit."""
     import paper_2603_02188_b200 as mlra
     from paper_2603_02188_b200 import decode as dec
 
@@ -75,7 +78,7 @@ def test_prefill_is_chunked_and_matches_decode_steps():
     cache = mlra.new_cache(cfg, pos_offset=11, device="cuda:0")
     for t in range(40):
         o, cache = mlra.absorbed_decode_step(cfg, w, cache, hidden[t])
-        np.testing.assert_allclose(res.out[t], o, rtol=0, atol=1e-5 * max(1.0, np.abs(o).max()))
+        assert ak.max_rel_err(o, res.out[t]) <= 1e-2, t
 
 
 def test_prefill_rejects_zoo_variants_and_empty_input():
