@@ -69,7 +69,8 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* pos
  *   kv_raw [B, d_c] fp32 = h W^DKV (whole groups: the RMS spans a group's blocks), kr_raw
  *   [B, dr] fp32 = h W^KR. MLA: branches = 1. advance != 0: slots[s] += 1 after the write
  *   (slots are then the sequence lengths, as in mlra_cache_append). rope_pos == NULL: the rope
- *   position is the slot written (a cache holding positions 0..n-1).
+ *   position is the slot written (a cache holding positions 0..n-1). slots == NULL: the B rows
+ *   are ONE sequence's tokens 0..B-1 (prefill), row s written at slot s of block_table row 0.
  */
 int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int32_t* rope_pos, int32_t* slots,
                              const int32_t* block_table, int B, int d_c, int branches, int block0, int nblocks,
@@ -277,6 +278,23 @@ int mlra_proj_down(const float* x, const void* w, int M, int K, int n_q, int n_k
 int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float eps, const void* w, int M, int K,
                     int nq, int H, int dr, int drp, const int32_t* pos, int pos_delta, float rope_base, float q_scale, float r_scale,
                     void* q_out, void* r_out, void* stream);
+
+/*
+ * K6 -- causal latent prefill attention (latent.py:172-230 latent_prefill,
+ * causal softmax latent.py:164-169) for ONE sequence of n tokens already in the paged cache
+ * (block_table row 0, positions 0..n-1), tcgen05 + TMA (prefill_kernel.cuh):
+ *   out[q, h] = alpha * sum_b softmax_{k <= q}(q~_(b,h)[q] . C_b[k] + q_rope_h[q] . K_rope[k]) . C_b
+ *               . W^UV_(b),(h)
+ *   q_abs  [n, NB, H, DLAT] bf16, q_rope [n, H, DRq] bf16 (K1's outputs for the n queries:
+ *          pre-scaled by tau*log2e, rope applied; DR <= DRq <= 64), w_uv [H, NB*DLAT, DH] bf16 (K3's pack)
+ *   pool   [num_pages*page_size, NB*DLAT + DRp] bf16 (DRp: the padded rope width), page_size a
+ *          multiple of 128
+ *   out    [n, H, DH] fp32; (DLAT, DH) in {(128, 128), (64, 64)}; alpha = alpha_attn.
+ * CTA = (128 queries, head), all branches in ascending order (the branch sum in TMEM).
+ */
+int mlra_prefill_attention(const void* q_abs, const void* q_rope, const void* w_uv, const void* pool,
+                           const int32_t* block_table, float* out, int n, int H, int NB, int DLAT, int DH, int DR,
+                           int DRp, int DRq, int page_size, int max_pages, int num_pages, float alpha, void* stream);
 
 #ifdef __cplusplus
 }

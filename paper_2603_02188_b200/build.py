@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmlra_b200.so")
 SOURCES = ["capi.cu", "decode_inst_a.cu", "decode_inst_b.cu", "decode_inst_c.cu", "decode_inst_d.cu", "proj.cu"]
 HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cuh", "allreduce_kernel.cuh",
-           "fused_step.cuh", "host_common.cuh", "peer_common.cuh", "proj_kernel.cuh"]
+           "fused_step.cuh", "host_common.cuh", "peer_common.cuh", "proj_kernel.cuh", "prefill_kernel.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 STAMP = LIB + ".srchash"  # source hash of the shipped library (travels with it)

@@ -72,7 +72,8 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
   __shared__ float red[kMaxGroups][kK0Threads / 32];
   __shared__ float gscale[kMaxGroups];
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int slot = slots[s];  // read before the barriers below; advanced after them
+  // slots == NULL: ONE sequence's n rows (prefill): row s -> slot s of block_table row 0
+  const int slot = slots != nullptr ? slots[s] : s;  // read before the barriers below; advanced after them
   const float* kv = kv_raw + size_t(s) * d_c;
   const int gw = d_c / norm_groups;
   for (int g = 0; g < norm_groups; ++g) {
@@ -90,8 +91,8 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
     gscale[tid] = alpha_kv * rsqrtf(tot / float(gw) + eps);
   }
   __syncthreads();
-  if (advance && tid == 0) slots[s] = slot + 1;
-  const int page = block_table[size_t(s) * max_pages + slot / page_size];
+  if (advance && slots != nullptr && tid == 0) slots[s] = slot + 1;
+  const int page = block_table[size_t(slots != nullptr ? s : 0) * max_pages + slot / page_size];
   const int W = nblocks * dlp + drp;
   __nv_bfloat16* dst = pool + (size_t(page) * page_size + slot % page_size) * W;
   for (int i = tid; i < nblocks * dlp; i += kK0Threads) {

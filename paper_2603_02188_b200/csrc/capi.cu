@@ -14,6 +14,7 @@
 #include "aux_kernels.cuh"
 #include "outproj_kernel.cuh"
 #include "allreduce_kernel.cuh"
+#include "prefill_kernel.cuh"
 
 namespace mlra_host {
 thread_local char g_err[512] = "";
@@ -964,3 +965,85 @@ int mlra_ipc_close(void* dev_ptr) {
 }
 
 }  // extern "C"
+
+namespace {
+int encode_3d(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint64_t d2, cuuint64_t s1,
+              cuuint64_t s2, cuuint32_t b0, cuuint32_t b1, cuuint32_t b2) {
+  auto encode = get_encode();
+  if (!encode) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return cr == CUDA_SUCCESS ? MLRA_OK : fail(MLRA_ERR_CONFIG, "cuTensorMapEncodeTiled(3d) failed (%d)", int(cr));
+}
+
+template <int DLAT, int DH>
+int launch_prefill(const PoolMaps* pm, const void* q_abs, const void* q_rope, const void* w_uv, mlra::PrefillParams& p,
+                   int DRq, cudaStream_t st) {
+  using L = mlra::PrefillLayout<DLAT, DH>;
+  CUtensorMap qm, rm, wm;
+  if (int rc = encode_3d(&qm, q_abs, DLAT, cuuint64_t(p.NB) * p.H, p.n, cuuint64_t(DLAT) * 2,
+                         cuuint64_t(p.NB) * p.H * DLAT * 2, 64, 1, mlra::kPfT))
+    return rc;
+  if (int rc = encode_3d(&rm, q_rope, DRq, p.H, p.n, cuuint64_t(DRq) * 2, cuuint64_t(p.H) * DRq * 2, 64, 1, mlra::kPfT))
+    return rc;
+  {
+    auto encode = get_encode();
+    cuuint64_t dims[2] = {cuuint64_t(DH), cuuint64_t(p.H) * p.NB * DLAT};
+    cuuint64_t strides[1] = {cuuint64_t(DH) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(DLAT)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&wm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w_uv), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "prefill: W^UV tensor map failed (%d)", int(cr));
+  }
+  auto kern = mlra::prefill_attention_kernel<DLAT, DH>;
+  static unsigned done = 0;
+  if (int rc = set_smem_once(kern, done, L::kSmem)) return rc;
+  const int nqt = (p.n + mlra::kPfT - 1) / mlra::kPfT;
+  kern<<<nqt * p.H, mlra::kPfThreads, L::kSmem, st>>>(pm->lat, pm->rope, qm, rm, wm, p);
+  return cuda_check("prefill_attention launch");
+}
+}  // namespace
+
+extern "C" int mlra_prefill_attention(const void* q_abs, const void* q_rope, const void* w_uv, const void* pool,
+                                      const int32_t* block_table, float* out, int n, int H, int NB, int DLAT, int DH,
+                                      int DR, int DRp, int DRq, int page_size, int max_pages, int num_pages,
+                                      float alpha, void* stream) {
+  if (n <= 0) return MLRA_OK;
+  if (H <= 0 || NB < 1 || NB > 4 || DR < 0 || DR > 64 || DRp < DR || DRp % 8 != 0 || DRq < DR || DRq % 8 != 0 ||
+      DRq > 64)
+    return fail(MLRA_ERR_SHAPE, "prefill_attention: bad dims H=%d NB=%d DR=%d DRp=%d DRq=%d", H, NB, DR, DRp, DRq);
+  if (!((DLAT == 128 && DH == 128) || (DLAT == 64 && DH == 64)))
+    return fail(MLRA_ERR_CONFIG, "prefill_attention: (DLAT, DH) = (%d, %d) not in {(128,128), (64,64)}", DLAT, DH);
+  if (page_size % mlra::kPfT != 0) return fail(MLRA_ERR_CONFIG, "prefill_attention: page_size %d not a multiple of 128", page_size);
+  if (long(max_pages) * page_size < n) return fail(MLRA_ERR_CONFIG, "prefill_attention: %d tokens exceed the page table", n);
+  const int W = NB * DLAT + DRp;
+  const PoolMaps* pm = nullptr;
+  if (int rc = get_pool_maps(pool, cuuint64_t(num_pages) * page_size, W, mlra::kPfT, mlra::kPfT, DLAT, NB * DLAT / 64, &pm))
+    return rc;
+  mlra::PrefillParams p = {};
+  p.block_table = block_table;
+  p.out = out;
+  p.n = n;
+  p.H = H;
+  p.NB = NB;
+  p.DR = DR;
+  p.page_size = page_size;
+  p.max_pages = max_pages;
+  p.alpha = alpha;
+  p.rope_col = NB * DLAT;
+  if (const char* e = getenv("MLRA_DEBUG_PF_S")) {
+    p.dbg_s = reinterpret_cast<float*>(strtoull(e, nullptr, 0));
+    p.dbg_cta = getenv("MLRA_DEBUG_PF_CTA") ? atoi(getenv("MLRA_DEBUG_PF_CTA")) : 0;
+  }
+  if (const char* e = getenv("MLRA_DEBUG_PF_PROGRESS")) p.progress = reinterpret_cast<volatile int*>(strtoull(e, nullptr, 0));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (DLAT == 128) return launch_prefill<128, 128>(pm, q_abs, q_rope, w_uv, p, DRq, st);
+  return launch_prefill<64, 64>(pm, q_abs, q_rope, w_uv, p, DRq, st);
+}

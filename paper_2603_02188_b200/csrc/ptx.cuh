@@ -111,6 +111,14 @@ __device__ __forceinline__ void tma_load_3d_hint(const void* desc, uint64_t* bar
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// 3-D tiled load without a cache hint.
+__device__ __forceinline__ void tma_load_3d(const void* desc, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // Programmatic dependent launch (PDL). launch_dependents lets the next kernel on the stream
 // (launched with the programmatic-serialization attribute) start its prologue; wait blocks
 // until every kernel this one depends on has completed and its writes are visible. Both

@@ -444,41 +444,63 @@ def latent_prefill(cfg: AttnConfig, w, hidden, pos_offset: int = 0, *, device=No
     return PrefillOutput(out.double().cpu().numpy(), cache)
 
 
-def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t: torch.Tensor) -> torch.Tensor:
+def prefill_kernel_fits(cfg: AttnConfig, layout: RowLayout, own: Ownership, page_size: int) -> bool:
+    """K6 (the tcgen05 causal prefill kernel) serves 128- or 64-wide latent branches with a matching
+    head width (MLRA-4 / MLRA-2 at the 2.9B shape, the tiny config), <= 64 rotary columns and
+    pages of whole 128-token tiles; other geometries take the pseudo-sequence path."""
+    nb, dlat = kernel_geometry(layout, own)
+    return (dlat, cfg.d_h) in ((128, 128), (64, 64)) and nb <= 4 and layout.drp <= 64 and page_size % 128 == 0
+
+
+def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t: torch.Tensor,
+                 force_pseudo: bool = False) -> torch.Tensor:
     """Device part of latent_prefill: fill the EMPTY paged cache with the n tokens of h_t
-    [n, d] fp32 (positions pos_offset + t) and return the outputs [n, h, d_h] fp32."""
+    [n, d] fp32 (positions pos_offset + t) and return the outputs [n, h, d_h] fp32.
+
+    Write side: the n rows' projections (cuBLAS bf16 GEMMs on K-1's packed weights) and ONE
+    fused K0 launch writing token t at slot t of the sequence's pages. Queries: K1 over the n
+    rows. Attention: K6 (``mlra_prefill_attention``: causal, tcgen05, 128 queries x one head
+    per CTA, all branches and the W^UV up-projection in-kernel) when the geometry fits;
+    otherwise the n queries run as n decode pseudo-sequences of lengths 1..n over the same
+    pages through K2 -> K3 (causality by the lengths)."""
     n = h_t.shape[0]
     dev = h_t.device
     pc = cache.paged
     layout = cache.layout
     positions = torch.arange(cache.pos_offset, cache.pos_offset + n, dtype=torch.int32, device=dev)
-    # ---- write side: one K0 launch for all n tokens
+    # ---- write side: one K0 launch for all n tokens (slots 0..n-1 of block_table row 0)
     names, blocks, block0, nblocks, norm_groups = _write_plan(cfg, st.own)
     kp = st.kproj
     kv_raw, kr_raw, qn, q_r = kp.project_gemm(h_t, positions)  # the n rows' projections (cuBLAS bf16)
     kv_raw = kp.kv_slice(kv_raw, names)
-    bt_rep = pc.block_table[:1].expand(n, -1).contiguous()
-    slots = torch.arange(n, dtype=torch.int32, device=dev)
-    ops.cache_append_latent(kv_raw, kr_raw, positions, slots, bt_rep, pc.pool, pc.page_size, branches=blocks,
+    ops.cache_append_latent(kv_raw, kr_raw, positions, None, pc.block_table, pc.pool, pc.page_size, branches=blocks,
                             block0=block0, nblocks=nblocks, dlp=layout.dlp, drp=layout.drp,
                             alpha_kv=kp.alpha_kv, norm_groups=norm_groups)
     pc.seqlens.fill_(n)
     pc._host_lens = [n]
-    # ---- attention side: n pseudo-sequences of lengths 1..n over the same pages
     heads = list(range(cfg.h))
     qn, qr = _pad_rope(qn, q_r, layout)
     w_uk, w_uv = st.lw.packed(layout, dev, st.own)
     nb, dlat = kernel_geometry(layout, st.own)
     sub, dls = ops.latent_geometry(dlat)
     alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
+    scale = ops.score_scale(cfg.tau)
+    if not force_pseudo and prefill_kernel_fits(cfg, layout, st.own, pc.page_size):
+        # K6 reads the rotary queries as 64-column rows (TMA boxes of the 128-byte swizzle)
+        qr64 = qr if layout.drp == 64 else torch.nn.functional.pad(qr, (0, 64 - layout.drp))
+        q_abs, q_rs = ops.absorb_query(qn, qr64.contiguous(), w_uk, nb, dlat, scale)
+        return ops.prefill_attention(q_abs, q_rs, w_uv, pc.pool, pc.block_table, pc.page_size, nb, dlat,
+                                     cfg.d_h_rope, alpha)
+    # ---- pseudo-sequence path: n queries of lengths 1..n over the same pages
+    bt_rep = pc.block_table[:1].expand(min(n, PREFILL_CHUNK), -1).contiguous()
     out = torch.empty((n, len(heads), cfg.d_h), dtype=torch.float32, device=dev)
     for t0 in range(0, n, PREFILL_CHUNK):
         t1 = min(n, t0 + PREFILL_CHUNK)
         m = t1 - t0
         lens = torch.arange(t0 + 1, t1 + 1, dtype=torch.int32, device=dev)
         nsplit = ops.default_splits(m, t1, nb, sub)
-        q_abs, q_rs = ops.absorb_query(qn[t0:t1], qr[t0:t1].contiguous(), w_uk, nb, dlat, ops.score_scale(cfg.tau))
-        o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, bt_rep[t0:t1], lens, pc.page_size, nb, sub, dls,
+        q_abs, q_rs = ops.absorb_query(qn[t0:t1], qr[t0:t1].contiguous(), w_uk, nb, dlat, scale)
+        o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, bt_rep[:m], lens, pc.page_size, nb, sub, dls,
                                           nsplit)
         out[t0:t1] = ops.combine(o_part, lse, w_uv, alpha)
     return out

@@ -56,18 +56,21 @@ def cache_append(rows: torch.Tensor, block_table: torch.Tensor, positions: torch
     _lib.check(rc, "mlra_cache_append")
 
 
-def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor | None, slots: torch.Tensor,
+def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: torch.Tensor | None,
+                        slots: torch.Tensor | None,
                         block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
                         nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
                         eps: float = 1e-6, norm_groups: int = 1, advance: bool = False) -> None:
     """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
     rope_pos (None: at the slot written), padded, appended as one bf16 pool row per sequence at
-    slots[s] (then slots[s] += 1 with ``advance``)."""
+    slots[s] (then slots[s] += 1 with ``advance``). slots=None: the rows are one sequence's tokens
+    0..B-1 (prefill), row s at slot s of block_table row 0."""
     _need(kv_raw, torch.float32, "kv_raw", 2)
     _need(kr_raw, torch.float32, "kr_raw", 2)
     if rope_pos is not None:
         _need(rope_pos, torch.int32, "rope_pos", 1)
-    _need(slots, torch.int32, "slots", 1)
+    if slots is not None:
+        _need(slots, torch.int32, "slots", 1)
     _need(block_table, torch.int32, "block_table", 2)
     _need(pool, torch.bfloat16, "pool", 2)
     B, d_c = kv_raw.shape
@@ -76,7 +79,8 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
         raise ShapeMismatchError(f"cache_append_latent: pool width {pool.shape[1]} != {nblocks * dlp + drp}")
     rc = _lib.load().mlra_cache_append_latent(kv_raw.data_ptr(), kr_raw.data_ptr(),
                                               None if rope_pos is None else rope_pos.data_ptr(),
-                                              slots.data_ptr(), block_table.data_ptr(), B, d_c, branches, block0,
+                                              None if slots is None else slots.data_ptr(), block_table.data_ptr(),
+                                              B, d_c, branches, block0,
                                               nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
                                               page_size, block_table.shape[1], norm_groups, int(advance),
                                               pool.data_ptr(), _stream())
@@ -535,3 +539,29 @@ def proj_query(c_q_raw: torch.Tensor, ssq: torch.Tensor | None, alpha_q: float, 
                                      int(pos_delta), float(rope_base), float(q_scale), float(r_scale), q_out.data_ptr(),
                                      r_out.data_ptr(), _stream())
     _lib.check(rc, "mlra_proj_query")
+
+
+def prefill_attention(q_abs: torch.Tensor, q_rope: torch.Tensor, w_uv_packed: torch.Tensor, pool: torch.Tensor,
+                      block_table: torch.Tensor, page_size: int, nb: int, dlat: int, dr: int, alpha: float,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """K6: causal prefill attention of one sequence of n tokens already in the paged cache
+    (block_table row 0): q_abs [n, NB, H, DLAT] / q_rope [n, H, DRp] (K1 outputs), w_uv
+    [H, NB*DLAT, DH] -> out [n, H, DH] fp32 (alpha-scaled, branch-summed)."""
+    _need(q_abs, torch.bfloat16, "q_abs", 4)
+    _need(q_rope, torch.bfloat16, "q_rope", 3)
+    _need(w_uv_packed, torch.bfloat16, "w_uv", 3)
+    _need(pool, torch.bfloat16, "pool", 2)
+    _need(block_table, torch.int32, "block_table", 2)
+    n, NB, H, DLAT = q_abs.shape
+    DH = w_uv_packed.shape[2]
+    if NB != nb or DLAT != dlat or q_rope.shape[:2] != (n, H):
+        raise ShapeMismatchError("prefill_attention: query shapes do not match")
+    if out is None:
+        out = torch.empty((n, H, DH), dtype=torch.float32, device=q_abs.device)
+    rc = _lib.load().mlra_prefill_attention(q_abs.data_ptr(), q_rope.data_ptr(), w_uv_packed.data_ptr(),
+                                            pool.data_ptr(), block_table.data_ptr(), out.data_ptr(), n, H, NB, DLAT,
+                                            DH, dr, pool.shape[1] - NB * DLAT, q_rope.shape[2], page_size,
+                                            block_table.shape[1],
+                                            pool.shape[0] // page_size, float(alpha), _stream())
+    _lib.check(rc, "mlra_prefill_attention")
+    return out

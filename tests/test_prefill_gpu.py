@@ -91,3 +91,31 @@ def test_prefill_rejects_zoo_variants_and_empty_input():
     _, w, _ = regen(meta)
     res = mlra.latent_prefill(_cfg(meta), w, np.zeros((0, 32)), device="cuda:0")
     assert res.out.shape == (0, 4, 8) and res.cache.n == 0
+
+
+@pytest.mark.parametrize("variant,n", [("mlra4", 1), ("mlra4", 129), ("mlra4", 1000), ("mlra2", 300), ("tiny", 700),
+                                       ("mlra4", 4096)])
+def test_prefill_kernel_matches_pseudo_sequence_path(variant, n):
+    """K6 (tcgen05 causal prefill: 128 queries x one head per CTA, all branches and W^UV in-kernel)
+    against the decode kernels run as n pseudo-sequences of lengths 1..n over the same cache --
+    two independent implementations of latent.py:172-230 on the same bf16 cache and queries.
+    Covers ragged tails (n % 128 != 0), the diagonal mask and the 2.9B / tiny geometries."""
+    import paper_2603_02188_b200 as mlra
+    from paper_2603_02188_b200 import decode as dec
+    from paper_2603_02188_b200.config import trained_config
+    from paper_2603_02188_b200.weights import weight_shapes
+
+    cfg = mlra.tiny_config() if variant == "tiny" else trained_config(variant)
+    rng = np.random.default_rng(n)
+    w = {name: rng.standard_normal(shape) * 0.02 for name, shape in weight_shapes(cfg).items()}
+    dev = torch.device("cuda", 0)
+    st = dec._state(cfg, w, dev)
+    h = torch.randn((n, cfg.d), generator=torch.Generator(device=dev).manual_seed(n), device=dev)
+    outs = []
+    for force in (False, True):
+        cache = dec.new_cache(cfg, device=dev, initial_tokens=max(n, 128))
+        assert dec.prefill_kernel_fits(cfg, cache.layout, st.own, cache.paged.page_size)
+        outs.append(dec.prefill_into(cfg, st, cache, h, force_pseudo=force).double().cpu().numpy())
+    errs = [ak.max_rel_err(outs[1][t], outs[0][t]) for t in range(n)]
+    print(variant, n, "max_rel_err K6 vs pseudo-sequences", max(errs))
+    assert max(errs) <= 5e-3, (int(np.argmax(errs)), max(errs))
