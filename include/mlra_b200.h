@@ -285,8 +285,9 @@ int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float
  * (block_table row 0, positions 0..n-1), tcgen05 + TMA (prefill_kernel.cuh):
  *   out[q, h] = alpha * sum_b softmax_{k <= q}(q~_(b,h)[q] . C_b[k] + q_rope_h[q] . K_rope[k]) . C_b
  *               . W^UV_(b),(h)
- *   q_abs  [n, NB, H, DLAT] bf16, q_rope [n, H, DRq] bf16 (K1's outputs for the n queries:
- *          pre-scaled by tau*log2e, rope applied; DR <= DRq <= 64), w_uv [H, NB*DLAT, DH] bf16 (K3's pack)
+ *   q_abs  [H, n, NB, DLAT] bf16 head-major absorbed queries (the batched GEMM q_nope_h .
+ *          W^UK_h of the n rows), q_rope [n, H, DRq] bf16 (rope applied; DR <= DRq <= 64), both
+ *          pre-scaled by tau*log2e; w_uv [H, NB*DLAT, DH] bf16 (K3's pack)
  *   pool   [num_pages*page_size, NB*DLAT + DRp] bf16 (DRp: the padded rope width), page_size a
  *          multiple of 128
  *   out    [n, H, DH] fp32; (DLAT, DH) in {(128, 128), (64, 64)}; alpha = alpha_attn.
@@ -295,6 +296,19 @@ int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float
 int mlra_prefill_attention(const void* q_abs, const void* q_rope, const void* w_uv, const void* pool,
                            const int32_t* block_table, float* out, int n, int H, int NB, int DLAT, int DH, int DR,
                            int DRp, int DRq, int page_size, int max_pages, int num_pages, float alpha, void* stream);
+
+/*
+ * Prefill projection helpers (the n-row projections run as cuBLAS bf16 GEMMs around them):
+ * mlra_rows_split: x [n, ldx] fp32 (first K columns) -> hi, lo bf16 [n, K] with x (norm = 0) or
+ *   alpha * rmsnorm(x) (norm != 0; tensors.py:83-87) = hi + lo to ~16 bits.
+ * mlra_query_epilogue: y [n, ldy] fp32 = [q_x (nq columns) | q_r (H * dr)] -> q_out bf16 [n, nq] =
+ *   q_scale * q_x, r_out bf16 [n, H, drq] = r_scale * rope(q_r, pos0 + row) (rope.py:37-60),
+ *   columns [dr, drq) zero.
+ */
+int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, float alpha, float eps, void* hi, void* lo,
+                    void* stream);
+int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H, int dr, int drq, int pos0, float rope_base,
+                        float q_scale, float r_scale, void* q_out, void* r_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,8 @@ SIGNATURES = {
     "mlra_ipc_open": (_I, [_P, _P]),
     "mlra_ipc_close": (_I, [_P]),
     "mlra_prefill_attention": (_I, [_P] * 6 + [_I] * 11 + [_F, _P]),
+    "mlra_rows_split": (_I, [_P] + [_I] * 4 + [_F, _F, _P, _P, _P]),
+    "mlra_query_epilogue": (_I, [_P] + [_I] * 7 + [_F, _F, _F, _P, _P, _P]),
     "mlra_proj_down": (_I, [_P, _P] + [_I] * 5 + [_P] * 5),
     "mlra_proj_query": (_I, [_P, _P, _F, _F, _P] + [_I] * 6 + [_P, _I, _F, _F, _F, _P, _P, _P]),
 }

@@ -986,9 +986,17 @@ int launch_prefill(const PoolMaps* pm, const void* q_abs, const void* q_rope, co
                    int DRq, cudaStream_t st) {
   using L = mlra::PrefillLayout<DLAT, DH>;
   CUtensorMap qm, rm, wm;
-  if (int rc = encode_3d(&qm, q_abs, DLAT, cuuint64_t(p.NB) * p.H, p.n, cuuint64_t(DLAT) * 2,
-                         cuuint64_t(p.NB) * p.H * DLAT * 2, 64, 1, mlra::kPfT))
-    return rc;
+  {  // q~ head-major [H, n, NB, DLAT]: 4-D {DLAT, NB, n, H}, box {64, 1, 128, 1}
+    auto encode = get_encode();
+    cuuint64_t dims[4] = {cuuint64_t(DLAT), cuuint64_t(p.NB), cuuint64_t(p.n), cuuint64_t(p.H)};
+    cuuint64_t strides[3] = {cuuint64_t(DLAT) * 2, cuuint64_t(p.NB) * DLAT * 2, cuuint64_t(p.n) * p.NB * DLAT * 2};
+    cuuint32_t box[4] = {64, 1, mlra::kPfT, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult cr = encode(&qm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q_abs), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MLRA_ERR_CONFIG, "prefill: q~ tensor map failed (%d)", int(cr));
+  }
   if (int rc = encode_3d(&rm, q_rope, DRq, p.H, p.n, cuuint64_t(DRq) * 2, cuuint64_t(p.H) * DRq * 2, 64, 1, mlra::kPfT))
     return rc;
   {
@@ -1046,4 +1054,25 @@ extern "C" int mlra_prefill_attention(const void* q_abs, const void* q_rope, con
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (DLAT == 128) return launch_prefill<128, 128>(pm, q_abs, q_rope, w_uv, p, DRq, st);
   return launch_prefill<64, 64>(pm, q_abs, q_rope, w_uv, p, DRq, st);
+}
+
+extern "C" int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, float alpha, float eps, void* hi,
+                               void* lo, void* stream) {
+  if (n <= 0) return MLRA_OK;
+  if (K <= 0 || ldx < K) return fail(MLRA_ERR_SHAPE, "rows_split: K=%d ldx=%d", K, ldx);
+  mlra::rows_split_kernel<<<n, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, K, ldx, norm, alpha, eps, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo));
+  return cuda_check("rows_split launch");
+}
+
+extern "C" int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H, int dr, int drq, int pos0,
+                                   float rope_base, float q_scale, float r_scale, void* q_out, void* r_out,
+                                   void* stream) {
+  if (n <= 0) return MLRA_OK;
+  if (nq < 0 || H <= 0 || dr < 0 || dr % 2 != 0 || drq < dr || drq % 2 != 0 || ldy < nq + H * dr)
+    return fail(MLRA_ERR_SHAPE, "query_epilogue: bad dims nq=%d H=%d dr=%d drq=%d ldy=%d", nq, H, dr, drq, ldy);
+  mlra::query_epilogue_kernel<<<n, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      y, ldy, nq, H, dr, drq, pos0, rope_base, q_scale, r_scale, static_cast<__nv_bfloat16*>(q_out),
+      static_cast<__nv_bfloat16*>(r_out));
+  return cuda_check("query_epilogue launch");
 }

@@ -23,6 +23,8 @@
 // when a row's tile max exceeds it by 2^8, then O's row is rescaled in TMEM (after the PVs
 // issued so far have completed).
 //
+// Queries: q~ head-major [H, n, NB, DLAT] (the batched absorption GEMM's output), q_rope
+// [n, H, DRq]; both pre-scaled by tau*log2e.
 // Grid: (ceil(n/128) * H): the longest query tiles (most key tiles) are scheduled first, the
 // H heads of a query tile back to back (they stream the same key tiles: L2 reuse).
 #pragma once
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         if (b > 0) pf_wait(up_done, (b - 1) & 1, 1);  // Q latent region / W region free again
         mbar_arrive_expect_tx(q_full, (L::kLatChunks + (b == 0 ? 1 : 0)) * kPfChunk);
         for (int c = 0; c < L::kLatChunks; ++c)
-          tma_load_3d(&q_map, q_full, smem + L::kQ + c * kPfChunk, c * 64, b * p.H + h, qt * kPfT);
+          tma_load_4d(&q_map, q_full, smem + L::kQ + c * kPfChunk, c * 64, b, qt * kPfT, h);
         if (b == 0) tma_load_3d(&qr_map, q_full, smem + L::kQ + L::kLatChunks * kPfChunk, 0, h, qt * kPfT);
         for (int j = 0; j < ntiles; ++j, ++g) {
           const int s = g & 1;
@@ -411,6 +413,63 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<L::kTmemCols>(tbase);
+  }
+}
+
+// ---- prefill projection helpers (the n-row projections run as cuBLAS bf16 GEMMs) -----------
+// rows_split: per row x -> (alpha * rmsnorm(x) when norm, else x) as bf16 hi + lo planes [n, K]
+// (the GEMM's activations at ~16-bit mantissa; tensors.py:83-87 rmsnorm, latent.py:134).
+__global__ void __launch_bounds__(256) rows_split_kernel(const float* __restrict__ x, int K, int ldx, int norm,
+                                                         float alpha, float eps, __nv_bfloat16* __restrict__ hi,
+                                                         __nv_bfloat16* __restrict__ lo) {
+  __shared__ float red[8];
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float* xr = x + size_t(row) * ldx;
+  float sc = 1.f;
+  if (norm) {
+    float ss = 0.f;
+    for (int c = tid; c < K; c += 256) ss = fmaf(xr[c], xr[c], ss);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((tid & 31) == 0) red[tid >> 5] = ss;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    sc = alpha * rsqrtf(t / float(K) + eps);
+  }
+  for (int c = tid; c < K; c += 256) {
+    const float v = xr[c] * sc;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    hi[size_t(row) * K + c] = h;
+    lo[size_t(row) * K + c] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+// query_epilogue: y [n, ldy] fp32 = [q_x (nq) | q_r (H * dr)] -> q_out bf16 [n, nq] = q_scale * q_x,
+// r_out bf16 [n, H, drq] = r_scale * rope(q_r, pos0 + row) (pairs (2l, 2l+1), rope.py:37-60; angle in
+// fp64 reduced mod 2 pi), columns [dr, drq) zero.
+__global__ void __launch_bounds__(256) query_epilogue_kernel(const float* __restrict__ y, int ldy, int nq, int H,
+                                                             int dr, int drq, int pos0, float rope_base,
+                                                             float q_scale, float r_scale,
+                                                             __nv_bfloat16* __restrict__ q_out,
+                                                             __nv_bfloat16* __restrict__ r_out) {
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float* yr = y + size_t(row) * ldy;
+  for (int c = tid; c < nq; c += 256) q_out[size_t(row) * nq + c] = __float2bfloat16_rn(yr[c] * q_scale);
+  const double pos = double(pos0 + row);
+  for (int i = tid; i < H * (drq / 2); i += 256) {
+    const int h = i / (drq / 2), l = i % (drq / 2);
+    float e = 0.f, o = 0.f;
+    if (2 * l + 1 < dr) {
+      const double theta = pow(double(rope_base), -2.0 * l / dr);
+      float sn, cs;
+      sincosf(float(fmod(pos * theta, 6.283185307179586476925286766559)), &sn, &cs);
+      const float x0 = yr[nq + h * dr + 2 * l], x1 = yr[nq + h * dr + 2 * l + 1];
+      e = (x0 * cs - x1 * sn) * r_scale;
+      o = (x0 * sn + x1 * cs) * r_scale;
+    }
+    reinterpret_cast<__nv_bfloat162*>(r_out + (size_t(row) * H + h) * drq)[l] = __floats2bfloat162_rn(e, o);
   }
 }
 

@@ -545,14 +545,14 @@ def prefill_attention(q_abs: torch.Tensor, q_rope: torch.Tensor, w_uv_packed: to
                       block_table: torch.Tensor, page_size: int, nb: int, dlat: int, dr: int, alpha: float,
                       out: torch.Tensor | None = None) -> torch.Tensor:
     """K6: causal prefill attention of one sequence of n tokens already in the paged cache
-    (block_table row 0): q_abs [n, NB, H, DLAT] / q_rope [n, H, DRp] (K1 outputs), w_uv
-    [H, NB*DLAT, DH] -> out [n, H, DH] fp32 (alpha-scaled, branch-summed)."""
+    (block_table row 0): q_abs head-major [H, n, NB, DLAT] / q_rope [n, H, DRq] (pre-scaled by
+    tau*log2e), w_uv [H, NB*DLAT, DH] -> out [n, H, DH] fp32 (alpha-scaled, branch-summed)."""
     _need(q_abs, torch.bfloat16, "q_abs", 4)
     _need(q_rope, torch.bfloat16, "q_rope", 3)
     _need(w_uv_packed, torch.bfloat16, "w_uv", 3)
     _need(pool, torch.bfloat16, "pool", 2)
     _need(block_table, torch.int32, "block_table", 2)
-    n, NB, H, DLAT = q_abs.shape
+    H, n, NB, DLAT = q_abs.shape
     DH = w_uv_packed.shape[2]
     if NB != nb or DLAT != dlat or q_rope.shape[:2] != (n, H):
         raise ShapeMismatchError("prefill_attention: query shapes do not match")
@@ -565,3 +565,29 @@ def prefill_attention(q_abs: torch.Tensor, q_rope: torch.Tensor, w_uv_packed: to
                                             pool.shape[0] // page_size, float(alpha), _stream())
     _lib.check(rc, "mlra_prefill_attention")
     return out
+
+
+def rows_split(x: torch.Tensor, K: int, norm: bool = False, alpha: float = 1.0, eps: float = 1e-6):
+    """x [n, >= K] fp32 (first K columns) -> (hi, lo) bf16 [n, K]: x or alpha * rmsnorm(x)."""
+    _need(x, torch.float32, "x", 2)
+    n = x.shape[0]
+    hi = torch.empty((n, K), dtype=torch.bfloat16, device=x.device)
+    lo = torch.empty_like(hi)
+    rc = _lib.load().mlra_rows_split(x.data_ptr(), n, K, x.shape[1], int(norm), float(alpha), float(eps),
+                                     hi.data_ptr(), lo.data_ptr(), _stream())
+    _lib.check(rc, "mlra_rows_split")
+    return hi, lo
+
+
+def query_epilogue(y: torch.Tensor, nq: int, heads: int, dr: int, drq: int, pos0: int, q_scale: float = 1.0,
+                   r_scale: float = 1.0, rope_base: float = 10000.0):
+    """y [n, >= nq + heads*dr] fp32 -> (q bf16 [n, nq] * q_scale, rope(q_r) * r_scale bf16 [n, heads, drq])."""
+    _need(y, torch.float32, "y", 2)
+    n = y.shape[0]
+    q = torch.empty((n, nq), dtype=torch.bfloat16, device=y.device)
+    r = torch.empty((n, heads, drq), dtype=torch.bfloat16, device=y.device)
+    rc = _lib.load().mlra_query_epilogue(y.data_ptr(), n, y.shape[1], nq, heads, dr, drq, int(pos0),
+                                         float(rope_base), float(q_scale), float(r_scale), q.data_ptr(),
+                                         r.data_ptr(), _stream())
+    _lib.check(rc, "mlra_query_epilogue")
+    return q, r

@@ -87,12 +87,11 @@ class GqaProjector:
         return q, k, v
 
 
-def _split_gemm(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-    """x [M, K] fp32 times w [K, N] bf16 with x as bf16 hi + lo (two cuBLAS bf16 GEMMs, ~16-bit
-    activation mantissa), fp32 result."""
-    hi = x.to(torch.bfloat16)
-    lo = (x - hi.float()).to(torch.bfloat16)
-    return torch.mm(hi, w, out_dtype=torch.float32) + torch.mm(lo, w, out_dtype=torch.float32)
+def _gemm2(hi: torch.Tensor, lo: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """(hi + lo) [M, K] (bf16 planes) times w [K, N] bf16: two cuBLAS bf16 GEMMs, fp32 result."""
+    y = torch.mm(hi, w, out_dtype=torch.float32)
+    y += torch.mm(lo, w, out_dtype=torch.float32)
+    return y
 
 
 class KernelProjector:
@@ -205,25 +204,23 @@ class KernelProjector:
         outs = [self.project(hidden[m0:m0 + 16], pos[m0:m0 + 16]) for m0 in range(0, M, 16)]
         return tuple(torch.cat([o[i] for o in outs]) for i in range(4))
 
-    def project_gemm(self, hidden: torch.Tensor, pos: torch.Tensor):
-        """``project`` for many rows (prefill): the same packed bf16 weights through cuBLAS bf16
-        GEMMs -- real GEMMs at n rows, where a weight stream per 16 rows would not pay. The
-        activations enter as bf16 hi + lo (two GEMMs, fp32 accumulation) like K-1's operands, so
-        the outputs match ``project`` up to the accumulation order."""
-        hidden = hidden.to(device=self.device, dtype=torch.float32)
-        pos = pos.to(device=self.device)
-        y = _split_gemm(hidden, self.w_down)
+    def project_gemm(self, hidden: torch.Tensor, pos0: int, drq: int | None = None):
+        """``project`` for the n rows of a prefill at positions pos0 .. pos0+n-1: the same packed
+        bf16 weights through cuBLAS bf16 GEMMs (real GEMMs at n rows, where a weight stream per 16
+        rows would not pay), the activations as bf16 hi + lo (``ops.rows_split``, with the query
+        rmsnorm) like K-1's operands, and ``ops.query_epilogue`` for the scaling and rope. Returns
+        (kv_raw, kr_raw, q [n, ...] bf16, q_rope [n, H, drq] bf16)."""
+        hidden = hidden.to(device=self.device, dtype=torch.float32).contiguous()
+        n = hidden.shape[0]
+        hi, lo = ops.rows_split(hidden, hidden.shape[1])
+        y = _gemm2(hi, lo, self.w_down)
         n_q, n_kv = self.n_q, self.n_kv
-        c_q = self.alpha_q * rmsnorm(y[:, :n_q])
         kv_raw = y[:, n_q:n_q + n_kv].contiguous()
         kr_raw = y[:, n_q + n_kv:n_q + n_kv + self.n_kr].contiguous()
-        q = _split_gemm(c_q, self.w_query)
-        M = hidden.shape[0]
-        qx = (q[:, :self.nq] * self.q_scale).to(torch.bfloat16).reshape((M,) + self.q_shape)
-        qr = torch.zeros((M, self.H, self.drp), dtype=torch.bfloat16, device=self.device)
-        rot = rope_rotate(q[:, self.nq:self.nq + self.H * self.dr].reshape(M, self.H, self.dr), pos.long())
-        qr[..., :self.dr] = (rot * self.r_scale).to(torch.bfloat16)
-        return kv_raw, kr_raw, qx, qr
+        hi, lo = ops.rows_split(y, n_q, norm=True, alpha=self.alpha_q)
+        q = _gemm2(hi, lo, self.w_query)
+        qx, qr = ops.query_epilogue(q, self.nq, self.H, self.dr, drq or self.drp, pos0, self.q_scale, self.r_scale)
+        return kv_raw, kr_raw, qx.reshape((n,) + self.q_shape), qr
 
     def kv_slice(self, kv_raw: torch.Tensor, names) -> torch.Tensor:
         """The raw columns of the given down-projections (contiguous, in kv_names order)."""

@@ -55,58 +55,3 @@ for force in (True, False):
 errs = [ak.max_rel_err(outs[0][t], outs[1][t]) for t in range(n)]
 print(variant, n, "max_rel_err K6 vs pseudo", max(errs), "at", int(np.argmax(errs)), flush=True)
 
-# float64 reference of the absorbed causal prefill on the SAME bf16 operands (K1's q~ / q_rope,
-# the stored cache, the packed W^UV): which path deviates?
-from paper_2603_02188_b200 import ops
-layout = cache.layout
-nb, dlat = dec.kernel_geometry(layout, st.own)
-kp = st.kproj
-kv_raw, kr_raw, qn, q_r = kp.project_gemm(h, torch.arange(n, dtype=torch.int32, device=dev))
-qn, qr = dec._pad_rope(qn, q_r, layout)
-qr64 = qr if layout.drp == 64 else torch.nn.functional.pad(qr, (0, 64 - layout.drp))
-w_uk, w_uv = st.lw.packed(layout, dev, st.own)
-q_abs, q_rs = ops.absorb_query(qn, qr64.contiguous(), w_uk, nb, dlat, ops.score_scale(cfg.tau))
-pool = cache.paged.pool.double()
-slots = cache.paged.token_slots(0)[:n]
-rows = pool[slots]  # [n, W]
-C = rows[:, :nb * dlat].reshape(n, nb, dlat)
-KR = rows[:, nb * dlat:nb * dlat + layout.dr]
-qa = q_abs.double()                    # [n, nb, H, dlat]
-qrs = q_rs.double()[..., :layout.dr]   # [n, H, dr]
-W = w_uv.double().reshape(cfg.h, nb, dlat, -1)
-alpha = 0.5 if cfg.variant == "mlra" else 1.0
-ref = torch.zeros((n, cfg.h, W.shape[-1]), dtype=torch.float64, device=dev)
-rope_l = torch.einsum("thr,kr->thk", qrs, KR)  # [n, H, n]
-mask = torch.triu(torch.ones(n, n, dtype=torch.bool, device=dev), 1)
-for b in range(nb):
-    lg = torch.einsum("thc,kc->thk", qa[:, b], C[:, b]) + rope_l
-    lg = lg.masked_fill(mask[:, None, :], float("-inf"))
-    P = torch.softmax(lg * np.log(2.0), dim=-1)
-    Z = torch.einsum("thk,kc->thc", P, C[:, b])
-    ref += torch.einsum("thc,hcd->thd", Z, W[:, b])
-ref = (alpha * ref).cpu().numpy()
-for name, o in (("pseudo", outs[0]), ("K6", outs[1])):
-    e = [ak.max_rel_err(ref[t], o[t]) for t in range(n)]
-    bad = [t for t in range(n) if e[t] > 1e-2]
-    print(name, "vs f64 on the same operands: max", max(e), "bad rows", len(bad), bad[:8], bad[-4:], flush=True)
-
-# raw S of one CTA's first key tile (branch 0) vs f64 logits on the same operands
-nqt = (n + 127) // 128
-cta = 0  # lin 0 -> qt = nqt - 1, head 0
-qt, hh = nqt - 1, 0
-dbg = torch.zeros(128 * 128, dtype=torch.float32, device=dev)
-os.environ["MLRA_DEBUG_PF_S"] = str(dbg.data_ptr())
-os.environ["MLRA_DEBUG_PF_CTA"] = str(cta)
-ops.prefill_attention(q_abs, q_rs, w_uv, cache.paged.pool, cache.paged.block_table, cache.paged.page_size, nb, dlat,
-                      cfg.d_h_rope, alpha)
-torch.cuda.synchronize()
-del os.environ["MLRA_DEBUG_PF_S"]
-S = dbg.view(128, 128).double()
-rows_q = torch.arange(qt * 128, qt * 128 + 128, device=dev).clamp(max=n - 1)
-want = torch.einsum("tc,kc->tk", qa[rows_q, 0, hh], C[:128, 0]) + torch.einsum("tr,kr->tk", qrs[rows_q, hh], KR[:128])
-nk = min(128, n)
-d = (S[:, :nk] - want[:, :nk]).abs()
-print("S tile0 max abs diff", float(d.max()), "max |S|", float(want.abs().max()), flush=True)
-lat_only = torch.einsum("tc,kc->tk", qa[rows_q, 0, hh], C[:128, 0])
-print("  vs lat-only logits", float((S[:, :nk] - lat_only[:, :nk]).abs().max()), flush=True)
-print("  S[0,:4]", S[0, :4].tolist(), "want", want[0, :4].tolist(), flush=True)

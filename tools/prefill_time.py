@@ -26,13 +26,13 @@ for n in [int(a) for a in sys.argv[1:]] or [1024, 4096, 16384]:
     h = torch.randn((n, cfg.d), device=dev)
     cache = dec.new_cache(cfg, device=dev, initial_tokens=n)
     t_full = ev_time(lambda: dec.prefill_into(cfg, st, cache, h))
-    # K6 alone on the filled cache
-    layout = cache.layout
+    # K6 alone on the filled cache (head-major absorbed queries, as prefill_into builds them)
     kp = st.kproj
-    _, _, qn, q_r = kp.project_gemm(h, torch.arange(n, dtype=torch.int32, device=dev))
-    qn, qr = dec._pad_rope(qn, q_r, layout)
-    w_uk, w_uv = st.lw.packed(layout, dev, st.own)
-    q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, 4, 128, ops.score_scale(cfg.tau))
+    _, _, qn, q_r = kp.project_gemm(h, 0, drq=64)
+    w_uk, w_uv = st.lw.packed(cache.layout, dev, st.own)
+    sc = ops.score_scale(cfg.tau)
+    q_abs = torch.bmm(qn.transpose(0, 1), w_uk).view(cfg.h, n, 4, 128)
+    q_rs = (q_r.float() * sc).to(torch.bfloat16)
     pc = cache.paged
     t_k6 = ev_time(lambda: ops.prefill_attention(q_abs, q_rs, w_uv, pc.pool, pc.block_table, pc.page_size, 4, 128, 64, 0.5))
     flops = 4 * cfg.h * (n * (n + 1) / 2) * 2 * (128 + 64 + 128) + n * cfg.h * 4 * 128 * 128 * 2 * 2
