@@ -50,6 +50,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def peaks_bf16():
+    """Measured dense bf16 TFLOP/s (MEASURED_PEAKS.json, burst) or the guide's 2250 nominal."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
 def ncu_traffic(workload: str):
     """dram read+write bytes per launch of K2 from the committed ncu capture, if present."""
     try:
@@ -112,7 +121,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workloads
-def make_engine(cfg, own, batch, ctx, seed, device, page_size=128, weights=None):
+def make_engine(cfg, own, batch, ctx, seed, device, page_size=128, weights=None, ragged=False):
     """DecodeEngine with a synthetic cache filled on the device (RMS like the reference's rows)."""
     import torch
 
@@ -129,7 +138,8 @@ def make_engine(cfg, own, batch, ctx, seed, device, page_size=128, weights=None)
     else:
         w = {"w_uk": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02,
              "w_uv": rng.standard_normal((cfg.d_c, cfg.h * cfg.d_h)) * 0.02}
-    eng = DecodeEngine(cfg, w, own, batch=batch, max_tokens=ctx + 64, page_size=page_size, device=device)
+    eng = DecodeEngine(cfg, w, own, batch=batch, max_tokens=ctx + 64, page_size=page_size, device=device,
+                       ragged=ragged)
     lay = eng.layout
     akv = calib_factors(cfg).alpha_kv
     # rope ~ N(0, d * sigma^2) ~ N(0, 1.2) at d = 3072, sigma = 0.02
@@ -319,6 +329,94 @@ def time_k2_alone(eng_qs, iters):
     e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / (reps * per)
+
+
+RAGGED_LENS = [int(1024 * 64 ** (i / 15)) for i in range(16)]  # 1K .. 64K, geometric
+
+
+def ragged_times(device, args):
+    """A ragged batch (16 sequences, 1K..64K tokens, geometric) on one TP4 rank: the uniform split
+    grid (every sequence nsplit = 9 CTAs) against the device-side plan (mlra_decode_plan: the
+    sequences' tiles balanced over one wave of CTAs). Two engines per mode alternate (L2-cold)."""
+    import torch
+
+    from paper_2603_02188_b200.config import trained_config
+    from paper_2603_02188_b200.costs import algorithmic_bytes
+    from paper_2603_02188_b200.tp import shard_ownership
+
+    cfg = trained_config("mlra4")
+    own = shard_ownership(cfg, 4, 0)
+    nbytes = algorithmic_bytes(cfg, 4, RAGGED_LENS)
+    res = {"lens": RAGGED_LENS, "algorithmic_bytes": nbytes}
+    for mode in ("uniform", "plan"):
+        engs = []
+        for seed in (21, 22):
+            eng, qn, qr = make_engine(cfg, own, len(RAGGED_LENS), max(RAGGED_LENS), seed, device,
+                                      ragged=(mode == "plan"))
+            eng.cache.seqlens.copy_(torch.tensor(RAGGED_LENS, dtype=torch.int32))
+            eng.cache._host_lens = list(RAGGED_LENS)
+            engs.append((eng, qn, qr))
+        for eng, qn, qr in engs:
+            eng.decode_attention(qn, qr)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+            for i in range(10):
+                eng, qn, qr = engs[i % 2]
+                eng.decode_attention(qn, qr)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 50 * 1e3
+        res[mode] = {"us_per_step": round(us, 2), "gbs": round(nbytes / (us * 1e-6) / 1e9, 1),
+                     "nsplit": engs[0][0].nsplit}
+        del engs, g
+        torch.cuda.empty_cache()
+    res["speedup"] = round(res["uniform"]["us_per_step"] / res["plan"]["us_per_step"], 3)
+    return res
+
+
+def time_paper_scope(eng_qs, iters=40):
+    """The paper's decode-attention scope (Eq. step-2 decoding): absorbed queries in,
+    latent mixture Z out -- K2 + the split merge (K3 with upproj = 0), no absorption (Step 1) and no
+    W^UV up-projection (Step 3). One CUDA graph of 10 steps alternating the two caches."""
+    import torch
+
+    from paper_2603_02188_b200 import ops
+
+    preps = []
+    for eng, qn, qr in eng_qs:
+        q_abs, q_rs = ops.absorb_query(qn, qr, eng.w_uk, eng.nb, eng.dlat, eng.scale)
+        c = eng.cache
+        parts = ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub,
+                                    eng.dls, eng.nsplit)
+        z = ops.combine(*parts, None, 1.0)
+        preps.append((eng, q_abs, q_rs, parts, z))
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for i in range(10):
+            eng, q_abs, q_rs, parts, z = preps[i % 2]
+            c = eng.cache
+            ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub,
+                                eng.dls, eng.nsplit, out=parts)
+            ops.combine(*parts, None, 1.0, out=z)
+    g.replay()
+    torch.cuda.synchronize()
+    reps = max(1, iters // 10)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * 10)
 
 
 def e2e_steps(engines, steps, warmup, reducer=None, rank_sync=None):
@@ -726,8 +824,10 @@ def per_gpu_comparisons(cfg, device, args):
         r = StepRunner(c, own, BATCH_PER_GROUP, CTX, device)
         ms = median_ms(r, args)
         nbytes = algorithmic_bytes(c, phi, [CTX] * BATCH_PER_GROUP)
+        ps = time_paper_scope(r.engines)
         res[name] = {"us_per_step": round(ms * 1e3, 2), "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
-                     "algorithmic_bytes": nbytes}
+                     "algorithmic_bytes": nbytes, "paper_scope_us": round(ps * 1e3, 2),
+                     "paper_scope_gbs": round(nbytes / (ps * 1e-3) / 1e9, 1)}
         del r
         torch.cuda.empty_cache()
     out["tp4_per_gpu"] = res["mlra4_tp4_rank"]
@@ -737,6 +837,14 @@ def per_gpu_comparisons(cfg, device, args):
         "speedup_per_gpu_tp4": round(res["mla_tp4_rank"]["us_per_step"] / res["mlra4_tp4_rank"]["us_per_step"], 3),
         "mla_tp1_us": res["mla_tp1"]["us_per_step"], "mla_tp1_gbs": res["mla_tp1"]["gbs"],
         "paper_claim": "~2.8x (H100, FlashMLA vs FA3-based MLRA-4)", "traffic_ratio": 3.0,
+        "paper_scope": {
+            "what": "the paper's decode-attention scope (PAPER.md:551, Eq. step-2): absorbed queries in, latent "
+                    "mixture out = K2 + split merge, without the W^UK absorption (Step 1) and the W^UV "
+                    "up-projection (Step 3)",
+            "mlra4_tp4_rank_us": res["mlra4_tp4_rank"]["paper_scope_us"],
+            "mla_tp4_rank_us": res["mla_tp4_rank"]["paper_scope_us"],
+            "speedup_per_gpu_tp4": round(res["mla_tp4_rank"]["paper_scope_us"] /
+                                         res["mlra4_tp4_rank"]["paper_scope_us"], 3)},
     }
     # GQA baseline (2.9B, g=6: K and V heads, 3072 B/token at TP1, 1536 B/token per TP2 rank)
     gqa = trained_config("gqa")
@@ -769,6 +877,7 @@ def per_gpu_comparisons(cfg, device, args):
         "traffic_ratio_gqa_tp2_rank_vs_mlra4_tp4_rank": 4.0,
     }
     out["layer"] = layer_times(device, args)
+    out["ragged"] = ragged_times(device, args)
     out["output_side"] = output_side_times(device)
     out["prefill"] = prefill_times(device)
     return out
@@ -890,11 +999,15 @@ def layer_times(device, args):
 
 
 def prefill_times(device):
-    """latent_prefill's device part (K0 over all tokens + K1..K3 over n prefix pseudo-sequences)
-    for one 2.9B MLRA-4 sequence at TP1, in tokens/s (random weights, one warm-up pass)."""
+    """latent_prefill's device part for one 2.9B MLRA-4 sequence at TP1 (random weights): the n-row
+    projections (cuBLAS bf16 + fused split / rope epilogues), K0 over all tokens, the batched
+    absorption GEMM and K6 (tcgen05 causal prefill); K6 alone against the measured bf16 tensor peak
+    (algorithmic FLOPs: 2*(d_lat + d_rope + d_lat) per causal (query, key) pair per head and branch,
+    plus the in-kernel W^UV up-projection); and the previous n-pseudo-sequence decode path at 4096."""
     import torch
 
     from paper_2603_02188_b200 import decode as dec
+    from paper_2603_02188_b200 import ops
     from paper_2603_02188_b200.config import trained_config
     from paper_2603_02188_b200.weights import weight_shapes
 
@@ -902,21 +1015,44 @@ def prefill_times(device):
     rng = np.random.default_rng(0)
     w = {name: rng.standard_normal(shape) * 0.02 for name, shape in weight_shapes(cfg).items()}
     st = dec._state(cfg, w, device)
-    res = {}
-    for n in (1024, 4096):
-        h_t = torch.randn((n, cfg.d), device=device)
-        times = []
-        for rep in range(3):
-            cache = dec.new_cache(cfg, device=device, initial_tokens=n)
+    tflops_peak = peaks_bf16()
+
+    def ev(fn, reps=3):
+        ts = []
+        for _ in range(reps):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            dec.prefill_into(cfg, st, cache, h_t)
+            fn()
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        ms = min(times[1:])
-        res[f"n{n}"] = {"ms": round(ms, 3), "tokens_per_s": round(n / (ms * 1e-3), 1)}
+            ts.append(e0.elapsed_time(e1))
+        return min(ts[1:])
+
+    res = {}
+    for n in (1024, 4096, 16384):
+        h_t = torch.randn((n, cfg.d), device=device)
+        cache = dec.new_cache(cfg, device=device, initial_tokens=n)
+        ms = ev(lambda: dec.prefill_into(cfg, st, cache, h_t))
+        kp = st.kproj
+        _, _, qn, q_r = kp.project_gemm(h_t, 0, drq=64)
+        w_uk, w_uv = st.lw.packed(cache.layout, device, st.own)
+        q_abs = torch.bmm(qn.transpose(0, 1), w_uk).view(cfg.h, n, 4, 128)
+        q_rs = (q_r.float() * ops.score_scale(cfg.tau)).to(torch.bfloat16)
+        pc = cache.paged
+        k6 = ev(lambda: ops.prefill_attention(q_abs, q_rs, w_uv, pc.pool, pc.block_table, pc.page_size, 4, 128, 64,
+                                              0.5))
+        flops = 4 * cfg.h * (n * (n + 1) / 2) * 2 * (128 + 64 + 128) + n * cfg.h * 4 * 128 * 128 * 2 * 2
+        row = {"ms": round(ms, 3), "tokens_per_s": round(n / (ms * 1e-3), 1), "k6_ms": round(k6, 3),
+               "k6_tflops": round(flops / (k6 * 1e-3) / 1e12, 1),
+               "k6_frac_of_bf16_peak": round(flops / (k6 * 1e-3) / 1e12 / tflops_peak, 3)}
+        if n == 4096:
+            row["pseudo_sequence_path_ms"] = round(ev(lambda: dec.prefill_into(cfg, st, cache, h_t,
+                                                                               force_pseudo=True), reps=2), 3)
+        res[f"n{n}"] = row
+        del cache
+        torch.cuda.empty_cache()
+    res["roofline"] = {"bound": "tensor", "peak_tflops": tflops_peak, "peak_kind": "measured cuBLAS bf16 (burst)"}
     return res
 
 

@@ -109,6 +109,9 @@ int mlra_check_status(int32_t* status, int reset, void* stream);
 
 /* Split count used when the caller passes nsplit <= 0 (fills the SMs for this batch). */
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB);
+/* The same for H heads per device: K2's grid has ceil(H / head-group width) head groups, so one
+ * wave needs nsplit * B * groups <= #SMs. */
+int mlra_default_splits_heads(int B, int max_seqlen, int NB, int SUB, int H);
 
 /*
  * K2 -- split-KV flash-decode over the paged latent cache (tcgen05 + TMA).
@@ -309,6 +312,26 @@ int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, float alpha
                     void* stream);
 int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H, int dr, int drq, int pos0, float rope_base,
                         float q_scale, float r_scale, void* q_out, void* r_out, void* stream);
+
+/*
+ * Ragged batches (sequences of very different lengths; attnkit/decode.py:204-230 decodes any
+ * length). mlra_decode_plan builds K2's work table on the device (graph-safe): the tile budget
+ * per CTA is the smallest c >= ceil(total tiles / ctas) for which the per-sequence split counts
+ * ns_s = max(1, ceil(tiles_s / c)) (<= nsplit_max) fit `ctas` CTAs; sequence s gets ns_s
+ * consecutive splits, items in ascending (sequence, split) order (the merge's order), surplus
+ * items {-1, ...} (lse_part is not touched: the merge reads only the ns_s slots of a sequence).
+ *   plan [ctas][4] int32 {sequence, split, first tile, tiles}; seq_splits [B] int32 = ns_s (the
+ *   merge reads only those slots); tile_tokens = 128 (64 for MLA).
+ * mlra_decode_step_ragged: mlra_decode_step with that plan (K2 grid = one wave of planned CTAs
+ * per head group; K3 merges up to nsplit_max slots per sequence). w_uk == NULL: pre-absorbed
+ * queries as in mlra_decode_step. Workspace: mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit_max).
+ */
+int mlra_decode_plan(const int32_t* seqlens, int B, int tile_tokens, int ctas, int nsplit_max, int32_t* plan,
+                     int32_t* seq_splits, float* lse_part, int NB, int H, void* stream);
+int mlra_decode_step_ragged(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,
+                            const void* pool, const int32_t* block_table, const int32_t* seqlens, float* out,
+                            void* workspace, int B, int H, int DH, int NB, int SUB, int DLS, int DR, int page_size,
+                            int max_pages, int num_pages, int nsplit_max, float score_scale, float alpha, void* stream);
 
 #ifdef __cplusplus
 }

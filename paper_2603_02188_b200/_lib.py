@@ -32,6 +32,7 @@ SIGNATURES = {
     "mlra_absorb_query": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P]),
     "mlra_workspace_bytes": (ctypes.c_size_t, [_I, _I, _I, _I, _I, _I]),
     "mlra_default_splits": (_I, [_I, _I, _I, _I]),
+    "mlra_default_splits_heads": (_I, [_I, _I, _I, _I, _I]),
     "mlra_decode_partials": (_I, [_P] * 7 + [_I] * 10 + [_P]),
     "mlra_combine": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _I, _P, _P]),
     "mlra_check_status": (_I, [_P, _I, _P]),
@@ -56,6 +57,8 @@ SIGNATURES = {
     "mlra_prefill_attention": (_I, [_P] * 6 + [_I] * 11 + [_F, _P]),
     "mlra_rows_split": (_I, [_P] + [_I] * 4 + [_F, _F, _P, _P, _P]),
     "mlra_query_epilogue": (_I, [_P] + [_I] * 7 + [_F, _F, _F, _P, _P, _P]),
+    "mlra_decode_plan": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
+    "mlra_decode_step_ragged": (_I, [_P] * 9 + [_I] * 11 + [_F, _F, _P]),
     "mlra_proj_down": (_I, [_P, _P] + [_I] * 5 + [_P] * 5),
     "mlra_proj_query": (_I, [_P, _P, _F, _F, _P] + [_I] * 6 + [_P, _I, _F, _F, _F, _P, _P, _P]),
 }

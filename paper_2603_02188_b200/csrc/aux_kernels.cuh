@@ -216,69 +216,167 @@ inline size_t head_gemm_smem(int kp) {
   return ((size_t(kp) * NT * 2 + 15) / 16) * 16 + size_t(kHG_S) * kp * 4;
 }
 
+// ----------------------------------------------------------------------------- K2 plan
+// Ragged-batch split scheduler (mlra_decode_plan): a deterministic work table for K2 that
+// balances the token tiles of B sequences of any lengths over `ctas` CTAs (one wave per head
+// group). The smallest per-CTA tile budget c >= ceil(total / ctas) is searched such that the
+// per-sequence split counts ns_s = max(1, ceil(tiles_s / c)) (<= nsplit_max) fit the CTAs;
+// sequence s gets ns_s consecutive splits of ceil(tiles_s / ns_s) tiles (items in ascending
+// (sequence, split) order: the merge adds the splits in that order). seq_splits[s] = ns_s: the
+// merge reads only those slots. One CTA.
+constexpr int kPlanThreads = 256;
+__global__ void __launch_bounds__(kPlanThreads)
+decode_plan_kernel(const int32_t* __restrict__ seqlens, int B, int T, int ctas, int nsplit_max,
+                   int32_t* __restrict__ plan, int32_t* __restrict__ seq_splits, float* __restrict__ lse_part,
+                   int NB, int H) {
+  extern __shared__ int pl_smem[];
+  int* tiles = pl_smem;           // [B]
+  int* ns = pl_smem + B;          // [B]
+  __shared__ int red_i[kPlanThreads / 32];
+  __shared__ int s_total, s_max, s_c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto block_sum = [&](int v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red_i[warp] = v;
+    __syncthreads();
+    int t = 0;
+    for (int w = 0; w < kPlanThreads / 32; ++w) t += red_i[w];
+    __syncthreads();
+    return t;
+  };
+  int loc = 0, mx = 0;
+  for (int s = tid; s < B; s += kPlanThreads) {
+    const int t = (max(seqlens[s], 0) + T - 1) / T;
+    tiles[s] = t;
+    loc += t;
+    mx = max(mx, t);
+  }
+  const int total = block_sum(loc);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red_i[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    int m = 0;
+    for (int w = 0; w < kPlanThreads / 32; ++w) m = max(m, red_i[w]);
+    s_total = total;
+    s_max = m;
+  }
+  __syncthreads();
+  // binary search of the tile budget c: feasible(c) <=> sum_s max(1, ceil(tiles_s / c)) <= ctas and
+  // every ceil(tiles_s / c) <= nsplit_max (monotone in c)
+  int lo = max(1, (s_total + ctas - 1) / ctas), hi = max(lo, s_max);
+  while (lo < hi) {
+    const int c = (lo + hi) / 2;
+    int cnt = 0, bad = 0;
+    for (int s = tid; s < B; s += kPlanThreads) {
+      const int k = max(1, (tiles[s] + c - 1) / c);
+      cnt += k;
+      bad += k > nsplit_max;
+    }
+    cnt = block_sum(cnt);
+    bad = block_sum(bad);
+    if (cnt <= ctas && bad == 0) hi = c; else lo = c + 1;
+  }
+  if (tid == 0) s_c = lo;
+  __syncthreads();
+  const int c = s_c;
+  for (int s = tid; s < B; s += kPlanThreads) ns[s] = min(nsplit_max, max(1, (tiles[s] + c - 1) / c));
+  __syncthreads();
+  // item offsets: exclusive prefix sum of ns over the sequences (serial: B is small)
+  if (tid == 0) {
+    int acc = 0;
+    for (int s = 0; s < B; ++s) {
+      const int k = ns[s];
+      ns[s] = acc;  // offset
+      tiles[s] |= k << 20;  // (keep the count next to the tiles: tiles < 2^20)
+      acc += k;
+    }
+    s_total = acc;
+  }
+  __syncthreads();
+  for (int s = tid; s < B; s += kPlanThreads) {
+    const int t = tiles[s] & ((1 << 20) - 1), k = tiles[s] >> 20, off = ns[s];
+    const int per = (t + k - 1) / max(k, 1);
+    seq_splits[s] = k;
+    for (int j = 0; j < k; ++j) {
+      int32_t* it = plan + size_t(off + j) * 4;
+      it[0] = s;
+      it[1] = j;
+      it[2] = j * per;
+      it[3] = max(0, min(per, t - j * per));
+    }
+  }
+  for (int i = s_total + tid; i < ctas; i += kPlanThreads) plan[size_t(i) * 4] = -1;
+}
+
 // ----------------------------------------------------------------------------- K3a
 // Flash-decoding merge of the K2 split partials: for every (sequence, branch, head) row,
 //   Z = sum_k w_k O_k with w_k = 2^(lse_k - max) / sum_j 2^(lse_j - max).
-// One warp per row: lane k < nsplit computes split k's weight once (shuffled to all
-// lanes), then every lane sums its latent columns over the splits with independent loads.
-// Output [B, H, NB*DLAT] (the K3b input) or, with zout_bnh, [B, NB, H, DLAT] * alpha.
+// CTA = (row, 128 latent columns), 128 threads: warp 0 forms the split weights once (lane k <
+// nsplit, shuffled max / sum) into smem, then every thread merges one column over the splits
+// with 8 loads in flight at a time. Output [B, H, NB*DLAT] (the K3b input) or, with zout_bnh,
+// [B, NB, H, DLAT] * alpha (the latent mixture itself: the paper's decode scope).
 constexpr int kMergeMaxSplits = 160;  // 5 per lane
-__global__ void merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
-                                    float* __restrict__ z, int B, int NB, int H, int DLAT, int nsplit, float alpha,
-                                    int zout_bnh, int* __restrict__ status) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+__global__ void __launch_bounds__(128)
+merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, float* __restrict__ z, int B,
+                    int NB, int H, int DLAT, int nsplit, float alpha, int zout_bnh, int* __restrict__ status,
+                    const int32_t* __restrict__ seq_splits) {
+  __shared__ float wsh[kMergeMaxSplits];
+  const int row = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
   const int lane = threadIdx.x % 32;
-  if (row >= B * NB * H) return;
   const int h = row % H, b = (row / H) % NB, s = row / (H * NB);
-  const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
-  float lk[kMergeMaxSplits / 32];
-  float m = -INFINITY;
+  const int ns = seq_splits != nullptr ? min(seq_splits[s], nsplit) : nsplit;  // splits of this sequence
+  griddep_wait();
+  if (threadIdx.x < 32) {
+    const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
+    float lk[kMergeMaxSplits / 32];
+    float m = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
-    const int k = lane + 32 * j;
-    lk[j] = k < nsplit ? l[size_t(k) * NB * H] : -INFINITY;
-    m = fmaxf(m, lk[j]);
+    for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
+      const int k = lane + 32 * j;
+      lk[j] = k < ns ? __ldcg(l + size_t(k) * NB * H) : -INFINITY;
+      m = fmaxf(m, lk[j]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    {  // numeric status (attnkit/tensors.py:74-78): a NaN logit, or no finite logit in the row
+      bool nan = false;
+#pragma unroll
+      for (int j = 0; j < kMergeMaxSplits / 32; ++j) nan |= lk[j] != lk[j];
+      const bool any_nan = __any_sync(0xffffffffu, nan);
+      if (status != nullptr && lane == 0 && blockIdx.y == 0 && (any_nan || m == -INFINITY))
+        atomicOr(status, (any_nan ? kStatusNaN : 0) | (m == -INFINITY ? kStatusNoFinite : 0));
+    }
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
+      lk[j] = (m == -INFINITY || lk[j] == -INFINITY) ? 0.f : exp2f(lk[j] - m);
+      tot += lk[j];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+    const float inv = tot > 0.f ? 1.f / tot : 0.f;
+#pragma unroll
+    for (int j = 0; j < kMergeMaxSplits / 32; ++j)
+      if (lane + 32 * j < ns) wsh[lane + 32 * j] = lk[j] * inv;
   }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  {  // numeric status (attnkit/tensors.py:74-78): a NaN logit, or no finite logit in the row
-    bool nan = false;
-#pragma unroll
-    for (int j = 0; j < kMergeMaxSplits / 32; ++j) nan |= lk[j] != lk[j];
-    const bool any_nan = __any_sync(0xffffffffu, nan);
-    if (status != nullptr && lane == 0 && (any_nan || m == -INFINITY))
-      atomicOr(status, (any_nan ? kStatusNaN : 0) | (m == -INFINITY ? kStatusNoFinite : 0));
-  }
-  float wk[kMergeMaxSplits / 32], tot = 0.f;
-#pragma unroll
-  for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
-    wk[j] = (m == -INFINITY || lk[j] == -INFINITY) ? 0.f : exp2f(lk[j] - m);
-    tot += wk[j];
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-  const float inv = tot > 0.f ? 1.f / tot : 0.f;
-  const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT;  // split stride NB*H*DLAT
-  float* dst = zout_bnh ? z + ((size_t(s) * NB + b) * H + h) * DLAT : z + (size_t(s) * H + h) * (NB * DLAT) + b * DLAT;
-  const float sc = (zout_bnh ? alpha : 1.f) * inv;
+  __syncthreads();
+  if (c >= DLAT) return;
+  const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
   const size_t sstride = size_t(NB) * H * DLAT;
-  for (int c0 = 0; c0 < DLAT; c0 += 32 * 4) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = 0; k < nsplit; ++k) {
-      const float w = __shfl_sync(0xffffffffu, wk[k >> 5], k & 31);
-      if (w == 0.f) continue;
+  float acc = 0.f;
+  for (int k0 = 0; k0 < ns; k0 += 8) {
+    float v[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = c0 + lane + 32 * j;
-        if (c < DLAT) acc[j] = fmaf(w, o[k * sstride + c], acc[j]);
-      }
-    }
+    for (int j = 0; j < 8; ++j) v[j] = k0 + j < ns ? __ldcg(o + size_t(k0 + j) * sstride) : 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = c0 + lane + 32 * j;
-      if (c < DLAT) dst[c] = acc[j] * sc;
-    }
+    for (int j = 0; j < 8; ++j)
+      if (k0 + j < ns) acc = fmaf(wsh[k0 + j], v[j], acc);
   }
+  float* dst = zout_bnh ? z + ((size_t(s) * NB + b) * H + h) * DLAT : z + (size_t(s) * H + h) * (NB * DLAT) + b * DLAT;
+  dst[c] = acc * (zout_bnh ? alpha : 1.f);
 }
 
 
@@ -483,7 +581,8 @@ template <int SEQS, int THREADS = 256>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS * 2)
 combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                 const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT, int DH,
-                int nsplit, float alpha, int per_branch, const TpSum tp, int* __restrict__ status) {
+                int nsplit, float alpha, int per_branch, const TpSum tp, int* __restrict__ status,
+                const int32_t* __restrict__ seq_splits) {
   static_assert(SEQS == 2 || SEQS == 4 || SEQS == 8, "2, 4 or 8 sequences per CTA");
   constexpr int kQ = THREADS / kG4Cols;  // parts of the contraction per output column
   extern __shared__ __align__(128) uint8_t c4_smem[];
@@ -535,8 +634,9 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
       const int i = i0 + u * THREADS, c = i / SEQS, sq = i % SEQS, s = s0 + sq;
       const bool ok = i < DLAT * SEQS && s < B;
       const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
+      const int ns = (ok && seq_splits != nullptr) ? min(seq_splits[s], nsplit) : nsplit;
 #pragma unroll
-      for (int j = 0; j < kMergeChunk; ++j) v[u][j] = (ok && k0 + j < nsplit) ? __ldcg(o + size_t(k0 + j) * kstride) : 0.f;
+      for (int j = 0; j < kMergeChunk; ++j) v[u][j] = (ok && k0 + j < ns) ? __ldcg(o + size_t(k0 + j) * kstride) : 0.f;
     }
   };
   float v[2][kMergeChunk];
@@ -546,12 +646,13 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
   {
     const int sq = tid / 32, lane = tid % 32, s = s0 + sq;
     if (sq < SEQS) {
+      const int ns = (s < B && seq_splits != nullptr) ? min(seq_splits[s], nsplit) : nsplit;
       float lk[kMergeMaxSplits / 32];
       float m = -INFINITY;
 #pragma unroll
       for (int j = 0; j < kMergeMaxSplits / 32; ++j) {
         const int k = lane + 32 * j;
-        lk[j] = (s < B && k < nsplit) ? __ldcg(lse_part + (size_t(s) * nsplit * NB + b) * H + h + size_t(k) * NB * H)
+        lk[j] = (s < B && k < ns) ? __ldcg(lse_part + (size_t(s) * nsplit * NB + b) * H + h + size_t(k) * NB * H)
                                       : -INFINITY;
         m = fmaxf(m, lk[j]);
       }
@@ -580,9 +681,14 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
     }
   }
   __syncthreads();
+  int ns_cta = nsplit;
+  if (seq_splits != nullptr) {
+    ns_cta = 0;
+    for (int sq = 0; sq < SEQS && s0 + sq < B; ++sq) ns_cta = max(ns_cta, min(seq_splits[s0 + sq], nsplit));
+  }
   for (int i0 = tid; i0 < DLAT * SEQS; i0 += 2 * THREADS) {
     float z[2] = {0.f, 0.f};
-    for (int k0 = 0; k0 < nsplit; k0 += kMergeChunk) {
+    for (int k0 = 0; k0 < ns_cta; k0 += kMergeChunk) {
       if (i0 != tid || k0 != 0) load_pair(i0, k0, v);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -794,7 +900,8 @@ template <int KP>
 __global__ void __launch_bounds__(kSkThreads)
 combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part,
                       const __nv_bfloat16* __restrict__ w_uv, float* __restrict__ out, int B, int H, int NB, int DLAT,
-                      int DH, int nsplit, float alpha, int* __restrict__ status) {
+                      int DH, int nsplit, float alpha, int* __restrict__ status,
+                      const int32_t* __restrict__ seq_splits) {
   extern __shared__ __align__(128) uint8_t sk_smem[];
   const int rows = NB * DLAT, DSL = DH / KP;
   __nv_bfloat16* wsl = reinterpret_cast<__nv_bfloat16*>(sk_smem);  // [rows][DSL]
@@ -817,7 +924,7 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
   }
   griddep_wait();
   // ---- 2. local merge over this CTA's splits; item = (sequence q, row r = b*DLAT + c)
-  const int k0 = int((long long)kp * nsplit / KP), k1 = int((long long)(kp + 1) * nsplit / KP);
+  const int k0 = int((long long)kp * nsplit / KP), k1_all = int((long long)(kp + 1) * nsplit / KP);
   const size_t kstride = size_t(NB) * H * DLAT;  // split stride of o_part
   for (int it = tid; it < 4 * rows; it += kSkThreads) {
     const int q = it / rows, r = it % rows, b = r / DLAT, c = r % DLAT, s = s0 + q;
@@ -826,6 +933,7 @@ combine_splitk_kernel(const float* __restrict__ o_part, const float* __restrict_
     if (s < B) {
       const float* lp = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
       const float* op = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;
+      const int k1 = seq_splits != nullptr ? min(k1_all, min(seq_splits[s], nsplit)) : k1_all;
       for (int kb = k0; kb < k1; kb += kMergeChunk) {
         float lk[kMergeChunk], v[kMergeChunk];
 #pragma unroll

@@ -78,6 +78,11 @@ int get_pool_maps(const void* pool, cuuint64_t total_rows, int W, int T, int box
 
 // TMEM columns used: 2 S slots (+ 2 rope-logit slots when NB > 1) + NB*SUB O blocks, NPAD each (<= 512).
 int pick_npad(int H, int NB, int SUB) {
+  if (const char* e = getenv("MLRA_DEBUG_NPAD")) {  // dev: force the head-group width (16/32/64)
+    const int v = atoi(e);
+    const int slots = 2 + (NB > 1 ? 2 : 0) + NB * SUB;
+    if ((v == 16 || v == 32 || v == 64) && slots * v <= 512 && !(NB == 4 && v == 64)) return v;
+  }
   // registers: the softmax keeps NB x NPAD/2 sum partials per thread; cap NB = 4 at NPAD = 32
   if (NB == 4) return H <= 16 ? 16 : 32;
   // S slots (2) + shared rope-logit slots (2, NB > 1) + one O block per sub-block
@@ -200,8 +205,9 @@ int mlra_absorb_query(const void* q_nope, const void* q_rope, const void* w_uk, 
 // Workspace of mlra_decode_step: [status word | q~ | scaled q_rope | o_part | lse_part | merge /
 // per-chunk scratch | fused-step counters], each 256-byte aligned. The status word (int32, the
 // first 4 bytes of every workspace) collects the kernels' numeric flags (mlra_check_status).
+constexpr int kPlanMaxCtas = 1024;
 struct WsLayout {
-  size_t q_abs, q_rope, o_part, lse, zbuf, sync, total;
+  size_t q_abs, q_rope, o_part, lse, zbuf, sync, plan, total;
 };
 
 static WsLayout ws_layout(int B, int H, int NB, int DLAT, int DR, int nsplit) {
@@ -215,6 +221,7 @@ static WsLayout ws_layout(int B, int H, int NB, int DLAT, int DR, int nsplit) {
   w.zbuf = o; o += al(size_t(B) * NB * H * DLAT * 4);
   // fused-step counters: head groups <= ceil(H / 16) (the smallest head group is 16)
   w.sync = o; o += al(mlra::fuse_sync_words(B, H, (H + 15) / 16) * 4);
+  w.plan = o; o += al(size_t(kPlanMaxCtas) * 4 * 4 + size_t(B) * 4);  // ragged-batch work items + split counts
   w.total = o;
   return w;
 }
@@ -238,6 +245,11 @@ int mlra_check_status(int32_t* status, int reset, void* stream) {
   return MLRA_OK;
 }
 
+int mlra_default_splits_heads(int B, int max_seqlen, int NB, int SUB, int H) {
+  const int groups = H > 0 ? (H + pick_npad(H, NB, SUB) - 1) / pick_npad(H, NB, SUB) : 1;
+  return mlra_default_splits(B * groups, max_seqlen, NB, SUB);
+}
+
 int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
   int sms = mlra_num_sms();
   if (sms <= 0) sms = 148;
@@ -253,7 +265,8 @@ int mlra_default_splits(int B, int max_seqlen, int NB, int SUB) {
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       bool pdl = false, const mlra::FuseArgs* fz = nullptr, int fuse_mode = 1);
+                       bool pdl = false, const mlra::FuseArgs* fz = nullptr, int fuse_mode = 1,
+                       const int32_t* plan = nullptr, int plan_ctas = 0);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
@@ -265,7 +278,7 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       bool pdl, const mlra::FuseArgs* fz, int fuse_mode) {
+                       bool pdl, const mlra::FuseArgs* fz, int fuse_mode, const int32_t* plan, int plan_ctas) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -296,6 +309,8 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.B = B; p.H = H; p.SUB = SUB; p.DR = DR; p.W = W;
   p.page_size = page_size; p.max_pages = max_pages; p.nsplit = nsplit; p.box_rows = box_rows;
   p.pdl = pdl ? 1 : 0;
+  p.plan = plan;
+  p.plan_ctas = plan_ctas;
   if (fz != nullptr) {
     p.fused = fuse_mode;
     p.fz = *fz;
@@ -384,7 +399,7 @@ static int gqa_decode_impl(const void* q, const void* pool, const int32_t* block
 static int allreduce_launch(mlra::AllReduceParams& p, int nlocal, bool sim, cudaStream_t st);
 static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
                            int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                           bool pdl, const mlra::TpSum* tp, int32_t* status);
+                           bool pdl, const mlra::TpSum* tp, int32_t* status, const int32_t* seq_splits);
 
 // After a K3 variant without the fused TP sum: K5 on the output, in place, same region.
 static int tp_sum_after(const mlra::TpSum* tp, float* out, int n, cudaStream_t st) {
@@ -399,9 +414,10 @@ static int tp_sum_after(const mlra::TpSum* tp, float* out, int n, cudaStream_t s
 
 static int combine_impl(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf, int B,
                         int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                        bool pdl = false, const mlra::TpSum* tp = nullptr, int32_t* status = nullptr) {
+                        bool pdl = false, const mlra::TpSum* tp = nullptr, int32_t* status = nullptr,
+                        const int32_t* seq_splits = nullptr) {
   if (int rc = combine_variant(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, upproj, st, pdl, tp,
-                               status))
+                               status, seq_splits))
     return rc == 1 ? tp_sum_after(tp, out, B * H * DH, st) : rc;
   return MLRA_OK;
 }
@@ -410,10 +426,9 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
 // requested TP sum still has to run (the K3 variant has no fused sum), < 0 on error.
 static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
                            int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                           bool pdl, const mlra::TpSum* tp, int32_t* status) {
+                           bool pdl, const mlra::TpSum* tp, int32_t* status, const int32_t* seq_splits) {
   const int tp_pending = (tp != nullptr && tp->world > 1 && upproj == 1) ? 1 : 0;
   const int rows = B * NB * H;
-  const int warps_per_cta = 8;
   // summed output: split-K merge over a cluster of KP CTAs (KP = 8 once the splits are many)
   const int KP = nsplit > 24 ? 8 : 4;
   const size_t sksmem = KP == 8 ? mlra::combine_splitk_smem<8>(NB, DLAT, DH) : mlra::combine_splitk_smem<4>(NB, DLAT, DH);
@@ -423,7 +438,8 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
   // 1.5x fewer round trips (small batches: many splits per sequence).
   const int rt_c4 = 2 * ((nsplit + 11) / 12);
   const int rt_sk = 2 * NB * (((nsplit + KP - 1) / KP + 11) / 12);
-  if (upproj == 1 && 3 * rt_sk < 2 * rt_c4 && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
+  // (ragged plans: the per-sequence split counts vary, most sequences have few -- per-branch CTAs)
+  if (seq_splits == nullptr && upproj == 1 && 3 * rt_sk < 2 * rt_c4 && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
       sksmem <= size_t(kSmemBudget) && (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
     auto kern = KP == 8 ? mlra::combine_splitk_kernel<8> : mlra::combine_splitk_kernel<4>;
     static unsigned attr4 = 0, attr8 = 0;
@@ -443,7 +459,7 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha, status) != cudaSuccess)
+                           DH, nsplit, alpha, status, seq_splits) != cudaSuccess)
       return cuda_check("combine launch");
     if (int rc = cuda_check("combine launch")) return rc;
     return tp_pending;
@@ -499,18 +515,18 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
       }
     }
     if (cudaLaunchKernelEx(&cfg, kern, o_part, lse_part, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB, DLAT,
-                           DH, nsplit, alpha, per_branch, tps, status) != cudaSuccess)
+                           DH, nsplit, alpha, per_branch, tps, status, seq_splits) != cudaSuccess)
       return cuda_check("combine launch");
     if (int rc = cuda_check("combine launch")) return rc;
     return fused ? MLRA_OK : tp_pending;
   }
   if (upproj == 0) {
-    mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
-        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status);
+    mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128, 0, st>>>(
+        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status, seq_splits);
     return cuda_check("merge launch");
   }
-  mlra::merge_splits_kernel<<<(rows + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
-      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status);
+  mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128, 0, st>>>(
+      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status, seq_splits);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;
   const int kp = NB * DLAT / kparts;
@@ -1075,4 +1091,55 @@ extern "C" int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H
       y, ldy, nq, H, dr, drq, pos0, rope_base, q_scale, r_scale, static_cast<__nv_bfloat16*>(q_out),
       static_cast<__nv_bfloat16*>(r_out));
   return cuda_check("query_epilogue launch");
+}
+
+// ----------------------------------------------------------------------------- ragged batches
+extern "C" int mlra_decode_plan(const int32_t* seqlens, int B, int tile_tokens, int ctas, int nsplit_max,
+                                int32_t* plan, int32_t* seq_splits, float* lse_part, int NB, int H, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  if (tile_tokens <= 0 || ctas < B || ctas > kPlanMaxCtas || nsplit_max < 1 || NB < 1 || H < 1)
+    return fail(MLRA_ERR_CONFIG, "decode_plan: B=%d ctas=%d (>= B, <= %d) nsplit_max=%d", B, ctas, kPlanMaxCtas,
+                nsplit_max);
+  const size_t smem = size_t(2) * B * sizeof(int);
+  if (smem > 48 * 1024) return fail(MLRA_ERR_CONFIG, "decode_plan: batch %d too large", B);
+  mlra::decode_plan_kernel<<<1, mlra::kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      seqlens, B, tile_tokens, ctas, nsplit_max, plan, seq_splits, lse_part, NB, H);
+  return cuda_check("decode_plan launch");
+}
+
+extern "C" int mlra_decode_step_ragged(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,
+                                       const void* pool, const int32_t* block_table, const int32_t* seqlens,
+                                       float* out, void* workspace, int B, int H, int DH, int NB, int SUB, int DLS,
+                                       int DR, int page_size, int max_pages, int num_pages, int nsplit_max,
+                                       float score_scale, float alpha, void* stream) {
+  if (B <= 0) return MLRA_OK;
+  const int DLAT = SUB * DLS;
+  const WsLayout wl = ws_layout(B, H, NB, DLAT, DR, nsplit_max);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int32_t* status = reinterpret_cast<int32_t*>(ws);
+  void* q_abs = ws + wl.q_abs;
+  void* q_rope_s = ws + wl.q_rope;
+  float* o_part = reinterpret_cast<float*>(ws + wl.o_part);
+  float* lse_part = reinterpret_cast<float*>(ws + wl.lse);
+  float* zbuf = reinterpret_cast<float*>(ws + wl.zbuf);
+  int32_t* plan = reinterpret_cast<int32_t*>(ws + wl.plan);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int hgroups = (H + pick_npad(H, NB, SUB) - 1) / pick_npad(H, NB, SUB);
+  const int ctas = std::min(kPlanMaxCtas, std::max(B, num_sms() / hgroups));
+  const int T = (SUB == 1) ? 128 : 64;
+  int32_t* seq_splits = plan + kPlanMaxCtas * 4;
+  if (int rc = mlra_decode_plan(seqlens, B, T, ctas, nsplit_max, plan, seq_splits, lse_part, NB, H, stream)) return rc;
+  if (w_uk != nullptr) {
+    if (int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream))
+      return rc;
+  } else {
+    q_abs = const_cast<void*>(q_nope);
+    q_rope_s = const_cast<void*>(q_rope);
+  }
+  int rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
+                       page_size, max_pages, num_pages, nsplit_max, stream, w_uk != nullptr && getenv("MLRA_NO_PDL") == nullptr,
+                       nullptr, 1, plan, ctas);
+  if (rc) return rc;
+  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit_max, alpha, 1, st, false, nullptr,
+                      status, seq_splits);
 }

@@ -61,6 +61,8 @@ struct DecodeParams {
   int nb_total;
   float qk_scale;
   int pdl;                      // host side: launch with programmatic stream serialization
+  const int32_t* plan;          // ragged-batch work items [gridDim.x][4] (mlra_decode_plan), or null
+  int plan_ctas;                // host side: gridDim.x with a plan
   // ---- fused step (fused_step.cuh): K1 in the prologue, K3 (+ TP sum) in the epilogue -------
   int fused;                    // 0: partials only (K1 / K3 run as separate kernels)
   int hgroups;                  // head groups (gridDim.z) -- completion-counter stride
@@ -133,7 +135,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const int SUB = GQA ? 1 : p.SUB;
   const int DLAT = SUB * DLS;
-  const int seq = blockIdx.y, split = blockIdx.x;
+  // Work item: uniform grid (split, sequence) -- or, with a ragged-batch plan (mlra_decode_plan),
+  // item blockIdx.x of the plan: {sequence, split slot, first tile, tile count}; surplus CTAs
+  // (sequence < 0) leave at once.
+  int4 item = make_int4(int(blockIdx.y), int(blockIdx.x), 0, -1);
+  if (p.plan != nullptr) {
+    item = __ldg(reinterpret_cast<const int4*>(p.plan) + blockIdx.x);
+    if (item.x < 0) return;
+  }
+  const int seq = item.x, split = item.y;
   // MLRA/MLA: blockIdx.z = head group; GQA: blockIdx.z = group of NB KV heads (all its heads)
   const int hg = GQA ? 0 : blockIdx.z;
   const int branch0 = GQA ? blockIdx.z * NB : 0;  // first branch of this CTA in the q/partials layout
@@ -141,8 +151,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int len = p.seqlens[seq];
   const int ntiles_total = (len + T - 1) / T;
   const int per = (ntiles_total + p.nsplit - 1) / p.nsplit;
-  const int t0 = min(split * per, ntiles_total);
-  const int ntiles = min(per, ntiles_total - t0);
+  const int t0 = p.plan != nullptr ? min(item.z, ntiles_total) : min(split * per, ntiles_total);
+  const int ntiles = p.plan != nullptr ? max(0, min(item.w, ntiles_total - t0)) : min(per, ntiles_total - t0);
   const int R = ntiles * NB;  // rounds: (tile, branch)
   const int n_valid_pages = (len + p.page_size - 1) / p.page_size;
   const int HV = min(NPAD, p.H - hg * NPAD);  // real heads in this head group

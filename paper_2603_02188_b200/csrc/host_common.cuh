@@ -197,7 +197,7 @@ int launch_decode(const CUtensorMap& lat_map, const CUtensorMap& rope_map, mlra:
     p.fz.hgroups = head_groups;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.nsplit, p.B, head_groups);
+  cfg.gridDim = p.plan != nullptr ? dim3(p.plan_ctas, 1, head_groups) : dim3(p.nsplit, p.B, head_groups);
   cfg.blockDim = dim3(mlra::kNumThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;

@@ -72,7 +72,7 @@ struct PrefillLayout {
   static constexpr int kWBytes = kDhChunks * DLAT * 128;  // [DLAT rows][64 cols] per dh chunk
   static_assert(kWBytes <= kLatChunks * kPfChunk, "W^UV must fit the Q latent region");
   static constexpr int kBar = kP + 2 * kPBytes;
-  static constexpr int kSmem = kBar + 192 + 2 * kPfT * 4;  // barriers, TMEM base, row-max exchange
+  static constexpr int kSmem = kBar + 192 + 6 * kPfT * 4;  // barriers, TMEM base, pair exchange slots
   static_assert(kLatChunks * kPfChunk <= kPBytes, "Z_hi must fit the P buffer");
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t S_COL = 0, O_COL = 2 * kPfT, OUT_COL = 2 * kPfT + DLAT;
@@ -268,7 +268,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const int q = qt * kPfT + r;           // query token index
     const uint32_t trow = pf_tmem_lane(tbase, warp);
     uint8_t* prow = smem + L::kP + hf * kPfChunk + r * 128;  // + (g & 1) * kPBytes
-    float* xmax = reinterpret_cast<float*>(smem + L::kBar + 192);  // [2][128] (+ l exchange)
+    // pair exchange slots [3][2][128]: the tile max of global tile g in slot g & 1 (a thread is at
+    // most one tile ahead of its partner: one pair barrier per tile), the row sums in slot 2
+    float* xmax = reinterpret_cast<float*>(smem + L::kBar + 192);
     const int pair_bar = 1 + (warp & 3);                           // named barrier of the warp pair
     int g = 0;
     for (int b = 0; b < NB; ++b) {
@@ -301,9 +303,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             tmax = fmaxf(tmax, x);
           }
         }
-        xmax[hf * kPfT + r] = tmax;
+        float* xs = xmax + (g & 1) * 2 * kPfT;
+        xs[hf * kPfT + r] = tmax;
         named_bar_sync(pair_bar, 64);
-        tmax = fmaxf(tmax, xmax[(hf ^ 1) * kPfT + r]);
+        tmax = fmaxf(tmax, xs[(hf ^ 1) * kPfT + r]);
         // Lazy rescale: a row moves its running max only when its tile max exceeds it by 2^8
         // (or on its first visible tile). tcgen05.ld / st are warp-collective, so the warp
         // rescales its half of O in TMEM if ANY of its rows moved (factor 1 for the others),
@@ -352,10 +355,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       }
       // Z_b = O / l -> bf16 hi (P region) + lo (Q latent region: the branch's QKs are done);
       // the row's sum is the pair's two halves
-      xmax[hf * kPfT + r] = l;
+      xmax[4 * kPfT + hf * kPfT + r] = l;
       named_bar_sync(pair_bar, 64);
-      const float lt = l + xmax[(hf ^ 1) * kPfT + r];
-      named_bar_sync(pair_bar, 64);  // both read before the next tile's max exchange
+      const float lt = l + xmax[4 * kPfT + (hf ^ 1) * kPfT + r];
       pf_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1, 11);  // the branch's last PV (and all before)
       tc_fence_after();
       const float inv = lt > 0.f ? 1.f / lt : 0.f;

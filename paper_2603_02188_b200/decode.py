@@ -246,7 +246,7 @@ def _run_units(cfg: AttnConfig, cache: PagedLatentCache, lw: LocalWeights, own: 
     nb, dlat = kernel_geometry(layout, own)
     sub, dls = ops.latent_geometry(dlat)
     pc = cache.paged
-    nsplit = ops.default_splits(1, max(cache.n, 1), nb, sub)
+    nsplit = ops.default_splits(1, max(cache.n, 1), nb, sub, heads=len(own.heads))
     q_abs, q_rs = ops.absorb_query(qn, qr, w_uk, nb, dlat, ops.score_scale(cfg.tau))
     o_part, lse = ops.decode_partials(q_abs, q_rs, pc.pool, pc.block_table, pc.seqlens, pc.page_size, nb, sub, dls,
                                       nsplit)
@@ -544,7 +544,7 @@ class DecodeEngine:
 
     def __init__(self, cfg: AttnConfig, w, own: Ownership | None = None, *, batch: int, max_tokens: int,
                  page_size: int = 128, device=None, nsplit: int | None = None, page_order=None,
-                 alpha: float | None = None):
+                 alpha: float | None = None, ragged: bool = False):
         _check_served(cfg)
         if cfg.variant == "gqa":
             raise RoutingError("DecodeEngine serves the latent family; use gqa.GqaDecodeEngine for gqa")
@@ -562,7 +562,12 @@ class DecodeEngine:
         if alpha is None:
             alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
         self.alpha = float(alpha)
-        self.nsplit = nsplit or ops.default_splits(batch, max_tokens, self.nb, self.sub)
+        # ragged=True: K2's work comes from the device-side plan (mlra_decode_plan) that balances the
+        # sequences' tiles over one wave of CTAs; nsplit is then the most splits one sequence may get
+        self.ragged = bool(ragged)
+        if ragged and nsplit is None:
+            nsplit = min(64, max(1, ops.num_sms() // max(1, -(-len(self.heads) // 64))))
+        self.nsplit = nsplit or ops.default_splits(batch, max_tokens, self.nb, self.sub, heads=len(self.heads))
         hl = len(self.heads)
         self.workspace = ops.DecodeWorkspace(batch, hl, self.nb, self.dlat, self.layout.drp, self.nsplit, self.device)
         self.out = torch.empty((batch, hl, cfg.d_h), dtype=torch.float32, device=self.device)
@@ -601,9 +606,10 @@ class DecodeEngine:
         q, qr = kp.query(B, c.seqlens, pos_delta=-1 if advance else 0)
         if advance and getattr(c, "_host_lens", None) is not None:  # host mirror (eager calls)
             c._host_lens = [n + 1 for n in c._host_lens]
-        return ops.decode_step(q, qr, None if kp.absorbed else self.w_uk, self.w_uv, c.pool, c.block_table,
-                               c.seqlens, c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale,
-                               self.alpha, self.workspace, out=self.out if out is None else out)
+        step = ops.decode_step_ragged if self.ragged else ops.decode_step
+        return step(q, qr, None if kp.absorbed else self.w_uk, self.w_uv, c.pool, c.block_table,
+                    c.seqlens, c.page_size, self.nb, self.sub, self.dls, self.nsplit, self.scale,
+                    self.alpha, self.workspace, out=self.out if out is None else out)
 
     @property
     def batch(self) -> int:
@@ -639,6 +645,7 @@ class DecodeEngine:
         """One decode-attention step over the cache: bf16 [B, h_local, d_h] / [B, h_local, drp]
         queries on this device -> fp32 [B, h_local, d_h] (alpha-scaled, branch-summed)."""
         c = self.cache
-        return ops.decode_step(q_nope, q_rope, self.w_uk, self.w_uv, c.pool, c.block_table, c.seqlens, c.page_size,
-                               self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
-                               self.workspace, out=self.out if out is None else out)
+        step = ops.decode_step_ragged if self.ragged else ops.decode_step
+        return step(q_nope, q_rope, self.w_uk, self.w_uv, c.pool, c.block_table, c.seqlens, c.page_size,
+                    self.nb, self.sub, self.dls, self.nsplit, self.scale, self.alpha,
+                    self.workspace, out=self.out if out is None else out)

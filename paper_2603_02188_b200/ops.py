@@ -36,7 +36,10 @@ def num_sms() -> int:
     return _lib.load().mlra_num_sms()
 
 
-def default_splits(batch: int, max_seqlen: int, nb: int, sub: int) -> int:
+def default_splits(batch: int, max_seqlen: int, nb: int, sub: int, heads: int | None = None) -> int:
+    """K2's split count: one wave of CTAs over the SMs (with ``heads``: counting K2's head groups)."""
+    if heads is not None:
+        return _lib.load().mlra_default_splits_heads(batch, max_seqlen, nb, sub, heads)
     return _lib.load().mlra_default_splits(batch, max_seqlen, nb, sub)
 
 
@@ -223,6 +226,33 @@ def decode_step(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seq
                                       sub, dls, DR, page_size, block_table.shape[1], pool.shape[0] // page_size,
                                       nsplit, float(score_scale), float(alpha), _stream())
     _lib.check(rc, "mlra_decode_step")
+    return out
+
+
+def decode_step_ragged(q_nope, q_rope, w_uk_packed, w_uv_packed, pool, block_table, seqlens, page_size: int, nb: int,
+                       sub: int, dls: int, nsplit_max: int, score_scale: float, alpha: float,
+                       workspace: DecodeWorkspace, out: torch.Tensor | None = None) -> torch.Tensor:
+    """decode_step for ragged batches (mlra_decode_step_ragged): the device-side plan balances the
+    sequences' token tiles over one wave of K2 CTAs (up to nsplit_max splits per sequence)."""
+    if w_uk_packed is None:
+        B, _, H, _ = q_nope.shape
+        DH = w_uv_packed.shape[2]
+    else:
+        B, H, DH = q_nope.shape
+    DR = q_rope.shape[2]
+    dlat = sub * dls
+    if workspace.key != (B, H, nb, dlat, DR, nsplit_max):
+        raise ConfigError(f"workspace sized for {workspace.key}, call needs {(B, H, nb, dlat, DR, nsplit_max)}")
+    if out is None:
+        out = torch.empty((B, H, DH), dtype=torch.float32, device=q_nope.device)
+    rc = _lib.load().mlra_decode_step_ragged(q_nope.data_ptr(), q_rope.data_ptr(),
+                                             None if w_uk_packed is None else w_uk_packed.data_ptr(),
+                                             w_uv_packed.data_ptr(), pool.data_ptr(), block_table.data_ptr(),
+                                             seqlens.data_ptr(), out.data_ptr(), workspace.buf.data_ptr(), B, H, DH,
+                                             nb, sub, dls, DR, page_size, block_table.shape[1],
+                                             pool.shape[0] // page_size, nsplit_max, float(score_scale),
+                                             float(alpha), _stream())
+    _lib.check(rc, "mlra_decode_step_ragged")
     return out
 
 
