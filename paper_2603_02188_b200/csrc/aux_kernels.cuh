@@ -224,91 +224,75 @@ inline size_t head_gemm_smem(int kp) {
 // sequence s gets ns_s consecutive splits of ceil(tiles_s / ns_s) tiles (items in ascending
 // (sequence, split) order: the merge adds the splits in that order). seq_splits[s] = ns_s: the
 // merge reads only those slots. One CTA.
-constexpr int kPlanThreads = 256;
+constexpr int kPlanThreads = 32;  // one warp: warp reductions only (the plan sits on the step's critical path)
 __global__ void __launch_bounds__(kPlanThreads)
 decode_plan_kernel(const int32_t* __restrict__ seqlens, int B, int T, int ctas, int nsplit_max,
-                   int32_t* __restrict__ plan, int32_t* __restrict__ seq_splits, float* __restrict__ lse_part,
-                   int NB, int H) {
+                   int32_t* __restrict__ plan, int32_t* __restrict__ seq_splits) {
   extern __shared__ int pl_smem[];
-  int* tiles = pl_smem;           // [B]
-  int* ns = pl_smem + B;          // [B]
-  __shared__ int red_i[kPlanThreads / 32];
-  __shared__ int s_total, s_max, s_c;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto block_sum = [&](int v) {
+  int* tiles = pl_smem;  // [B]
+  int* offs = pl_smem + B;  // [B]
+  const int lane = threadIdx.x;
+  auto wsum = [](int v) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red_i[warp] = v;
-    __syncthreads();
-    int t = 0;
-    for (int w = 0; w < kPlanThreads / 32; ++w) t += red_i[w];
-    __syncthreads();
-    return t;
+    return v;
+  };
+  auto wmax = [](int v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
   };
   int loc = 0, mx = 0;
-  for (int s = tid; s < B; s += kPlanThreads) {
+  for (int s = lane; s < B; s += 32) {
     const int t = (max(seqlens[s], 0) + T - 1) / T;
     tiles[s] = t;
     loc += t;
     mx = max(mx, t);
   }
-  const int total = block_sum(loc);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) red_i[warp] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    int m = 0;
-    for (int w = 0; w < kPlanThreads / 32; ++w) m = max(m, red_i[w]);
-    s_total = total;
-    s_max = m;
-  }
-  __syncthreads();
+  const int total = wsum(loc);
+  mx = wmax(mx);
+  __syncwarp();
   // binary search of the tile budget c: feasible(c) <=> sum_s max(1, ceil(tiles_s / c)) <= ctas and
   // every ceil(tiles_s / c) <= nsplit_max (monotone in c)
-  int lo = max(1, (s_total + ctas - 1) / ctas), hi = max(lo, s_max);
+  int lo = max(1, (total + ctas - 1) / ctas), hi = max(lo, mx);
   while (lo < hi) {
     const int c = (lo + hi) / 2;
     int cnt = 0, bad = 0;
-    for (int s = tid; s < B; s += kPlanThreads) {
+    for (int s = lane; s < B; s += 32) {
       const int k = max(1, (tiles[s] + c - 1) / c);
       cnt += k;
-      bad += k > nsplit_max;
+      bad |= k > nsplit_max;
     }
-    cnt = block_sum(cnt);
-    bad = block_sum(bad);
+    cnt = wsum(cnt);
+    bad = wsum(bad);
     if (cnt <= ctas && bad == 0) hi = c; else lo = c + 1;
   }
-  if (tid == 0) s_c = lo;
-  __syncthreads();
-  const int c = s_c;
-  for (int s = tid; s < B; s += kPlanThreads) ns[s] = min(nsplit_max, max(1, (tiles[s] + c - 1) / c));
-  __syncthreads();
-  // item offsets: exclusive prefix sum of ns over the sequences (serial: B is small)
-  if (tid == 0) {
-    int acc = 0;
-    for (int s = 0; s < B; ++s) {
-      const int k = ns[s];
-      ns[s] = acc;  // offset
-      tiles[s] |= k << 20;  // (keep the count next to the tiles: tiles < 2^20)
-      acc += k;
+  const int c = lo;
+  // item offsets: exclusive prefix sum of the split counts (lane-chunked scan)
+  int run = 0;
+  for (int s0 = 0; s0 < B; s0 += 32) {
+    const int s = s0 + lane;
+    const int k = s < B ? min(nsplit_max, max(1, (tiles[s] + c - 1) / c)) : 0;
+    int incl = k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    s_total = acc;
+    if (s < B) {
+      offs[s] = run + incl - k;
+      seq_splits[s] = k;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
   }
-  __syncthreads();
-  for (int s = tid; s < B; s += kPlanThreads) {
-    const int t = tiles[s] & ((1 << 20) - 1), k = tiles[s] >> 20, off = ns[s];
+  __syncwarp();
+  for (int s = lane; s < B; s += 32) {
+    const int t = tiles[s], k = seq_splits[s], off = offs[s];
     const int per = (t + k - 1) / max(k, 1);
-    seq_splits[s] = k;
-    for (int j = 0; j < k; ++j) {
-      int32_t* it = plan + size_t(off + j) * 4;
-      it[0] = s;
-      it[1] = j;
-      it[2] = j * per;
-      it[3] = max(0, min(per, t - j * per));
-    }
+    for (int j = 0; j < k; ++j)
+      reinterpret_cast<int4*>(plan)[off + j] = make_int4(s, j, j * per, max(0, min(per, t - j * per)));
   }
-  for (int i = s_total + tid; i < ctas; i += kPlanThreads) plan[size_t(i) * 4] = -1;
+  for (int i = run + lane; i < ctas; i += 32) reinterpret_cast<int4*>(plan)[i] = make_int4(-1, 0, 0, 0);
 }
 
 // ----------------------------------------------------------------------------- K3a

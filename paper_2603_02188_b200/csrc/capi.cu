@@ -1102,8 +1102,9 @@ extern "C" int mlra_decode_plan(const int32_t* seqlens, int B, int tile_tokens, 
                 nsplit_max);
   const size_t smem = size_t(2) * B * sizeof(int);
   if (smem > 48 * 1024) return fail(MLRA_ERR_CONFIG, "decode_plan: batch %d too large", B);
+  (void)lse_part, (void)NB, (void)H;  // (kept in the signature: the K2 partial layout the plan serves)
   mlra::decode_plan_kernel<<<1, mlra::kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      seqlens, B, tile_tokens, ctas, nsplit_max, plan, seq_splits, lse_part, NB, H);
+      seqlens, B, tile_tokens, ctas, nsplit_max, plan, seq_splits);
   return cuda_check("decode_plan launch");
 }
 
