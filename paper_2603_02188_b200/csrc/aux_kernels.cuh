@@ -298,17 +298,22 @@ decode_plan_kernel(const int32_t* __restrict__ seqlens, int B, int T, int ctas, 
 // ----------------------------------------------------------------------------- K3a
 // Flash-decoding merge of the K2 split partials: for every (sequence, branch, head) row,
 //   Z = sum_k w_k O_k with w_k = 2^(lse_k - max) / sum_j 2^(lse_j - max).
-// CTA = (row, 128 latent columns), 128 threads: warp 0 forms the split weights once (lane k <
-// nsplit, shuffled max / sum) into smem, then every thread merges one column over the splits
-// with 8 loads in flight at a time. Output [B, H, NB*DLAT] (the K3b input) or, with zout_bnh,
-// [B, NB, H, DLAT] * alpha (the latent mixture itself: the paper's decode scope).
+// CTA = (row, 128 latent columns), 512 threads = 128 columns x 4 split quarters: warp 0 forms
+// the split weights once (lane k < nsplit, shuffled max / sum) into smem; thread (q, c) merges
+// column c over the splits k = q, q+4, ... (8 loads in flight at a time) and the 4 quarter sums
+// are added in ascending order through smem (deterministic). Many splits (batch-1 decode runs
+// up to 148) cost ceil(nsplit / 32) round trips instead of ceil(nsplit / 8). Output
+// [B, H, NB*DLAT] (the K3b input) or, with zout_bnh, [B, NB, H, DLAT] * alpha (the latent mixture
+// itself: the paper's decode scope).
 constexpr int kMergeMaxSplits = 160;  // 5 per lane
-__global__ void __launch_bounds__(128)
+constexpr int kMergeQ = 4;
+__global__ void __launch_bounds__(128 * kMergeQ)
 merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, float* __restrict__ z, int B,
                     int NB, int H, int DLAT, int nsplit, float alpha, int zout_bnh, int* __restrict__ status,
                     const int32_t* __restrict__ seq_splits) {
   __shared__ float wsh[kMergeMaxSplits];
-  const int row = blockIdx.x, c = blockIdx.y * 128 + threadIdx.x;
+  __shared__ float part[kMergeQ][128];
+  const int row = blockIdx.x, cl = threadIdx.x % 128, qk = threadIdx.x / 128, c = blockIdx.y * 128 + cl;
   const int lane = threadIdx.x % 32;
   const int h = row % H, b = (row / H) % NB, s = row / (H * NB);
   const int ns = seq_splits != nullptr ? min(seq_splits[s], nsplit) : nsplit;  // splits of this sequence
@@ -347,20 +352,32 @@ merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ 
       if (lane + 32 * j < ns) wsh[lane + 32 * j] = lk[j] * inv;
   }
   __syncthreads();
-  if (c >= DLAT) return;
-  const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
-  const size_t sstride = size_t(NB) * H * DLAT;
   float acc = 0.f;
-  for (int k0 = 0; k0 < ns; k0 += 8) {
-    float v[8];
+  if (c < DLAT) {
+    const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
+    const size_t sstride = size_t(NB) * H * DLAT;
+    for (int k0 = qk; k0 < ns; k0 += 8 * kMergeQ) {
+      float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = k0 + j < ns ? __ldcg(o + size_t(k0 + j) * sstride) : 0.f;
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j * kMergeQ;
+        v[j] = k < ns ? __ldcg(o + size_t(k) * sstride) : 0.f;
+      }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (k0 + j < ns) acc = fmaf(wsh[k0 + j], v[j], acc);
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j * kMergeQ;
+        if (k < ns) acc = fmaf(wsh[k], v[j], acc);
+      }
+    }
   }
+  part[qk][cl] = acc;
+  __syncthreads();
+  if (qk != 0 || c >= DLAT) return;
+  float t = part[0][cl];
+#pragma unroll
+  for (int q = 1; q < kMergeQ; ++q) t += part[q][cl];
   float* dst = zout_bnh ? z + ((size_t(s) * NB + b) * H + h) * DLAT : z + (size_t(s) * H + h) * (NB * DLAT) + b * DLAT;
-  dst[c] = acc * (zout_bnh ? alpha : 1.f);
+  dst[c] = t * (zout_bnh ? alpha : 1.f);
 }
 
 

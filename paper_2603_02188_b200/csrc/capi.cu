@@ -521,11 +521,11 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     return fused ? MLRA_OK : tp_pending;
   }
   if (upproj == 0) {
-    mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128, 0, st>>>(
+    mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128 * mlra::kMergeQ, 0, st>>>(
         o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status, seq_splits);
     return cuda_check("merge launch");
   }
-  mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128, 0, st>>>(
+  mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128 * mlra::kMergeQ, 0, st>>>(
       o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status, seq_splits);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;

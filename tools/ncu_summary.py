@@ -17,11 +17,16 @@ def to_bytes(val, unit):
     f = float(val.replace(",", ""))
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
 
-summary = {}
+summary = json.load(open("profiles/ncu_summary.json")) if os.path.exists("profiles/ncu_summary.json") else {}
 for name, rep, algo, kname in [
         ("mlra4_tp1_b16_n32768", "gpurun_out/k2_tp1.ncu-rep", 603979776, "mlra_decode_kernel (K2)"),
         ("mlra4_tp4_b16_n32768", "gpurun_out/k2_tp4.ncu-rep", 201326592, "mlra_decode_kernel (K2)"),
-        ("outproj_b16_k3072_d3072", "gpurun_out/k4.ncu-rep", 3072 * 3072 * 2, "outproj_allreduce_kernel (K4, world 1)")]:
+        ("outproj_b16_k3072_d3072", "gpurun_out/k4.ncu-rep", 3072 * 3072 * 2, "outproj_allreduce_kernel (K4, world 1)"),
+        # K-1: the weight-streaming projection GEMMs (algorithmic bytes = the down weight of one launch)
+        ("proj_down_b16_k3072_n1600", "gpurun_out/proj.ncu-rep", 3072 * 1600 * 2, "proj_gemm_kernel (K-1 down)"),
+        # K6: causal prefill, n = 4096 (bytes are not its bound: the tensor pipe is; traffic recorded)
+        ("prefill_mlra4_tp1_n4096", "gpurun_out/k6.ncu-rep", 4096 * (1152 + 24 * 512 * 2 + 24 * 64 * 2 + 24 * 128 * 4),
+         "prefill_attention_kernel (K6; tensor-bound: bytes = cache + q~ + q_rope + out)")]:
     if not os.path.exists(rep):
         continue
     r = raw(rep)

@@ -1,6 +1,6 @@
 """Context x batch sweep (BASELINE configs[2] and configs[4]): MLRA-4 TP4 rank and TP1 on one
 B200, n in {4K..128K}, B in {1, 4, 16, 64}. Per point: full step (K1+K2+K3, CUDA graph of 10
-steps alternating two caches) and K2 alone, algorithmic GB/s and fraction of the measured HBM
+steps alternating two caches), K2 alone, and the paper's decode scope (K2 + split merge), algorithmic GB/s and fraction of the measured HBM
 peak. Writes JSON lines to stdout and a markdown table to gpurun_out/sweep.md."""
 import json, os, sys, torch
 sys.path.insert(0, ".")
@@ -35,12 +35,15 @@ for name in names:
             runner = bench.StepRunner(c, own, B, n, dev)
             step_ms = bench.time_graph_steps(runner, 20, 10, torch.cuda.synchronize)
             k2_ms = bench.time_k2_alone(runner.engines, 20)
+            ps_ms = bench.time_paper_scope(runner.engines, 20)
             nbytes = algorithmic_bytes(c, phi, [n] * B)
             r = {"layout": name, "ctx": n, "batch": B, "nsplit": runner.engines[0][0].nsplit,
                  "step_us": round(step_ms * 1e3, 2), "step_gbs": round(nbytes / (step_ms * 1e-3) / 1e9, 1),
                  "k2_us": round(k2_ms * 1e3, 2), "k2_gbs": round(nbytes / (k2_ms * 1e-3) / 1e9, 1),
                  "k2_frac": round(nbytes / (k2_ms * 1e-3) / 1e9 / peak, 3),
-                 "step_frac": round(nbytes / (step_ms * 1e-3) / 1e9 / peak, 3), "bytes": nbytes}
+                 "step_frac": round(nbytes / (step_ms * 1e-3) / 1e9 / peak, 3), "bytes": nbytes,
+                 "paper_scope_us": round(ps_ms * 1e3, 2),
+                 "paper_scope_frac": round(nbytes / (ps_ms * 1e-3) / 1e9 / peak, 3)}
             print(json.dumps(r), flush=True)
             rows.append(r)
             del runner
@@ -48,8 +51,9 @@ for name in names:
 os.makedirs("gpurun_out", exist_ok=True)
 with open(out_md, "w") as f:
     f.write(f"peak (MEASURED_PEAKS hbm_gbs) = {peak} GB/s\n\n")
-    f.write("| layout | ctx | B | nsplit | step µs | step GB/s | step frac | K2 µs | K2 GB/s | K2 frac |\n")
-    f.write("|---|---|---|---|---|---|---|---|---|---|\n")
+    f.write("| layout | ctx | B | nsplit | step µs | step GB/s | step frac | K2 µs | K2 GB/s | K2 frac | K2+merge µs | K2+merge frac |\n")
+    f.write("|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
         f.write(f"| {r['layout']} | {r['ctx']} | {r['batch']} | {r['nsplit']} | {r['step_us']} | {r['step_gbs']} | "
-                f"{r['step_frac']} | {r['k2_us']} | {r['k2_gbs']} | {r['k2_frac']} |\n")
+                f"{r['step_frac']} | {r['k2_us']} | {r['k2_gbs']} | {r['k2_frac']} | {r['paper_scope_us']} | "
+                f"{r['paper_scope_frac']} |\n")
