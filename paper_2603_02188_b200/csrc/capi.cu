@@ -311,6 +311,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.pdl = pdl ? 1 : 0;
   p.plan = plan;
   p.plan_ctas = plan_ctas;
+  p.late_trigger = getenv("MLRA_K3_PDL") != nullptr;
   if (fz != nullptr) {
     p.fused = fuse_mode;
     p.fz = *fz;
@@ -714,7 +715,8 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
   rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
                    max_pages, num_pages, nsplit, stream, pdl);
   if (rc) return rc;
-  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, false, tp, status);
+  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st,
+                      getenv("MLRA_K3_PDL") != nullptr, tp, status);
 }
 
 int mlra_gqa_default_splits(int B, int G, int max_seqlen) {

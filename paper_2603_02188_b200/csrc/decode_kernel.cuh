@@ -63,6 +63,7 @@ struct DecodeParams {
   int pdl;                      // host side: launch with programmatic stream serialization
   const int32_t* plan;          // ragged-batch work items [gridDim.x][4] (mlra_decode_plan), or null
   int plan_ctas;                // host side: gridDim.x with a plan
+  int late_trigger;             // release the dependent launch (K3) at the epilogue, not at the start
   // ---- fused step (fused_step.cuh): K1 in the prologue, K3 (+ TP sum) in the epilogue -------
   int fused;                    // 0: partials only (K1 / K3 run as separate kernels)
   int hgroups;                  // head groups (gridDim.z) -- completion-counter stride
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  griddep_launch_dependents();  // a dependent launch may start its prologue
+  if (!p.late_trigger) griddep_launch_dependents();  // a dependent launch may start its prologue
   if (p.fused == 2) cluster_arrive_relaxed();  // cluster step, phase 0: this CTA has started
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
@@ -674,6 +675,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
 
     // ============================================================ epilogue: partials
+    // (late trigger: the merge kernel may launch once every CTA has reached this point -- its
+    // launch and W^UV staging overlap the epilogues)
+    if (p.late_trigger) griddep_launch_dependents();
     // softmax sums: reduce this warp's 32 token lanes for all NB*kHG (branch, head) values at
     // once by recursive halving (a lane keeps one half and receives the partner's other half:
     // V/2 + V/4 + ... shuffles instead of 5*V), then the 4 quarters in smem.
@@ -842,6 +846,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     cluster_arrive_release();               // phase C
     cluster_wait_acquire();
   }
+  if (p.late_trigger && !(warp >= 2 && warp < 2 + kSoftThreads / 32)) griddep_launch_dependents();
   tc_fence_before();
   if (p.trace != nullptr && warp >= 2) atomicAdd(&tmem_base_sh[1], 1u);
   __syncthreads();
