@@ -1078,8 +1078,9 @@ extern "C" int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, 
                                void* lo, void* stream) {
   if (n <= 0) return MLRA_OK;
   if (K <= 0 || ldx < K) return fail(MLRA_ERR_SHAPE, "rows_split: K=%d ldx=%d", K, ldx);
-  mlra::rows_split_kernel<<<n, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      x, K, ldx, norm, alpha, eps, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo));
+  if (launch_ex(mlra::rows_split_kernel, dim3(n), dim3(256), 0, static_cast<cudaStream_t>(stream), false, x, K, ldx,
+                norm, alpha, eps, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo)) != cudaSuccess)
+    return cuda_check("rows_split launch");
   return cuda_check("rows_split launch");
 }
 
@@ -1089,9 +1090,10 @@ extern "C" int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H
   if (n <= 0) return MLRA_OK;
   if (nq < 0 || H <= 0 || dr < 0 || dr % 2 != 0 || drq < dr || drq % 2 != 0 || ldy < nq + H * dr)
     return fail(MLRA_ERR_SHAPE, "query_epilogue: bad dims nq=%d H=%d dr=%d drq=%d ldy=%d", nq, H, dr, drq, ldy);
-  mlra::query_epilogue_kernel<<<n, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      y, ldy, nq, H, dr, drq, pos0, rope_base, q_scale, r_scale, static_cast<__nv_bfloat16*>(q_out),
-      static_cast<__nv_bfloat16*>(r_out));
+  if (launch_ex(mlra::query_epilogue_kernel, dim3(n), dim3(256), 0, static_cast<cudaStream_t>(stream), false, y, ldy,
+                nq, H, dr, drq, pos0, rope_base, q_scale, r_scale, static_cast<__nv_bfloat16*>(q_out),
+                static_cast<__nv_bfloat16*>(r_out)) != cudaSuccess)
+    return cuda_check("query_epilogue launch");
   return cuda_check("query_epilogue launch");
 }
 

@@ -20,6 +20,7 @@ CPU fallback.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -329,16 +330,22 @@ class _StepState:
         return self._kproj
 
 
-_STATE: dict = {}
+_STATE: "OrderedDict[tuple, _StepState]" = OrderedDict()
+_STATE_MAX = 4  # device weight packs of the most recently used weight sets (LRU)
 
 
 def _state(cfg: AttnConfig, w, device) -> _StepState:
+    """Device state (packed weights, projector) of one weight set, kept for the last _STATE_MAX
+    weight sets used: a long-lived process that steps many models does not pin every one."""
     key = (cfg, id(w), str(device))
     st = _STATE.get(key)
     if st is None or st.__dict__.get("_w") is not w:
         st = _StepState(cfg, w, device)
         st._w = w
         _STATE[key] = st
+    _STATE.move_to_end(key)
+    while len(_STATE) > _STATE_MAX:
+        _STATE.popitem(last=False)
     return st
 
 

@@ -222,3 +222,31 @@ def test_decode_routing_errors():
         decode_step(trained_config("mlra4"), None, None, None, mode="turbo")
     with pytest.raises(RoutingError):  # naive covers the latent family only (decode.py:313-316)
         decode_step(trained_config("gqa"), None, None, None, mode="naive")
+
+
+def test_step_state_cache_is_bounded():
+    """The per-weight-set device state is an LRU (decode._STATE_MAX entries), not a leak."""
+    from paper_2603_02188_b200 import decode as dec
+
+    cfg = dec.AttnConfig("mlra", branches=4, h=4, d=32, d_h=8, d_h_rope=4, d_c=32, d_cq=16)
+    saved = dict(dec._STATE)
+    dec._STATE.clear()
+    try:
+        weights = [{"w_uk": np.zeros((32, 32)), "w_uv": np.zeros((32, 32))} for _ in range(dec._STATE_MAX + 3)]
+        orig = dec._StepState
+
+        class Dummy:
+            def __init__(self, cfg, w, device):
+                pass
+
+        dec._StepState = Dummy
+        try:
+            for w in weights:
+                dec._state(cfg, w, "cpu")
+        finally:
+            dec._StepState = orig
+        assert len(dec._STATE) == dec._STATE_MAX
+        assert [k[1] for k in dec._STATE] == [id(w) for w in weights[-dec._STATE_MAX:]]
+    finally:
+        dec._STATE.clear()
+        dec._STATE.update(saved)

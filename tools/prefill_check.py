@@ -3,7 +3,7 @@ import faulthandler, sys, time
 import numpy as np
 import torch
 sys.path.insert(0, ".")
-faulthandler.dump_traceback_later(90, exit=True)
+faulthandler.dump_traceback_later(900, exit=True)
 import paper_2603_02188_b200 as mlra
 from paper_2603_02188_b200 import decode as dec
 from paper_2603_02188_b200.config import trained_config
