@@ -114,7 +114,7 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* pos
   if (B <= 0) return MLRA_OK;
   if (W <= 0 || W % 8 != 0) return fail(MLRA_ERR_SHAPE, "cache_append: row width %d must be a positive multiple of 8", W);
   if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append: bad page geometry");
-  mlra::cache_append_kernel<<<B, 64, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_ex(mlra::cache_append_kernel, dim3(B), dim3(64), 0, static_cast<cudaStream_t>(stream), false, 
       static_cast<const __nv_bfloat16*>(rows), block_table, positions, W, page_size, max_pages, advance,
       static_cast<__nv_bfloat16*>(pool));
   return cuda_check("cache_append launch");
@@ -137,7 +137,7 @@ static int absorb_impl(const void* q_nope, const void* q_rope, const void* w_uk,
     if (int rc = set_smem_once(kern, hg_done, 200 * 1024)) return rc;
     const int NCOL = NB * DLAT;
     dim3 grid((NCOL + NT - 1) / NT, H, (B + mlra::kHG_S - 1) / mlra::kHG_S);
-    kern<<<grid, mlra::kHG_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(q_nope),
+    launch_ex(kern, dim3(grid), dim3(mlra::kHG_THREADS), smem, st, false, static_cast<const __nv_bfloat16*>(q_nope),
                                                 static_cast<const __nv_bfloat16*>(w_uk), q_abs, B, H, DH, NCOL, 1,
                                                 score_scale, NB, DLAT, static_cast<const __nv_bfloat16*>(q_rope),
                                                 DR > 0 ? static_cast<__nv_bfloat16*>(q_rope_out) : nullptr, DR);
@@ -191,7 +191,7 @@ int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int
   if (dr < 0 || dr % 2 != 0 || drp < dr || drp % 2 != 0)
     return fail(MLRA_ERR_CONFIG, "cache_append_latent: rope width %d (padded %d) must be even", dr, drp);
   if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append_latent: bad page geometry");
-  mlra::cache_append_latent_kernel<<<B, mlra::kK0Threads, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_ex(mlra::cache_append_latent_kernel, dim3(B), dim3(mlra::kK0Threads), 0, static_cast<cudaStream_t>(stream), false, 
       kv_raw, kr_raw, rope_pos, slots, block_table, d_c, bs, block0, nblocks, dlp, dr, drp, alpha_kv, rope_base, eps,
       page_size, max_pages, norm_groups, advance, static_cast<__nv_bfloat16*>(pool));
   return cuda_check("cache_append_latent launch");
@@ -522,11 +522,11 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     return fused ? MLRA_OK : tp_pending;
   }
   if (upproj == 0) {
-    mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128 * mlra::kMergeQ, 0, st>>>(
+    launch_ex(mlra::merge_splits_kernel, dim3(dim3(rows, (DLAT + 127) / 128)), dim3(128 * mlra::kMergeQ), 0, st, false, 
         o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status, seq_splits);
     return cuda_check("merge launch");
   }
-  mlra::merge_splits_kernel<<<dim3(rows, (DLAT + 127) / 128), 128 * mlra::kMergeQ, 0, st>>>(
+  launch_ex(mlra::merge_splits_kernel, dim3(dim3(rows, (DLAT + 127) / 128)), dim3(128 * mlra::kMergeQ), 0, st, false, 
       o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status, seq_splits);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;
@@ -542,7 +542,7 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     if (dev < 32) attr_done |= 1u << dev;
   }
   dim3 grid((DH + NT - 1) / NT, H, ((B + mlra::kHG_S - 1) / mlra::kHG_S) * kparts);
-  kern<<<grid, mlra::kHG_THREADS, smem, st>>>(zbuf, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
+  launch_ex(kern, dim3(grid), dim3(mlra::kHG_THREADS), smem, st, false, zbuf, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
                                               DH, kparts, alpha, 0, 0, nullptr, nullptr, 0);
   if (int rc = cuda_check("up-projection launch")) return rc;
   return tp_pending;
@@ -798,7 +798,7 @@ static int outproj_launch(mlra::OutProjParams& p, const float* const* attn, cons
   for (int r = 0; r < nlocal; ++r) {
     if (attn[r] == nullptr || ws[r] == nullptr || p.w_o[r] == nullptr || p.y[r] == nullptr)
       return fail(MLRA_ERR_CONFIG, "outproj: null tensor pointer (rank slot %d)", r);
-    mlra::outproj_gate_kernel<<<(n / 8 + 255) / 256, 256, 0, st>>>(attn[r], gate != nullptr ? gate[r] : nullptr,
+    launch_ex(mlra::outproj_gate_kernel, dim3((n / 8 + 255) / 256), dim3(256), 0, st, false, attn[r], gate != nullptr ? gate[r] : nullptr,
                                                                    static_cast<__nv_bfloat16*>(ws[r]), n);
     p.a[r] = static_cast<const __nv_bfloat16*>(ws[r]);
   }
@@ -1032,7 +1032,7 @@ int launch_prefill(const PoolMaps* pm, const void* q_abs, const void* q_rope, co
   static unsigned done = 0;
   if (int rc = set_smem_once(kern, done, L::kSmem)) return rc;
   const int nqt = (p.n + mlra::kPfT - 1) / mlra::kPfT;
-  kern<<<nqt * p.H, mlra::kPfThreads, L::kSmem, st>>>(pm->lat, pm->rope, qm, rm, wm, p);
+  launch_ex(kern, dim3(nqt * p.H), dim3(mlra::kPfThreads), L::kSmem, st, false, pm->lat, pm->rope, qm, rm, wm, p);
   return cuda_check("prefill_attention launch");
 }
 }  // namespace
@@ -1107,7 +1107,7 @@ extern "C" int mlra_decode_plan(const int32_t* seqlens, int B, int tile_tokens, 
   const size_t smem = size_t(2) * B * sizeof(int);
   if (smem > 48 * 1024) return fail(MLRA_ERR_CONFIG, "decode_plan: batch %d too large", B);
   (void)lse_part, (void)NB, (void)H;  // (kept in the signature: the K2 partial layout the plan serves)
-  mlra::decode_plan_kernel<<<1, mlra::kPlanThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+  launch_ex(mlra::decode_plan_kernel, dim3(1), dim3(mlra::kPlanThreads), smem, static_cast<cudaStream_t>(stream), false, 
       seqlens, B, tile_tokens, ctas, nsplit_max, plan, seq_splits);
   return cuda_check("decode_plan launch");
 }

@@ -473,9 +473,6 @@ __device__ __forceinline__ void fused_combine(const FuseArgs& f, const float* __
 __device__ __forceinline__ void st_shared_cluster_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
 
 __host__ __device__ inline int cluster_heads_per_cta(int H, int nsplit) { return (H + nsplit - 1) / nsplit; }
 // ring bytes the cluster epilogue needs: O [npad][dlat] + lse [npad] + W^UV of the CTA's heads +

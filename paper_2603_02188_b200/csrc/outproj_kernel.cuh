@@ -129,7 +129,8 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
   const __nv_bfloat16* w = p.w_o[li];
   const uint32_t ring_u32 = smem_u32(ring), a_u32 = smem_u32(a_tile), slots_u32 = smem_u32(slots);
   MLRA_OP_STAMP(0);
-  bool waited = false;
+  cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (peers started)
+  bool waited = false, cl_started = false;
 
   for (int m0 = 0; m0 < B; m0 += kOpM) {
     float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -189,6 +190,10 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
       __syncthreads();  // ring and A tile are reused by the next pass
     }
     MLRA_OP_STAMP(2);
+    if (!cl_started) {  // every CTA of the cluster runs: its shared memory may be written
+      cluster_wait_acquire();
+      cl_started = true;
+    }
     // slice partial of rows m0+g, m0+g+8 -> owner (m % KS) slot [ks][m / KS] through DSMEM
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -203,6 +208,7 @@ outproj_allreduce_kernel(const __grid_constant__ OutProjParams p) {
     }
   }
   if (!waited) griddep_wait();  // (empty K slice) keep the dependency on K4a
+  if (!cl_started) cluster_wait_acquire();
   cluster_arrive_release();
   cluster_wait_acquire();
   MLRA_OP_STAMP(3);

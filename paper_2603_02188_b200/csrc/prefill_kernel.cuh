@@ -18,8 +18,9 @@
 //          OUT += Z_hi . W^UV_(b),(h) + Z_lo . W^UV_(b),(h)   (N = DH)
 //   out[q, h, :] = alpha * OUT[q]
 // TMEM: S double buffer (2 x 128 columns) + O (DLAT) + OUT (DH) <= 512.
-// Warps: 0 = TMA producer, 1 = MMA issuer (elected lane), 2..9 = softmax / epilogue (two
-// warps per TMEM lane quarter; thread = (query row, half of the columns)). Lazy rescale: the running max moves only
+// Warps: 0 = TMA producer, 1 = QK issuer, 10 = PV + up-projection issuer (elected lanes),
+// 2..9 = softmax / epilogue (two warps per TMEM lane quarter; thread = (query row, half of
+// the columns)). Lazy rescale: the running max moves only
 // when a row's tile max exceeds it by 2^8, then O's row is rescaled in TMEM (after the PVs
 // issued so far have completed).
 //
@@ -42,17 +43,18 @@ struct PrefillParams {
   int n, H, NB, DR, page_size, max_pages;
   float alpha;
   int rope_col;                // first rope column of a pool row (NB * DLAT)
-  volatile int* progress;      // dev: per-CTA [8] progress words in mapped host memory, or null
+  volatile int* progress;      // dev: per-CTA [16] progress words (one per warp) in mapped host memory, or null
   float* dbg_s;                // dev: raw S rows of CTA dbg_cta's first key tile [128][128], or null
   int dbg_cta;
 };
 
 #define PF_PROG(slot, v)                                                                  \
   do {                                                                                   \
-    if (p.progress != nullptr && (threadIdx.x & 31) == 0) p.progress[blockIdx.x * 8 + (slot)] = (v); \
+    if (p.progress != nullptr && (threadIdx.x & 31) == 0) p.progress[blockIdx.x * 16 + (slot)] = (v); \
   } while (0)
 
-constexpr int kPfThreads = 320;  // TMA warp, MMA warp, 8 softmax warps (2 per TMEM lane quarter)
+constexpr int kPfThreads = 352;  // TMA warp, QK warp, 8 softmax warps (2 per TMEM lane quarter), PV warp
+constexpr int kPfPvWarp = 10;
 constexpr int kPfT = 128;        // query rows and key tokens per tile
 constexpr int kPfChunk = kPfT * 128;  // [128 rows][64 bf16] SW128 chunk (16 KB)
 
@@ -186,8 +188,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       }
     }
     __syncwarp();  // reconverge before the CTA barrier (an aligned barrier needs the whole warp)
-  } else if (warp == 1) {
-    // ============================================================ MMA issuer
+  } else if (warp == 1 || warp == kPfPvWarp) {
+    // ============================================================ MMA issuers (elected lane each)
+    // Warp 1 issues every QK as soon as its K/V tile and S slot are there (up to two tiles
+    // ahead of the softmax); warp 10 issues every PV as soon as its P is, then the branch's
+    // up-projection. With one issuer, QK(j+2) queued behind the wait for P(j) and the
+    // softmax sat idle waiting for S. tcgen05.commit tracks the issuing thread's MMAs: PV(j)
+    // exists only after S(j) = QK(j) completed, so the PV warp's commits also release the K/V
+    // stage QK(j) read.
     const uint64_t kmaj = make_sdesc(0, 16, 1024, kSw128);         // K-major, 128B swizzle
     const uint64_t vmaj = make_sdesc(0, kPfChunk, 1024, kSw128);   // MN-major V (LBO = next 64 columns)
     const uint64_t wmaj = make_sdesc(0, DLAT * 128, 1024, kSw128); // MN-major W^UV (LBO = next 64 columns)
@@ -198,64 +206,59 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t q_addr = sm + L::kQ, p_addr = sm + L::kP, w_addr = sm + L::kW;
     int g = 0;
     for (int b = 0; b < NB; ++b) {
-      pf_wait(q_full, b & 1, 2);
-      tc_fence_after();
-      auto issue_qk = [&](int j, int gg) {
-        const int s = gg & 1;
-        pf_wait(&kv_full[s], (gg >> 1) & 1, 3);
-        pf_wait(&s_empty[s], ((gg >> 1) & 1) ^ 1, 14);
+      if (warp == 1) {
+        pf_wait(q_full, b & 1, 2);
         tc_fence_after();
-        const uint32_t kv = sm + L::kKV + s * L::kKVStage;
-        const uint32_t d = tbase + L::S_COL + s * kPfT;
-        uint32_t acc = 0;
+        PF_PROG(1, 100 + g);
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int s = g & 1;
+          pf_wait(&kv_full[s], (g >> 1) & 1, 3);
+          pf_wait(&s_empty[s], ((g >> 1) & 1) ^ 1, 14);
+          tc_fence_after();
+          const uint32_t kv = sm + L::kKV + s * L::kKVStage;
+          const uint32_t d = tbase + L::S_COL + s * kPfT;
+          uint32_t acc = 0;
 #pragma unroll
-        for (int c = 0; c < L::kLatChunks; ++c)
+          for (int c = 0; c < L::kLatChunks; ++c)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_bf16_ss_w(d, kmaj + ((q_addr + c * kPfChunk + kk * 32) >> 4), kmaj + ((kv + c * kPfChunk + kk * 32) >> 4),
-                          idesc_qk, acc);
-            acc = 1;
-          }
-        for (int kk = 0; kk < kq_rope; ++kk)
-          mma_bf16_ss_w(d, kmaj + ((q_addr + L::kLatChunks * kPfChunk + kk * 32) >> 4),
-                        kmaj + ((kv + L::kLatChunks * kPfChunk + kk * 32) >> 4), idesc_qk, 1);
-        mma_commit_w(&s_full[s]);
-      };
-      auto issue_pv = [&](int j, int gg) {
-        const int s = gg & 1;
-        pf_wait(&p_full[s], (gg >> 1) & 1, 4);
+            for (int kk = 0; kk < 4; ++kk) {
+              mma_bf16_ss_w(d, kmaj + ((q_addr + c * kPfChunk + kk * 32) >> 4),
+                            kmaj + ((kv + c * kPfChunk + kk * 32) >> 4), idesc_qk, acc);
+              acc = 1;
+            }
+          for (int kk = 0; kk < kq_rope; ++kk)
+            mma_bf16_ss_w(d, kmaj + ((q_addr + L::kLatChunks * kPfChunk + kk * 32) >> 4),
+                          kmaj + ((kv + L::kLatChunks * kPfChunk + kk * 32) >> 4), idesc_qk, 1);
+          mma_commit_w(&s_full[s]);
+        }
+      } else {
+        PF_PROG(kPfPvWarp, 100 + g);
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int s = g & 1;
+          pf_wait(&p_full[s], (g >> 1) & 1, 4);
+          tc_fence_after();
+          const uint32_t kv = sm + L::kKV + s * L::kKVStage, pb = p_addr + s * L::kPBytes;
+#pragma unroll
+          for (int k = 0; k < kPfT / 16; ++k)  // 16 keys per step: P chunk k/4, V rows 16k..
+            mma_bf16_ss_w(tbase + L::O_COL, kmaj + ((pb + (k >> 2) * kPfChunk + (k & 3) * 32) >> 4),
+                          vmaj + ((kv + k * 2048) >> 4), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+          mma_commit_w(&kv_empty[s]);
+          mma_commit_w(&pv_done[s]);
+        }
+        // up-projection of branch b into OUT (ascending branch order: the reference's sum order)
+        pf_wait(z_full, b & 1, 5);
+        pf_wait(w_full, b & 1, 6);
         tc_fence_after();
-        const uint32_t kv = sm + L::kKV + s * L::kKVStage, pb = p_addr + s * L::kPBytes;
 #pragma unroll
-        for (int k = 0; k < kPfT / 16; ++k)  // 16 keys per step: P chunk k/4, V rows 16k..
-          mma_bf16_ss_w(tbase + L::O_COL, kmaj + ((pb + (k >> 2) * kPfChunk + (k & 3) * 32) >> 4),
-                        vmaj + ((kv + k * 2048) >> 4), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit_w(&kv_empty[s]);
-        mma_commit_w(&pv_done[s]);
-      };
-      const int g0 = g;
-      PF_PROG(1, 100 + g0);
-      issue_qk(0, g0);
-      for (int j = 1; j < ntiles; ++j) {
-        issue_qk(j, g0 + j);
-        issue_pv(j - 1, g0 + j - 1);
+        for (int half = 0; half < 2; ++half) {  // Z_hi (P buffer 0), Z_lo (P buffer 1)
+          const uint32_t z = p_addr + half * L::kPBytes;
+#pragma unroll
+          for (int k = 0; k < DLAT / 16; ++k)
+            mma_bf16_ss_w(tbase + L::OUT_COL, kmaj + ((z + (k >> 2) * kPfChunk + (k & 3) * 32) >> 4),
+                          wmaj + ((w_addr + k * 2048) >> 4), idesc_up, (b > 0 || half > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit_w(up_done);
       }
-      issue_pv(ntiles - 1, g0 + ntiles - 1);
-      g = g0 + ntiles;
-      PF_PROG(1, 1000 + b);
-      // up-projection of branch b into OUT (ascending branch order: the reference's sum order)
-      pf_wait(z_full, b & 1, 5);
-      pf_wait(w_full, b & 1, 6);
-      tc_fence_after();
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {  // Z_hi (P buffer 0), Z_lo (P buffer 1)
-        const uint32_t z = p_addr + half * L::kPBytes;
-#pragma unroll
-        for (int k = 0; k < DLAT / 16; ++k)
-          mma_bf16_ss_w(tbase + L::OUT_COL, kmaj + ((z + (k >> 2) * kPfChunk + (k & 3) * 32) >> 4),
-                        wmaj + ((w_addr + k * 2048) >> 4), idesc_up, (b > 0 || half > 0 || k > 0) ? 1u : 0u);
-      }
-      mma_commit_w(up_done);
     }
   } else {
     // ============================================================ softmax / epilogue

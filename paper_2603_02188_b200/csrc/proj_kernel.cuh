@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
   const uint32_t wt_u32 = smem_u32(wt), xt_u32 = smem_u32(xt);
 
   pj_stamp(p, 0);
+  cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (peers started)
   if (tid == 0) {
     tma_prefetch_desc(&w_map);
     for (int b = 0; b < nbox; ++b) mbar_init(&bars[b], 1);
@@ -216,7 +217,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
   }
   __syncthreads();
   pj_stamp(p, 4);
-  // slab partial of this slice -> cluster rank 0's slot [ks] (DSMEM; rank 0 stores locally)
+  // slab partial of this slice -> cluster rank 0's slot [ks] (DSMEM; rank 0 stores locally),
+  // once every CTA of the cluster is known to run (its shared memory exists)
+  cluster_wait_acquire();
   const uint32_t slot_u32 = mapa_shared(smem_u32(slots + ks * kPjM * kPjNC), 0);
   for (int i = tid; i < kPjM * kPjNC; i += kPjThreads) st_shared_cluster_f32(slot_u32 + i * 4, red[i] + red[kPjM * kPjNC + i]);
   cluster_arrive_release();
