@@ -302,14 +302,14 @@ int mlra_prefill_attention(const void* q_abs, const void* q_rope, const void* w_
 
 /*
  * Prefill projection helpers (the n-row projections run as cuBLAS bf16 GEMMs around them):
- * mlra_rows_split: x [n, ldx] fp32 (first K columns) -> hi, lo bf16 [n, K] with x (norm = 0) or
- *   alpha * rmsnorm(x) (norm != 0; tensors.py:83-87) = hi + lo to ~16 bits.
+ * mlra_rows_split: x [n, ldx] fp32 (first K columns) -> hi, lo bf16 (row stride ldo >= K) with x
+ *   (norm = 0) or alpha * rmsnorm(x) (norm != 0; tensors.py:83-87) = hi + lo to ~16 bits.
  * mlra_query_epilogue: y [n, ldy] fp32 = [q_x (nq columns) | q_r (H * dr)] -> q_out bf16 [n, nq] =
  *   q_scale * q_x, r_out bf16 [n, H, drq] = r_scale * rope(q_r, pos0 + row) (rope.py:37-60),
  *   columns [dr, drq) zero.
  */
 int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, float alpha, float eps, void* hi, void* lo,
-                    void* stream);
+                    int ldo, void* stream);
 int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H, int dr, int drq, int pos0, float rope_base,
                         float q_scale, float r_scale, void* q_out, void* r_out, void* stream);
 

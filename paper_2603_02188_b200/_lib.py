@@ -55,7 +55,7 @@ SIGNATURES = {
     "mlra_ipc_open": (_I, [_P, _P]),
     "mlra_ipc_close": (_I, [_P]),
     "mlra_prefill_attention": (_I, [_P] * 6 + [_I] * 11 + [_F, _P]),
-    "mlra_rows_split": (_I, [_P] + [_I] * 4 + [_F, _F, _P, _P, _P]),
+    "mlra_rows_split": (_I, [_P] + [_I] * 4 + [_F, _F, _P, _P, _I, _P]),
     "mlra_query_epilogue": (_I, [_P] + [_I] * 7 + [_F, _F, _F, _P, _P, _P]),
     "mlra_decode_plan": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _P]),
     "mlra_decode_step_ragged": (_I, [_P] * 9 + [_I] * 11 + [_F, _F, _P]),

@@ -1075,11 +1075,11 @@ extern "C" int mlra_prefill_attention(const void* q_abs, const void* q_rope, con
 }
 
 extern "C" int mlra_rows_split(const float* x, int n, int K, int ldx, int norm, float alpha, float eps, void* hi,
-                               void* lo, void* stream) {
+                               void* lo, int ldo, void* stream) {
   if (n <= 0) return MLRA_OK;
-  if (K <= 0 || ldx < K) return fail(MLRA_ERR_SHAPE, "rows_split: K=%d ldx=%d", K, ldx);
+  if (K <= 0 || ldx < K || ldo < K) return fail(MLRA_ERR_SHAPE, "rows_split: K=%d ldx=%d ldo=%d", K, ldx, ldo);
   if (launch_ex(mlra::rows_split_kernel, dim3(n), dim3(256), 0, static_cast<cudaStream_t>(stream), false, x, K, ldx,
-                norm, alpha, eps, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo)) != cudaSuccess)
+                norm, alpha, eps, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo), ldo) != cudaSuccess)
     return cuda_check("rows_split launch");
   return cuda_check("rows_split launch");
 }
@@ -1088,7 +1088,7 @@ extern "C" int mlra_query_epilogue(const float* y, int n, int ldy, int nq, int H
                                    float rope_base, float q_scale, float r_scale, void* q_out, void* r_out,
                                    void* stream) {
   if (n <= 0) return MLRA_OK;
-  if (nq < 0 || H <= 0 || dr < 0 || dr % 2 != 0 || drq < dr || drq % 2 != 0 || ldy < nq + H * dr)
+  if (nq < 0 || H <= 0 || dr < 0 || dr % 2 != 0 || dr > 128 || drq < dr || drq % 2 != 0 || ldy < nq + H * dr)
     return fail(MLRA_ERR_SHAPE, "query_epilogue: bad dims nq=%d H=%d dr=%d drq=%d ldy=%d", nq, H, dr, drq, ldy);
   if (launch_ex(mlra::query_epilogue_kernel, dim3(n), dim3(256), 0, static_cast<cudaStream_t>(stream), false, y, ldy,
                 nq, H, dr, drq, pos0, rope_base, q_scale, r_scale, static_cast<__nv_bfloat16*>(q_out),

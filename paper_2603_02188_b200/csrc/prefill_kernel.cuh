@@ -422,11 +422,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 }
 
 // ---- prefill projection helpers (the n-row projections run as cuBLAS bf16 GEMMs) -----------
-// rows_split: per row x -> (alpha * rmsnorm(x) when norm, else x) as bf16 hi + lo planes [n, K]
+// rows_split: per row x -> (alpha * rmsnorm(x) when norm, else x) as bf16 hi + lo planes (row
+// stride ldo: two [n, K] planes, or the halves of one [n, 2K] operand)
 // (the GEMM's activations at ~16-bit mantissa; tensors.py:83-87 rmsnorm, latent.py:134).
 __global__ void __launch_bounds__(256) rows_split_kernel(const float* __restrict__ x, int K, int ldx, int norm,
                                                          float alpha, float eps, __nv_bfloat16* __restrict__ hi,
-                                                         __nv_bfloat16* __restrict__ lo) {
+                                                         __nv_bfloat16* __restrict__ lo, int ldo) {
   __shared__ float red[8];
   const int row = blockIdx.x, tid = threadIdx.x;
   const float* xr = x + size_t(row) * ldx;
@@ -446,33 +447,51 @@ __global__ void __launch_bounds__(256) rows_split_kernel(const float* __restrict
   for (int c = tid; c < K; c += 256) {
     const float v = xr[c] * sc;
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    hi[size_t(row) * K + c] = h;
-    lo[size_t(row) * K + c] = __float2bfloat16_rn(v - __bfloat162float(h));
+    hi[size_t(row) * ldo + c] = h;
+    lo[size_t(row) * ldo + c] = __float2bfloat16_rn(v - __bfloat162float(h));
   }
 }
 
 // query_epilogue: y [n, ldy] fp32 = [q_x (nq) | q_r (H * dr)] -> q_out bf16 [n, nq] = q_scale * q_x,
-// r_out bf16 [n, H, drq] = r_scale * rope(q_r, pos0 + row) (pairs (2l, 2l+1), rope.py:37-60; angle in
-// fp64 reduced mod 2 pi), columns [dr, drq) zero.
+// r_out bf16 [n, H, drq] = r_scale * rope(q_r, pos0 + row) (pairs (2l, 2l+1), rope.py:37-60),
+// columns [dr, drq) zero. The row's dr/2 angles (fp64 product, reduced mod 2 pi) and their
+// sin / cos are formed once into smem and shared by the H heads.
 __global__ void __launch_bounds__(256) query_epilogue_kernel(const float* __restrict__ y, int ldy, int nq, int H,
                                                              int dr, int drq, int pos0, float rope_base,
                                                              float q_scale, float r_scale,
                                                              __nv_bfloat16* __restrict__ q_out,
                                                              __nv_bfloat16* __restrict__ r_out) {
+  __shared__ float cs_sh[64], sn_sh[64];
   const int row = blockIdx.x, tid = threadIdx.x;
   const float* yr = y + size_t(row) * ldy;
-  for (int c = tid; c < nq; c += 256) q_out[size_t(row) * nq + c] = __float2bfloat16_rn(yr[c] * q_scale);
-  const double pos = double(pos0 + row);
+  if (tid < dr / 2) {
+    const double theta = pow(double(rope_base), -2.0 * tid / dr);
+    const double a = double(pos0 + row) * theta;
+    const double two_pi = 6.283185307179586476925286766559;
+    float sn, cs;
+    sincosf(float(a - two_pi * floor(a / two_pi)), &sn, &cs);
+    cs_sh[tid] = cs;
+    sn_sh[tid] = sn;
+  }
+  for (int c = tid * 4; c < nq; c += 256 * 4) {
+    if (c + 4 <= nq && (nq % 4) == 0) {
+      const float4 v = *reinterpret_cast<const float4*>(yr + c);
+      uint2 o;
+      o.x = pack_bf16(v.x * q_scale, v.y * q_scale);
+      o.y = pack_bf16(v.z * q_scale, v.w * q_scale);
+      *reinterpret_cast<uint2*>(q_out + size_t(row) * nq + c) = o;
+    } else {
+      for (int j = c; j < min(nq, c + 4); ++j) q_out[size_t(row) * nq + j] = __float2bfloat16_rn(yr[j] * q_scale);
+    }
+  }
+  __syncthreads();
   for (int i = tid; i < H * (drq / 2); i += 256) {
     const int h = i / (drq / 2), l = i % (drq / 2);
     float e = 0.f, o = 0.f;
     if (2 * l + 1 < dr) {
-      const double theta = pow(double(rope_base), -2.0 * l / dr);
-      float sn, cs;
-      sincosf(float(fmod(pos * theta, 6.283185307179586476925286766559)), &sn, &cs);
       const float x0 = yr[nq + h * dr + 2 * l], x1 = yr[nq + h * dr + 2 * l + 1];
-      e = (x0 * cs - x1 * sn) * r_scale;
-      o = (x0 * sn + x1 * cs) * r_scale;
+      e = (x0 * cs_sh[l] - x1 * sn_sh[l]) * r_scale;
+      o = (x0 * sn_sh[l] + x1 * cs_sh[l]) * r_scale;
     }
     reinterpret_cast<__nv_bfloat162*>(r_out + (size_t(row) * H + h) * drq)[l] = __floats2bfloat162_rn(e, o);
   }

@@ -480,7 +480,9 @@ def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t
     kp = st.kproj
     use_k6 = not force_pseudo and prefill_kernel_fits(cfg, layout, st.own, pc.page_size)
     # the n rows' projections (cuBLAS bf16); K6 reads 64-column rotary query rows
-    kv_raw, kr_raw, qn, q_r = kp.project_gemm(h_t, cache.pos_offset, drq=64 if use_k6 else layout.drp)
+    scale = ops.score_scale(cfg.tau)
+    kv_raw, kr_raw, qn, q_r = kp.project_gemm(h_t, cache.pos_offset, drq=64 if use_k6 else layout.drp,
+                                              rope_scale=scale if use_k6 else None)
     kv_raw = kp.kv_slice(kv_raw, names)
     ops.cache_append_latent(kv_raw, kr_raw, positions, None, pc.block_table, pc.pool, pc.page_size, branches=blocks,
                             block0=block0, nblocks=nblocks, dlp=layout.dlp, drp=layout.drp,
@@ -492,15 +494,13 @@ def prefill_into(cfg: AttnConfig, st: "_StepState", cache: PagedLatentCache, h_t
     nb, dlat = kernel_geometry(layout, st.own)
     sub, dls = ops.latent_geometry(dlat)
     alpha = calib_factors(cfg).alpha_attn if cfg.variant == "mlra" else 1.0
-    scale = ops.score_scale(cfg.tau)
     if use_k6:
         # absorption of the n queries as one batched GEMM over the heads (bf16 operands, fp32
         # accumulation, tau*log2e applied before the bf16 rounding -- K1's arithmetic), written
-        # head-major [H, n, NB*DLAT] as K6 reads it; the rotary queries scaled the same way
+        # head-major [H, n, NB*DLAT] as K6 reads it (the rotary queries come scaled from the epilogue)
         q_abs = torch.baddbmm(torch.zeros((1, 1, 1), dtype=torch.bfloat16, device=dev), qn.transpose(0, 1), w_uk,
                               beta=0.0, alpha=scale)
-        q_rs = (q_r.float() * scale).to(torch.bfloat16)
-        return ops.prefill_attention(q_abs.view(cfg.h, n, nb, dlat), q_rs, w_uv, pc.pool, pc.block_table,
+        return ops.prefill_attention(q_abs.view(cfg.h, n, nb, dlat), q_r, w_uv, pc.pool, pc.block_table,
                                      pc.page_size, nb, dlat, cfg.d_h_rope, alpha)
     qn, qr = _pad_rope(qn, q_r, layout)
     # ---- pseudo-sequence path: n queries of lengths 1..n over the same pages

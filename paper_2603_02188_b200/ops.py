@@ -597,16 +597,23 @@ def prefill_attention(q_abs: torch.Tensor, q_rope: torch.Tensor, w_uv_packed: to
     return out
 
 
-def rows_split(x: torch.Tensor, K: int, norm: bool = False, alpha: float = 1.0, eps: float = 1e-6):
-    """x [n, >= K] fp32 (first K columns) -> (hi, lo) bf16 [n, K]: x or alpha * rmsnorm(x)."""
+def rows_split(x: torch.Tensor, K: int, norm: bool = False, alpha: float = 1.0, eps: float = 1e-6,
+               stacked: bool = False):
+    """x [n, >= K] fp32 (first K columns) -> (hi, lo) bf16 [n, K]: x or alpha * rmsnorm(x);
+    ``stacked``: one [n, 2K] tensor [hi | lo] (the operand of a single GEMM against [W; W])."""
     _need(x, torch.float32, "x", 2)
     n = x.shape[0]
-    hi = torch.empty((n, K), dtype=torch.bfloat16, device=x.device)
-    lo = torch.empty_like(hi)
-    rc = _lib.load().mlra_rows_split(x.data_ptr(), n, K, x.shape[1], int(norm), float(alpha), float(eps),
-                                     hi.data_ptr(), lo.data_ptr(), _stream())
+    if stacked:
+        both = torch.empty((n, 2 * K), dtype=torch.bfloat16, device=x.device)
+        hi_p, lo_p, ld = both.data_ptr(), both.data_ptr() + K * 2, 2 * K
+    else:
+        hi = torch.empty((n, K), dtype=torch.bfloat16, device=x.device)
+        lo = torch.empty_like(hi)
+        hi_p, lo_p, ld = hi.data_ptr(), lo.data_ptr(), K
+    rc = _lib.load().mlra_rows_split(x.data_ptr(), n, K, x.shape[1], int(norm), float(alpha), float(eps), hi_p, lo_p,
+                                     ld, _stream())
     _lib.check(rc, "mlra_rows_split")
-    return hi, lo
+    return both if stacked else (hi, lo)
 
 
 def query_epilogue(y: torch.Tensor, nq: int, heads: int, dr: int, drq: int, pos0: int, q_scale: float = 1.0,

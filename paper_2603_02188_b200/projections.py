@@ -87,11 +87,10 @@ class GqaProjector:
         return q, k, v
 
 
-def _gemm2(hi: torch.Tensor, lo: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-    """(hi + lo) [M, K] (bf16 planes) times w [K, N] bf16: two cuBLAS bf16 GEMMs, fp32 result."""
-    y = torch.mm(hi, w, out_dtype=torch.float32)
-    y += torch.mm(lo, w, out_dtype=torch.float32)
-    return y
+def _gemm2(hilo: torch.Tensor, w2: torch.Tensor) -> torch.Tensor:
+    """[hi | lo] [M, 2K] (bf16 planes of fp32 activations) times [W; W] [2K, N] bf16: ONE cuBLAS
+    bf16 GEMM with fp32 accumulation and output (= (hi + lo) . W)."""
+    return torch.mm(hilo, w2, out_dtype=torch.float32)
 
 
 class KernelProjector:
@@ -152,6 +151,7 @@ class KernelProjector:
         sf = calib_factors(cfg)
         self.alpha_q, self.alpha_kv = float(sf.alpha_q), float(sf.alpha_kv)
         self._bufs: dict = {}
+        self._w2 = None
 
     def _pack(self, m):
         """bf16 [K, N] (cuBLAS paths) and its slab pack for K-1 (``ops.slab_pack``)."""
@@ -204,22 +204,24 @@ class KernelProjector:
         outs = [self.project(hidden[m0:m0 + 16], pos[m0:m0 + 16]) for m0 in range(0, M, 16)]
         return tuple(torch.cat([o[i] for o in outs]) for i in range(4))
 
-    def project_gemm(self, hidden: torch.Tensor, pos0: int, drq: int | None = None):
+    def project_gemm(self, hidden: torch.Tensor, pos0: int, drq: int | None = None, rope_scale: float | None = None):
         """``project`` for the n rows of a prefill at positions pos0 .. pos0+n-1: the same packed
         bf16 weights through cuBLAS bf16 GEMMs (real GEMMs at n rows, where a weight stream per 16
         rows would not pay), the activations as bf16 hi + lo (``ops.rows_split``, with the query
         rmsnorm) like K-1's operands, and ``ops.query_epilogue`` for the scaling and rope. Returns
-        (kv_raw, kr_raw, q [n, ...] bf16, q_rope [n, H, drq] bf16)."""
+        (kv_raw, kr_raw, q [n, ...] bf16, q_rope [n, H, drq] bf16); ``rope_scale`` overrides the
+        rotary query's scale (the prefill kernel takes it pre-scaled by tau*log2e)."""
         hidden = hidden.to(device=self.device, dtype=torch.float32).contiguous()
         n = hidden.shape[0]
-        hi, lo = ops.rows_split(hidden, hidden.shape[1])
-        y = _gemm2(hi, lo, self.w_down)
+        if self._w2 is None:  # [W; W] for the one-GEMM hi + lo product
+            self._w2 = (torch.cat([self.w_down, self.w_down]), torch.cat([self.w_query, self.w_query]))
+        y = _gemm2(ops.rows_split(hidden, hidden.shape[1], stacked=True), self._w2[0])
         n_q, n_kv = self.n_q, self.n_kv
         kv_raw = y[:, n_q:n_q + n_kv].contiguous()
         kr_raw = y[:, n_q + n_kv:n_q + n_kv + self.n_kr].contiguous()
-        hi, lo = ops.rows_split(y, n_q, norm=True, alpha=self.alpha_q)
-        q = _gemm2(hi, lo, self.w_query)
-        qx, qr = ops.query_epilogue(q, self.nq, self.H, self.dr, drq or self.drp, pos0, self.q_scale, self.r_scale)
+        q = _gemm2(ops.rows_split(y, n_q, norm=True, alpha=self.alpha_q, stacked=True), self._w2[1])
+        r_scale = self.r_scale if rope_scale is None else rope_scale
+        qx, qr = ops.query_epilogue(q, self.nq, self.H, self.dr, drq or self.drp, pos0, self.q_scale, r_scale)
         return kv_raw, kr_raw, qx.reshape((n,) + self.q_shape), qr
 
     def kv_slice(self, kv_raw: torch.Tensor, names) -> torch.Tensor:

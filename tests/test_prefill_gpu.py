@@ -118,4 +118,6 @@ def test_prefill_kernel_matches_pseudo_sequence_path(variant, n):
         outs.append(dec.prefill_into(cfg, st, cache, h, force_pseudo=force).double().cpu().numpy())
     errs = [ak.max_rel_err(outs[1][t], outs[0][t]) for t in range(n)]
     print(variant, n, "max_rel_err K6 vs pseudo-sequences", max(errs))
-    assert max(errs) <= 5e-3, (int(np.argmax(errs)), max(errs))
+    # same bf16 cache and q~; the rotary query is rounded once (K6: scaled in the projection
+    # epilogue) vs twice (pseudo path: rounded, then scaled by K1) -- one bf16 ulp apart
+    assert max(errs) <= 1e-2, (int(np.argmax(errs)), max(errs))
