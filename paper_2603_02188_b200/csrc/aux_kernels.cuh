@@ -311,9 +311,12 @@ __global__ void __launch_bounds__(128 * kMergeQ)
 merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, float* __restrict__ z, int B,
                     int NB, int H, int DLAT, int nsplit, float alpha, int zout_bnh, int* __restrict__ status,
                     const int32_t* __restrict__ seq_splits) {
+  // blockDim.x = CW * kMergeQ: CW latent columns per CTA (128, or 32 when the rows are few and
+  // the splits many -- batch-1 decode -- so the grid still covers the SMs)
   __shared__ float wsh[kMergeMaxSplits];
   __shared__ float part[kMergeQ][128];
-  const int row = blockIdx.x, cl = threadIdx.x % 128, qk = threadIdx.x / 128, c = blockIdx.y * 128 + cl;
+  const int CW = blockDim.x / kMergeQ;
+  const int row = blockIdx.x, cl = threadIdx.x % CW, qk = threadIdx.x / CW, c = blockIdx.y * CW + cl;
   const int lane = threadIdx.x % 32;
   const int h = row % H, b = (row / H) % NB, s = row / (H * NB);
   const int ns = seq_splits != nullptr ? min(seq_splits[s], nsplit) : nsplit;  // splits of this sequence

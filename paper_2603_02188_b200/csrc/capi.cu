@@ -521,12 +521,13 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     if (int rc = cuda_check("combine launch")) return rc;
     return fused ? MLRA_OK : tp_pending;
   }
+  const int mcw = (long(rows) * ((DLAT + 127) / 128) < 148 && nsplit > 16) ? 32 : 128;  // merge columns per CTA
   if (upproj == 0) {
-    launch_ex(mlra::merge_splits_kernel, dim3(dim3(rows, (DLAT + 127) / 128)), dim3(128 * mlra::kMergeQ), 0, st, false, 
+    launch_ex(mlra::merge_splits_kernel, dim3(rows, (DLAT + mcw - 1) / mcw), dim3(mcw * mlra::kMergeQ), 0, st, false, 
         o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status, seq_splits);
     return cuda_check("merge launch");
   }
-  launch_ex(mlra::merge_splits_kernel, dim3(dim3(rows, (DLAT + 127) / 128)), dim3(128 * mlra::kMergeQ), 0, st, false, 
+  launch_ex(mlra::merge_splits_kernel, dim3(rows, (DLAT + mcw - 1) / mcw), dim3(mcw * mlra::kMergeQ), 0, st, false, 
       o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status, seq_splits);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;
