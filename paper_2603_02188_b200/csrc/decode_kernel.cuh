@@ -582,9 +582,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           dmax = (c < h_cnt) ? fmaxf(dmax, mx) : dmax;
         }
         // m_run is finite (0 before the first tile), so masked lanes stay at -inf. The first
-        // tile of the split always takes the slow path (uniform: no vote needed).
-        // (per group: the groups own disjoint heads, so their rescale decisions are independent)
-        const bool slow = (t == 0) ? true : named_bar_or(3 + grp, kSoftThreads / 2, dmax > thr);
+        // tile keeps the reference max 0 unless a score could overflow P (> 2^thr) or a head's
+        // scores could underflow it (< 2^-64): the exact-max slow path (warp + quarter maxima,
+        // a second barrier) is then taken only when needed -- it cost a CTA's first round ~2K
+        // cycles. (per group: the groups own disjoint heads, so their decisions are independent)
+        bool vote = dmax > thr;
+        if (t == 0) {
+          float dmin = INFINITY;
+#pragma unroll
+          for (int c = 0; c < kHG; ++c)
+            if (c < h_cnt && s[c] != -INFINITY) dmin = fminf(dmin, s[c]);
+          vote = vote || dmin < -64.f;
+        }
+        const bool slow = named_bar_or(3 + grp, kSoftThreads / 2, vote);
         if (ws == 0 && lane == 0) trace_event(p.trace, p.trace_cta, 8, r);
         bool rescale = false;
         if (slow) {
