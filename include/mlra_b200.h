@@ -250,7 +250,8 @@ int mlra_ipc_close(void* dev_ptr);
 /*
  * K-1 -- pre-attention projections: the GEMVs of latent.py:129-159
  * (latent_projections) for a decode batch, as two weight-streaming GEMM launches (M <= 16
- * rows per launch; larger M loops). Weights are bf16 and SLAB-PACKED once at load time: a
+ * rows per launch; larger M loops; K <= 3072: at most 8 slices of 384 rows). Weights are bf16
+ * and SLAB-PACKED once at load time: a
  * weight W [K, N] (row-major (in, out) as weights.py stores it) is passed as
  * [ceil(N/64)][round_up(K, 64)][64] with element [s][k][c] = W[k][64 s + c] (zero outside W), so
  * each CTA's slice is one contiguous HBM run. Activations enter as fp32 (split into bf16 hi +

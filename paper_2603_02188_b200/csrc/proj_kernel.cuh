@@ -18,7 +18,7 @@
 // and the grid's interleaved reads ran at ~10% of the DRAM bandwidth.
 //
 // Grid: slabs of 64 output columns x KS slices of K; the KS CTAs of a slab are one cluster.
-//   1. W slice: k_slice x 64 bf16 (<= 96 KB) by TMA, issued first (before griddepcontrol.wait:
+//   1. W slice: k_slice x 64 bf16 (<= 48 KB) by TMA, issued first (before griddepcontrol.wait:
 //      the weights do not depend on the previous kernel).
 //   2. X slice: the M rows of X[:, kbeg:kend) (fp32) -> (rmsnorm scale) -> bf16 hi + lo planes
 //      (two MMAs per step: ~16-bit mantissa for the activations; the weights are bf16).
@@ -33,7 +33,10 @@
 
 namespace mlra {
 
-constexpr int kPjThreads = 256, kPjNC = 64, kPjBox = 64, kPjM = 16, kPjMaxRows = 768, kPjMaxKS = 8;
+// kPjMaxRows bounds a CTA's weight slice (48 KB) so that a CTA needs ~105 KB of shared memory:
+// two fit an SM, and the query launch (a programmatic dependent) prefetches its weights into
+// SMs the down launch leaves free while the down projection still runs.
+constexpr int kPjThreads = 256, kPjNC = 64, kPjBox = 64, kPjM = 16, kPjMaxRows = 384, kPjMaxKS = 8;
 constexpr int kPjMaxBoxes = kPjMaxRows / kPjBox;
 constexpr int kPjXRow = (kPjMaxRows + 8) * 2;  // bytes per X plane row: 16 mod 128 (conflict-free ldmatrix)
 constexpr int kPjWBytes = kPjMaxRows * kPjNC * 2;
@@ -72,7 +75,8 @@ __device__ __forceinline__ void pj_stamp(const ProjParams& p, int k) {
   }
 }
 
-inline size_t proj_smem() { return size_t(kPjWBytes) + kPjXBytes + kPjRedBytes + kPjSlotBytes + 256; }
+static_assert(kPjRedBytes <= kPjXBytes, "the warp partials alias the (dead) X planes");
+inline size_t proj_smem() { return size_t(kPjWBytes) + kPjXBytes + kPjSlotBytes + 256; }
 
 __device__ __forceinline__ void st_shared_cluster_f32(uint32_t addr, float x) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(x) : "memory");
@@ -88,8 +92,8 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
   extern __shared__ __align__(1024) uint8_t pj_smem[];
   uint8_t* wt = pj_smem;                                               // [rows][64] bf16, SW128 boxes
   uint8_t* xt = wt + kPjWBytes;                                        // [2][16][kPjXRow] hi, lo
-  float* red = reinterpret_cast<float*>(xt + kPjXBytes);               // [2][16][64]
-  float* slots = red + 2 * kPjM * kPjNC;                               // [KS][16][64] (rank 0)
+  float* red = reinterpret_cast<float*>(xt);                           // [2][16][64] (aliases X after the GEMM)
+  float* slots = reinterpret_cast<float*>(xt + kPjXBytes);             // [KS][16][64] (rank 0)
   uint64_t* bars = reinterpret_cast<uint64_t*>(slots + kPjMaxKS * kPjM * kPjNC);
   float* rscale = reinterpret_cast<float*>(bars + kPjMaxBoxes);        // [16]
   const int KS = p.KS, slab = blockIdx.x / KS, ks = blockIdx.x % KS;
@@ -207,6 +211,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
       mma_m16n8k16_bf16(acc[1], alo, bf[2], bf[3]);
     }
   }
+  __syncthreads();  // every warp is done with the X planes: the partials reuse them
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int col = cg * 16 + j * 8 + 2 * t4;
