@@ -107,9 +107,9 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
     float e = 0.f, o = 0.f;
     if (2 * l + 1 < dr) {
       const double theta = pow(double(rope_base), -2.0 * l / dr);
-      const double ang = fmod(pos * theta, 6.283185307179586476925286766559);
+      const double a = pos * theta, two_pi = 6.283185307179586476925286766559;
       float sn, cs;
-      sincosf(float(ang), &sn, &cs);
+      sincosf(float(a - two_pi * floor(a * (1.0 / two_pi))), &sn, &cs);  // reduced mod 2 pi in fp64
       const float x0 = kr[2 * l], x1 = kr[2 * l + 1];
       e = x0 * cs - x1 * sn;
       o = x0 * sn + x1 * cs;

@@ -2,6 +2,7 @@
 // mlra_proj_down and mlra_proj_query. Validation, the weight's TMA descriptor (cached per
 // weight pointer and shape), the split of K over a cluster, and the launch.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include "host_common.cuh"
 #include "proj_kernel.cuh"
@@ -177,7 +178,7 @@ int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float
                     int nq, int H, int dr, int drp, const int32_t* pos, int pos_delta, float rope_base, float q_scale, float r_scale,
                     void* q_out, void* r_out, void* stream) {
   if (M <= 0) return MLRA_OK;
-  if (K <= 0 || nq <= 0 || nq % 2 != 0 || H <= 0 || dr < 0 || dr % 2 != 0 || drp < dr)
+  if (K <= 0 || nq <= 0 || nq % 2 != 0 || H <= 0 || dr < 0 || dr % 2 != 0 || dr > 64 || drp < dr)
     return fail(MLRA_ERR_SHAPE, "proj_query: bad dims K=%d nq=%d H=%d dr=%d drp=%d", K, nq, H, dr, drp);
   const int N = nq + H * dr;
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return fail(MLRA_ERR_CONFIG, "proj_query: w must be 16-byte aligned");
@@ -202,6 +203,7 @@ int mlra_proj_query(const float* c_q_raw, const float* ssq, float alpha_q, float
   p.pos = pos;
   p.pos_delta = pos_delta;
   p.rope_base = rope_base;
+  for (int l = 0; l < dr / 2; ++l) p.theta[l] = pow(double(rope_base), -2.0 * l / dr);
   p.q_scale = q_scale;
   p.r_scale = r_scale;
   return launch_proj(w, p, static_cast<cudaStream_t>(stream));

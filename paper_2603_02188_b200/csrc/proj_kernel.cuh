@@ -64,6 +64,7 @@ struct ProjParams {
   const int32_t* pos;    // [M] rope positions (+ pos_delta)
   int pos_delta;
   float rope_base, q_scale, r_scale;
+  double theta[32];      // rope frequencies rope_base^(-2l/dr), l < dr/2 (host-computed)
   unsigned long long* trace;  // dev: per-CTA globaltimer stamps [grid][8] (MLRA_DEBUG_PROJ_TRACE), or null
 };
 
@@ -266,10 +267,10 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
       continue;
     }
     const int j = n - p.nq, h = j / p.dr, l = (j % p.dr) / 2;
-    const double theta = pow(double(p.rope_base), -2.0 * l / p.dr);
-    const double ang = fmod(double(p.pos[r] + p.pos_delta) * theta, 6.283185307179586476925286766559);
+    const double a = double(p.pos[r] + p.pos_delta) * p.theta[l];
+    const double two_pi = 6.283185307179586476925286766559;
     float sn, cs;
-    sincosf(float(ang), &sn, &cs);
+    sincosf(float(a - two_pi * floor(a * (1.0 / two_pi))), &sn, &cs);
     const float e = (y0 * cs - y1 * sn) * p.r_scale, o = (y0 * sn + y1 * cs) * p.r_scale;
     reinterpret_cast<__nv_bfloat162*>(p.r_out + (size_t(r) * p.H + h) * p.drp)[l] = __floats2bfloat162_rn(e, o);
   }
