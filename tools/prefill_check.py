@@ -21,11 +21,11 @@ h = torch.randn((n, cfg.d), generator=torch.Generator(device=dev).manual_seed(n)
 outs = []
 import os, threading
 if os.environ.get("PROGRESS"):
-    prog = torch.zeros(8 * 4096, dtype=torch.int32, pin_memory=True)
+    prog = torch.zeros(16 * 4096, dtype=torch.int32, pin_memory=True)
     os.environ["MLRA_DEBUG_PF_PROGRESS"] = str(prog.data_ptr())
     def dump():
         time.sleep(20)
-        a = prog.numpy().reshape(-1, 8)
+        a = prog.numpy().reshape(-1, 16)
         nz = [(i, list(a[i])) for i in range(a.shape[0]) if a[i].any()]
         print("progress after 20 s:", len(nz), "CTAs touched", flush=True)
         for i, r in nz[:60]:
