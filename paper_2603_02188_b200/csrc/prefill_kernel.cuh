@@ -294,18 +294,22 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         mbar_arrive(&s_empty[s]);
         // causal mask on the diagonal tile (and the sequence end): keys [0, kmax] visible
         const int kmax = min(q, p.n - 1) - j * kPfT - hf * 64;
-        float tmax = -INFINITY;
+        // (8 independent max / sum chains: a single 64-long dependent chain cost ~4 cycles an element)
+        float tm[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) tm[i] = -INFINITY;
         if (__all_sync(0xffffffffu, kmax >= 63)) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) tmax = fmaxf(tmax, __uint_as_float(sv[c]));
+          for (int c = 0; c < 64; ++c) tm[c & 7] = fmaxf(tm[c & 7], __uint_as_float(sv[c]));
         } else {
 #pragma unroll
           for (int c = 0; c < 64; ++c) {
             const float x = c <= kmax ? __uint_as_float(sv[c]) : -INFINITY;
             sv[c] = __float_as_uint(x);
-            tmax = fmaxf(tmax, x);
+            tm[c & 7] = fmaxf(tm[c & 7], x);
           }
         }
+        float tmax = fmaxf(fmaxf(fmaxf(tm[0], tm[1]), fmaxf(tm[2], tm[3])), fmaxf(fmaxf(tm[4], tm[5]), fmaxf(tm[6], tm[7])));
         float* xs = xmax + (g & 1) * 2 * kPfT;
         xs[hf * kPfT + r] = tmax;
         named_bar_sync(pair_bar, 64);
@@ -337,7 +341,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const float mu = m;
         // P = 2^(S - m) as bf16 into the P buffer (free once the previous PV completed)
         if (g >= 2) pf_wait(&pv_done[g & 1], ((g >> 1) - 1) & 1, 10);  // this buffer's last PV read it
-        float sum = 0.f;
+        float sm[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i] = 0.f;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           uint32_t w4[4];
@@ -346,12 +352,13 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             const int k0 = u * 8 + 2 * e;
             const float p0 = (mu == -INFINITY) ? 0.f : ex2(__uint_as_float(sv[k0]) - mu);
             const float p1 = (mu == -INFINITY) ? 0.f : ex2(__uint_as_float(sv[k0 + 1]) - mu);
-            sum += p0 + p1;
+            sm[(2 * e) & 7] += p0;
+            sm[(2 * e + 1) & 7] += p1;
             w4[e] = pack_bf16(p0, p1);
           }
           *reinterpret_cast<uint4*>(prow + s * L::kPBytes + ((u ^ (r & 7)) * 16)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        l += sum;
+        l += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[s]);
