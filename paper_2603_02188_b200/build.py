@@ -19,6 +19,9 @@ HEADERS = ["ptx.cuh", "decode_kernel.cuh", "aux_kernels.cuh", "outproj_kernel.cu
            "fused_step.cuh", "host_common.cuh", "peer_common.cuh", "proj_kernel.cuh", "prefill_kernel.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+# dev builds only (e.g. MLRA_NVCC_DEFS=MLRA_PF_WAIT_STATS for tools/prefill_waits.py); part of the
+# source hash, so a dev library is never mistaken for the product one
+FLAGS += [f"-D{d}" for d in os.environ.get("MLRA_NVCC_DEFS", "").split(",") if d]
 STAMP = LIB + ".srchash"  # source hash of the shipped library (travels with it)
 
 

@@ -1069,6 +1069,13 @@ extern "C" int mlra_prefill_attention(const void* q_abs, const void* q_rope, con
     p.dbg_s = reinterpret_cast<float*>(strtoull(e, nullptr, 0));
     p.dbg_cta = getenv("MLRA_DEBUG_PF_CTA") ? atoi(getenv("MLRA_DEBUG_PF_CTA")) : 0;
   }
+#ifdef MLRA_PF_WAIT_STATS
+  if (const char* e = getenv("MLRA_DEBUG_PF_WAITS")) {  // dev build: per-barrier wait cycles of CTA 0
+    unsigned long long* ptr = reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0));
+    cudaMemcpyToSymbolAsync(mlra::g_pf_wait_acc, &ptr, sizeof(ptr), 0, cudaMemcpyHostToDevice,
+                            static_cast<cudaStream_t>(stream));
+  }
+#endif
   if (const char* e = getenv("MLRA_DEBUG_PF_PROGRESS")) p.progress = reinterpret_cast<volatile int*>(strtoull(e, nullptr, 0));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (DLAT == 128) return launch_prefill<128, 128>(pm, q_abs, q_rope, w_uv, p, DRq, st);

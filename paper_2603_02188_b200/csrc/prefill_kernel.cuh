@@ -83,7 +83,22 @@ struct PrefillLayout {
 
 // Bounded mbarrier wait: a broken pipeline invariant traps (with the barrier id and phase
 // printed) instead of hanging the GPU.
+#ifdef MLRA_PF_WAIT_STATS
+// dev build only (-DMLRA_PF_WAIT_STATS): per-barrier-id wait cycles of CTA 0 summed over the
+// waiting threads (tools/prefill_waits.py); the product build has no hook in the wait path
+__device__ unsigned long long* g_pf_wait_acc = nullptr;
+#endif
+
 __device__ __forceinline__ void pf_wait(uint64_t* bar, uint32_t parity, int id) {
+#ifdef MLRA_PF_WAIT_STATS
+  if (g_pf_wait_acc != nullptr && blockIdx.x == 0) {
+    const long long ts = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+    }
+    atomicAdd(g_pf_wait_acc + id, (unsigned long long)(clock64() - ts));
+    return;
+  }
+#endif
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {

@@ -55,3 +55,7 @@ for force in (True, False):
 errs = [ak.max_rel_err(outs[0][t], outs[1][t]) for t in range(n)]
 print(variant, n, "max_rel_err K6 vs pseudo", max(errs), "at", int(np.argmax(errs)), flush=True)
 
+for t0 in range(0, n, 128):
+    e = max(errs[t0:t0 + 128])
+    hs = [max(ak.max_rel_err(outs[0][t, hh], outs[1][t, hh]) for t in range(t0, min(n, t0 + 128))) for hh in range(outs[0].shape[1])]
+    print(f"  tile {t0 // 128}: {e:.3e} per head {[f'{x:.1e}' for x in hs[:8]]}", flush=True)

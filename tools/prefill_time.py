@@ -30,8 +30,8 @@ for n in [int(a) for a in sys.argv[1:]] or [1024, 4096, 16384]:
     kp = st.kproj
     _, _, qn, q_r = kp.project_gemm(h, 0, drq=64)
     w_uk, w_uv = st.lw.packed(cache.layout, dev, st.own)
-    sc = ops.score_scale(cfg.tau)
-    q_abs = torch.bmm(qn.transpose(0, 1), w_uk).view(cfg.h, n, 4, 128)
+    sc = ops.score_scale(cfg.tau)  # tau*log2e, as prefill_into applies it (realistic logit range)
+    q_abs = (torch.bmm(qn.transpose(0, 1), w_uk).float() * sc).to(torch.bfloat16).view(cfg.h, n, 4, 128)
     q_rs = (q_r.float() * sc).to(torch.bfloat16)
     pc = cache.paged
     t_k6 = ev_time(lambda: ops.prefill_attention(q_abs, q_rs, w_uv, pc.pool, pc.block_table, pc.page_size, 4, 128, 64, 0.5))
