@@ -298,29 +298,41 @@ decode_plan_kernel(const int32_t* __restrict__ seqlens, int B, int T, int ctas, 
 // ----------------------------------------------------------------------------- K3a
 // Flash-decoding merge of the K2 split partials: for every (sequence, branch, head) row,
 //   Z = sum_k w_k O_k with w_k = 2^(lse_k - max) / sum_j 2^(lse_j - max).
-// CTA = (row, 128 latent columns), 512 threads = 128 columns x 4 split quarters: warp 0 forms
-// the split weights once (lane k < nsplit, shuffled max / sum) into smem; thread (q, c) merges
-// column c over the splits k = q, q+4, ... (8 loads in flight at a time) and the 4 quarter sums
-// are added in ascending order through smem (deterministic). Many splits (batch-1 decode runs
-// up to 148) cost ceil(nsplit / 32) round trips instead of ceil(nsplit / 8). Output
-// [B, H, NB*DLAT] (the K3b input) or, with zout_bnh, [B, NB, H, DLAT] * alpha (the latent mixture
-// itself: the paper's decode scope).
+// CTA = (row, CW latent columns), CW x Q threads: warp 0 forms the split weights once (lane k <
+// nsplit, shuffled max / sum) into smem; thread (q, c) merges column c over the splits k = q,
+// q+Q, ... and the Q partial sums are added in ascending q through smem (deterministic).
+// Q = 4 with 128 columns (8 loads in flight per round); Q = 16 with 32 columns when the rows are
+// few and the splits many (batch-1 decode runs up to 148): a thread's <= 10 split values are all
+// loaded at once, issued before the weights are known, so the merge costs one round trip.
+// Output [B, H, NB*DLAT] (the K3b input) or, with zout_bnh, [B, NB, H, DLAT] * alpha (the latent
+// mixture itself: the paper's decode scope).
 constexpr int kMergeMaxSplits = 160;  // 5 per lane
-constexpr int kMergeQ = 4;
-__global__ void __launch_bounds__(128 * kMergeQ)
+constexpr int kMergeQ = 4;            // split groups with 128 columns per CTA
+constexpr int kMergeQWide = 16;       // split groups with 32 columns per CTA
+template <int Q>
+__global__ void __launch_bounds__(512)
 merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_part, float* __restrict__ z, int B,
                     int NB, int H, int DLAT, int nsplit, float alpha, int zout_bnh, int* __restrict__ status,
                     const int32_t* __restrict__ seq_splits) {
-  // blockDim.x = CW * kMergeQ: CW latent columns per CTA (128, or 32 when the rows are few and
-  // the splits many -- batch-1 decode -- so the grid still covers the SMs)
   __shared__ float wsh[kMergeMaxSplits];
-  __shared__ float part[kMergeQ][128];
-  const int CW = blockDim.x / kMergeQ;
+  __shared__ float part[512];  // [Q][CW]
+  const int CW = blockDim.x / Q;
   const int row = blockIdx.x, cl = threadIdx.x % CW, qk = threadIdx.x / CW, c = blockIdx.y * CW + cl;
   const int lane = threadIdx.x % 32;
   const int h = row % H, b = (row / H) % NB, s = row / (H * NB);
   const int ns = seq_splits != nullptr ? min(seq_splits[s], nsplit) : nsplit;  // splits of this sequence
+  const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
+  const size_t sstride = size_t(NB) * H * DLAT;
   griddep_wait();
+  constexpr int kPre = Q == kMergeQWide ? (kMergeMaxSplits + Q - 1) / Q : 1;
+  float pre[kPre];
+  if (Q == kMergeQWide) {  // every split value of this thread in flight before the weights
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      const int k = qk + j * Q;
+      pre[j] = (c < DLAT && k < ns) ? __ldcg(o + size_t(k) * sstride) : 0.f;
+    }
+  }
   if (threadIdx.x < 32) {
     const float* l = lse_part + (size_t(s) * nsplit * NB + b) * H + h;  // split stride NB*H
     float lk[kMergeMaxSplits / 32];
@@ -356,29 +368,33 @@ merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ 
   }
   __syncthreads();
   float acc = 0.f;
-  if (c < DLAT) {
-    const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
-    const size_t sstride = size_t(NB) * H * DLAT;
-    for (int k0 = qk; k0 < ns; k0 += 8 * kMergeQ) {
+  if (Q == kMergeQWide) {
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      const int k = qk + j * Q;
+      if (k < ns) acc = fmaf(wsh[k], pre[j], acc);
+    }
+  } else if (c < DLAT) {
+    for (int k0 = qk; k0 < ns; k0 += 8 * Q) {
       float v[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int k = k0 + j * kMergeQ;
+        const int k = k0 + j * Q;
         v[j] = k < ns ? __ldcg(o + size_t(k) * sstride) : 0.f;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int k = k0 + j * kMergeQ;
+        const int k = k0 + j * Q;
         if (k < ns) acc = fmaf(wsh[k], v[j], acc);
       }
     }
   }
-  part[qk][cl] = acc;
+  part[qk * CW + cl] = acc;
   __syncthreads();
   if (qk != 0 || c >= DLAT) return;
-  float t = part[0][cl];
+  float t = part[cl];
 #pragma unroll
-  for (int q = 1; q < kMergeQ; ++q) t += part[q][cl];
+  for (int q = 1; q < Q; ++q) t += part[q * CW + cl];
   float* dst = zout_bnh ? z + ((size_t(s) * NB + b) * H + h) * DLAT : z + (size_t(s) * H + h) * (NB * DLAT) + b * DLAT;
   dst[c] = t * (zout_bnh ? alpha : 1.f);
 }

@@ -521,14 +521,19 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     if (int rc = cuda_check("combine launch")) return rc;
     return fused ? MLRA_OK : tp_pending;
   }
-  const int mcw = (long(rows) * ((DLAT + 127) / 128) < 148 && nsplit > 16) ? 32 : 128;  // merge columns per CTA
+  // merge: 32 columns x 16 split groups per CTA when the rows are few and the splits many
+  // (batch-1 decode), else 128 columns x 4; PDL: the CTAs start while K2 drains
+  const bool wide = long(rows) * ((DLAT + 127) / 128) < 148 && nsplit > 16;
+  const int mcw = wide ? 32 : 128;
+  auto merge = wide ? mlra::merge_splits_kernel<mlra::kMergeQWide> : mlra::merge_splits_kernel<mlra::kMergeQ>;
+  const dim3 mgrid(rows, (DLAT + mcw - 1) / mcw), mblock(512);
   if (upproj == 0) {
-    launch_ex(mlra::merge_splits_kernel, dim3(rows, (DLAT + mcw - 1) / mcw), dim3(mcw * mlra::kMergeQ), 0, st, false, 
-        o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status, seq_splits);
+    launch_ex(merge, mgrid, mblock, 0, st, pdl, o_part, lse_part, out, B, NB, H, DLAT, nsplit, alpha, 1, status,
+              seq_splits);
     return cuda_check("merge launch");
   }
-  launch_ex(mlra::merge_splits_kernel, dim3(rows, (DLAT + mcw - 1) / mcw), dim3(mcw * mlra::kMergeQ), 0, st, false, 
-      o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status, seq_splits);
+  launch_ex(merge, mgrid, mblock, 0, st, pdl, o_part, lse_part, zbuf, B, NB, H, DLAT, nsplit, 1.f, 0, status,
+            seq_splits);
   const int kparts = (upproj == 2) ? NB : 1;
   constexpr int NT = 32;
   const int kp = NB * DLAT / kparts;
@@ -556,8 +561,9 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
   if (upproj < 0 || upproj > 2) return fail(MLRA_ERR_CONFIG, "combine: upproj mode %d", upproj);
   if (upproj && (DH % 8 != 0)) return fail(MLRA_ERR_SHAPE, "combine: DH=%d not a multiple of 8", DH);
   if (upproj && scratch == nullptr) return fail(MLRA_ERR_CONFIG, "combine: up-projection needs a scratch buffer");
+  // PDL: the merge's prologue overlaps K2's drain when K2 is the previous launch on the stream
   return combine_impl(o_part, lse_part, w_uv, out, scratch, B, H, NB, DLAT, DH, nsplit, alpha, upproj,
-                      static_cast<cudaStream_t>(stream), false, nullptr, status);
+                      static_cast<cudaStream_t>(stream), getenv("MLRA_NO_PDL") == nullptr, nullptr, status);
 }
 
 static int decode_step_impl(const void* q_nope, const void* q_rope, const void* w_uk, const void* w_uv,

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-( for sp in 0 1 2; do echo "spin=$sp"; MLRA_DEBUG_PF_SPIN=$sp timeout 300 python tools/prefill_time.py 1024 4096 16384; done ) > gpurun_out/prefill_time.txt 2>&1
-MLRA_DEBUG_PF_SPIN=1 timeout 120 python tools/prefill_check.py mlra4 1000 > gpurun_out/prefill_dbg.txt 2>&1
+timeout 900 python -m pytest tests/test_decode_gpu.py tests/test_api_gpu.py tests/test_ragged_gpu.py tests/test_gqa_gpu.py -q -x > gpurun_out/pytest_merge.txt 2>&1
+echo "exit $?" >> gpurun_out/pytest_merge.txt
+timeout 900 python tools/sweep.py 4096,131072 1,16 tp4_rank,h64_tp4_rank,h64_mla_tp4_rank gpurun_out/sweep_merge.md > gpurun_out/sweep_merge.log 2>&1
