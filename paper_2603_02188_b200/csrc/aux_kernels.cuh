@@ -151,6 +151,7 @@ head_gemm_kernel(const Tx* __restrict__ X, const __nv_bfloat16* __restrict__ W, 
     if (n0 + c8 * 8 < N) v = *reinterpret_cast<const uint4*>(W + (size_t(h) * K + k_begin + r) * N + n0 + c8 * 8);
     *reinterpret_cast<uint4*>(ws + size_t(r) * NT + c8 * 8) = v;
   }
+  griddep_wait();  // X is the previous kernel's output (PDL launch: the weights above overlap it)
   for (int i = threadIdx.x; i < kHG_S * kp; i += kHG_THREADS) {
     const int ss = i / kp, kk = i % kp;
     const int sg = sblk * kHG_S + ss;
@@ -323,6 +324,7 @@ merge_splits_kernel(const float* __restrict__ o_part, const float* __restrict__ 
   const int ns = seq_splits != nullptr ? min(seq_splits[s], nsplit) : nsplit;  // splits of this sequence
   const float* o = o_part + ((size_t(s) * nsplit * NB + b) * H + h) * DLAT + c;  // split stride NB*H*DLAT
   const size_t sstride = size_t(NB) * H * DLAT;
+  griddep_launch_dependents();  // the up-projection (K3b) may stage its weights meanwhile
   griddep_wait();
   constexpr int kPre = Q == kMergeQWide ? (kMergeMaxSplits + Q - 1) / Q : 1;
   float pre[kPre];

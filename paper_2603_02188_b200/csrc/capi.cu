@@ -440,7 +440,22 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
   const int rt_c4 = 2 * ((nsplit + 11) / 12);
   const int rt_sk = 2 * NB * (((nsplit + KP - 1) / KP + 11) / 12);
   // (ragged plans: the per-sequence split counts vary, most sequences have few -- per-branch CTAs)
-  if (seq_splits == nullptr && upproj == 1 && 3 * rt_sk < 2 * rt_c4 && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
+  // dev: MLRA_K3_FORCE = 1 split-K cluster, 2 per-branch CTAs, 3 merge + head GEMM
+  const int force = getenv("MLRA_K3_FORCE") ? atoi(getenv("MLRA_K3_FORCE")) : 0;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // Split-K clusters while their grid fits one wave; beyond that (many heads at batch 1: 64 x 8
+  // CTAs) the one-round-trip merge plus the head GEMM measured faster (64 heads, B = 1, 128K:
+  // K3 13.4 -> 8.4 us)
+  const long sk_ctas = long((B + 3) / 4) * H * KP;
+  const bool many_splits = 3 * rt_sk < 2 * rt_c4;
+  const bool auto_sk = force == 0 ? many_splits && sk_ctas <= sms : force == 1;
+  const bool merge_gemm = force == 3 || (force == 0 && many_splits && sk_ctas > sms);
+  if (seq_splits == nullptr && upproj == 1 && auto_sk && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
       sksmem <= size_t(kSmemBudget) && (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
     auto kern = KP == 8 ? mlra::combine_splitk_kernel<8> : mlra::combine_splitk_kernel<4>;
     static unsigned attr4 = 0, attr8 = 0;
@@ -467,19 +482,13 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
   }
   // 2 sequences per CTA (one merge item per thread) while the grid stays within one wave
   // (4 CTAs per SM), else 4
-  int sms = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const bool seq2 = long((B + 1) / 2) * H * NB <= 4L * sms && getenv("MLRA_K3_SEQ4") == nullptr;
   // many sequences (prefill's pseudo-sequences): 8 per CTA halves the W^UV re-reads
   const bool seq8 = !seq2 && B >= 256;
   const size_t c4smem = seq2   ? mlra::combine4_smem<2>(DLAT, DH, nsplit)
                         : seq8 ? mlra::combine4_smem<8>(DLAT, DH, nsplit)
                                : mlra::combine4_smem<4>(DLAT, DH, nsplit);
-  if (upproj != 0 && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
+  if (upproj != 0 && !merge_gemm && c4smem <= size_t(kSmemBudget) && (size_t(DLAT) * DH * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
     // CTA = (2 or 4 sequences, head, branch); with a summed output the NB branch CTAs of a
     // (sequence group, head) form a cluster and add their results through DSMEM.
@@ -548,7 +557,8 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
     if (dev < 32) attr_done |= 1u << dev;
   }
   dim3 grid((DH + NT - 1) / NT, H, ((B + mlra::kHG_S - 1) / mlra::kHG_S) * kparts);
-  launch_ex(kern, dim3(grid), dim3(mlra::kHG_THREADS), smem, st, false, zbuf, static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
+  launch_ex(kern, dim3(grid), dim3(mlra::kHG_THREADS), smem, st, getenv("MLRA_NO_PDL") == nullptr, zbuf,
+            static_cast<const __nv_bfloat16*>(w_uv), out, B, H, NB * DLAT,
                                               DH, kparts, alpha, 0, 0, nullptr, nullptr, 0);
   if (int rc = cuda_check("up-projection launch")) return rc;
   return tp_pending;

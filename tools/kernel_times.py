@@ -24,8 +24,11 @@ def gtime(fn, iters=50):
 dev = torch.device("cuda", 0)
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 CTX = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+from paper_2603_02188_b200.config import table_context
+tc = table_context()
 cases = [("mlra4 tp1", trained_config("mlra4"), None), ("mlra4 tp4 rank", trained_config("mlra4"), shard_ownership(trained_config("mlra4"), 4, 0)),
-         ("mla tp4 rank", trained_config("mla"), shard_ownership(trained_config("mla"), 4, 0))]
+         ("mla tp4 rank", trained_config("mla"), shard_ownership(trained_config("mla"), 4, 0)),
+         ("h64 mlra4 tp4 rank", tc["mlra4"], shard_ownership(tc["mlra4"], 4, 0))]
 for name, cfg, own in cases:
     eng, qn, qr = bench.make_engine(cfg, own, B, CTX, 1, dev)
     c = eng.cache
@@ -37,15 +40,5 @@ for name, cfg, own in cases:
     t2 = gtime(lambda: ops.decode_partials(q_abs, q_rs, c.pool, c.block_table, c.seqlens, c.page_size, eng.nb, eng.sub, eng.dls, eng.nsplit, out=parts))
     t3 = gtime(lambda: ops.combine(*parts, eng.w_uv, eng.alpha, out=out, scratch=scratch))
     tstep = gtime(lambda: eng.decode_attention(qn, qr))
-    import os
-    os.environ["MLRA_NO_FUSE"] = "1"
-    tstep3 = gtime(lambda: eng.decode_attention(qn, qr))
-    del os.environ["MLRA_NO_FUSE"]
-    parts = {}
-    for part in ("absorb", "combine"):
-        os.environ["MLRA_FUSE_PARTS"] = part
-        parts[part] = gtime(lambda: eng.decode_attention(qn, qr))
-        del os.environ["MLRA_FUSE_PARTS"]
-    print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  fused step {tstep:.1f} us  "
-          f"3-kernel step {tstep3:.1f} us  fused absorb only (+K3) {parts['absorb']:.1f}  fused combine only (K1+) "
-          f"{parts['combine']:.1f}  (graph replay, one cache: L2-warm)", flush=True)
+    print(f"B={B} n={CTX} nsplit={eng.nsplit} {name}: K1 {t1:.1f} us  K2 {t2:.1f} us  K3 {t3:.1f} us  "
+          f"step {tstep:.1f} us  (graph replay of 10 launches, one cache: L2-warm)", flush=True)
