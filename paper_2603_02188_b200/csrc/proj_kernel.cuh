@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
   const int cg = warp & 3, kh = warp >> 2, q = lane >> 3, g = lane >> 2, t4 = lane & 3;
   const int half = (nbox + 1) / 2;
   const int b_lo = kh == 0 ? 0 : half, b_hi = kh == 0 ? half : nbox;
-  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  // hi and lo planes into separate accumulators (summed at the end): independent mma.sync chains
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, acl[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
   for (int b = b_lo; b < b_hi; ++b) {
     mbar_wait(&bars[b], 0);
     if (b == 0) pj_stamp(p, 3);
@@ -207,11 +208,15 @@ __global__ void __launch_bounds__(kPjThreads, 1) proj_gemm_kernel(const __grid_c
       const int kr = kk * 16 + (q & 1) * 8 + (lane & 7);  // row within the box
       ldmatrix_x4_trans(bf, wb + kr * 128 + (((cg * 2 + (q >> 1)) ^ (kr & 7)) * 16));
       mma_m16n8k16_bf16(acc[0], ahi, bf[0], bf[1]);
-      mma_m16n8k16_bf16(acc[0], alo, bf[0], bf[1]);
+      mma_m16n8k16_bf16(acl[0], alo, bf[0], bf[1]);
       mma_m16n8k16_bf16(acc[1], ahi, bf[2], bf[3]);
-      mma_m16n8k16_bf16(acc[1], alo, bf[2], bf[3]);
+      mma_m16n8k16_bf16(acl[1], alo, bf[2], bf[3]);
     }
   }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[j][e] += acl[j][e];
   __syncthreads();  // every warp is done with the X planes: the partials reuse them
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
