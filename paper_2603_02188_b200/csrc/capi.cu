@@ -453,10 +453,12 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
   // K3 13.4 -> 8.4 us)
   const long sk_ctas = long((B + 3) / 4) * H * KP;
   const bool many_splits = 3 * rt_sk < 2 * rt_c4;
+  const bool sk_ok = seq_splits == nullptr && upproj == 1 && NB * DLAT <= 512 && DH % (8 * KP) == 0 &&
+                     256 % (DH / KP) == 0 && sksmem <= size_t(kSmemBudget) &&
+                     (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0;
   const bool auto_sk = force == 0 ? many_splits && sk_ctas <= sms : force == 1;
-  const bool merge_gemm = force == 3 || (force == 0 && many_splits && sk_ctas > sms);
-  if (seq_splits == nullptr && upproj == 1 && auto_sk && NB * DLAT <= 512 && DH % (8 * KP) == 0 && 256 % (DH / KP) == 0 &&
-      sksmem <= size_t(kSmemBudget) && (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0) {
+  const bool merge_gemm = force == 3 || (force == 0 && sk_ok && many_splits && sk_ctas > sms);
+  if (sk_ok && auto_sk) {
     auto kern = KP == 8 ? mlra::combine_splitk_kernel<8> : mlra::combine_splitk_kernel<4>;
     static unsigned attr4 = 0, attr8 = 0;
     if (int rc = set_smem_once(kern, KP == 8 ? attr8 : attr4, kSmemBudget)) return rc;
