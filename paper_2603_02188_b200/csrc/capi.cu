@@ -266,7 +266,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
                        bool pdl = false, const mlra::FuseArgs* fz = nullptr, int fuse_mode = 1,
-                       const int32_t* plan = nullptr, int plan_ctas = 0);
+                       const int32_t* plan = nullptr, int plan_ctas = 0, int late = -1);
 
 int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                          const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB,
@@ -278,7 +278,8 @@ int mlra_decode_partials(const void* q_abs, const void* q_rope, const void* pool
 static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, const int32_t* block_table,
                        const int32_t* seqlens, float* o_part, float* lse_part, int B, int H, int NB, int SUB, int DLS,
                        int DR, int page_size, int max_pages, int num_pages, int nsplit, void* stream,
-                       bool pdl, const mlra::FuseArgs* fz, int fuse_mode, const int32_t* plan, int plan_ctas) {
+                       bool pdl, const mlra::FuseArgs* fz, int fuse_mode, const int32_t* plan, int plan_ctas,
+                       int late) {
   if (B <= 0) return MLRA_OK;
   if (NB < 1 || NB > 4) return fail(MLRA_ERR_CONFIG, "decode: NB=%d branches per device not in [1,4]", NB);
   if (SUB < 1 || NB * SUB > 8) return fail(MLRA_ERR_CONFIG, "decode: SUB=%d sub-blocks not supported", SUB);
@@ -311,7 +312,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.pdl = pdl ? 1 : 0;
   p.plan = plan;
   p.plan_ctas = plan_ctas;
-  p.late_trigger = getenv("MLRA_K3_PDL") != nullptr;
+  p.late_trigger = late >= 0 ? late : getenv("MLRA_K3_PDL") != nullptr;
   if (fz != nullptr) {
     p.fused = fuse_mode;
     p.fz = *fz;
@@ -425,12 +426,10 @@ static int combine_impl(const float* o_part, const float* lse_part, const void* 
 
 // Returns MLRA_OK when the output is complete (TP sum fused in K3 when requested), 1 when a
 // requested TP sum still has to run (the K3 variant has no fused sum), < 0 on error.
-static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
-                           int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
-                           bool pdl, const mlra::TpSum* tp, int32_t* status, const int32_t* seq_splits) {
-  const int tp_pending = (tp != nullptr && tp->world > 1 && upproj == 1) ? 1 : 0;
-  const int rows = B * NB * H;
-  // summed output: split-K merge over a cluster of KP CTAs (KP = 8 once the splits are many)
+// K3 variant: 1 split-K clusters, 3 the split merge + head GEMM, 0 the per-branch CTAs (or, when
+// their smem does not fit, the merge + head GEMM as a fallback)
+static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int upproj, const void* w_uv,
+                      const int32_t* seq_splits) {
   const int KP = nsplit > 24 ? 8 : 4;
   const size_t sksmem = KP == 8 ? mlra::combine_splitk_smem<8>(NB, DLAT, DH) : mlra::combine_splitk_smem<4>(NB, DLAT, DH);
   // Cost model in dependent L2 round trips per thread (12 split loads in flight per item):
@@ -439,26 +438,52 @@ static int combine_variant(const float* o_part, const float* lse_part, const voi
   // 1.5x fewer round trips (small batches: many splits per sequence).
   const int rt_c4 = 2 * ((nsplit + 11) / 12);
   const int rt_sk = 2 * NB * (((nsplit + KP - 1) / KP + 11) / 12);
-  // (ragged plans: the per-sequence split counts vary, most sequences have few -- per-branch CTAs)
   // dev: MLRA_K3_FORCE = 1 split-K cluster, 2 per-branch CTAs, 3 merge + head GEMM
   const int force = getenv("MLRA_K3_FORCE") ? atoi(getenv("MLRA_K3_FORCE")) : 0;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Split-K clusters while their grid fits one wave; beyond that (many heads at batch 1: 64 x 8
+  // CTAs) the one-round-trip merge plus the head GEMM measured faster (64 heads, B = 1, 128K:
+  // K3 13.4 -> 8.4 us). Ragged plans (per-sequence split counts, most sequences have few) take
+  // the per-branch CTAs.
+  const long sk_ctas = long((B + 3) / 4) * H * KP;
+  const bool many_splits = 3 * rt_sk < 2 * rt_c4;
+  const bool sk_ok = seq_splits == nullptr && upproj == 1 && NB * DLAT <= 512 && DH % (8 * KP) == 0 &&
+                     256 % (DH / KP) == 0 && sksmem <= size_t(kSmemBudget) &&
+                     (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0;
+  if (force == 1) return sk_ok ? 1 : 0;
+  if (force == 3) return 3;
+  if (force == 2) return 0;
+  if (sk_ok && many_splits) return sk_ctas <= sms ? 1 : 3;
+  return 0;
+}
+
+// K3 released at K2's epilogue (programmatic dependent): only for the merge + head GEMM over
+// many heads (64 heads at batch 1: step 29.4 -> 27.6 us; 24 heads measured 0.4 us slower)
+static bool k3_late(int B, int H, int NB, int DLAT, int DH, int nsplit, const void* w_uv) {
+  if (getenv("MLRA_K3_PDL") != nullptr) return true;
+  return k3_variant(B, H, NB, DLAT, DH, nsplit, 1, w_uv, nullptr) == 3 &&
+         long((B + 3) / 4) * H * (nsplit > 24 ? 8 : 4) > 2L * mlra_num_sms();
+}
+
+static int combine_variant(const float* o_part, const float* lse_part, const void* w_uv, float* out, float* zbuf,
+                           int B, int H, int NB, int DLAT, int DH, int nsplit, float alpha, int upproj, cudaStream_t st,
+                           bool pdl, const mlra::TpSum* tp, int32_t* status, const int32_t* seq_splits) {
+  const int tp_pending = (tp != nullptr && tp->world > 1 && upproj == 1) ? 1 : 0;
+  const int rows = B * NB * H;
+  // summed output: split-K merge over a cluster of KP CTAs (KP = 8 once the splits are many)
+  const int KP = nsplit > 24 ? 8 : 4;
+  const size_t sksmem = KP == 8 ? mlra::combine_splitk_smem<8>(NB, DLAT, DH) : mlra::combine_splitk_smem<4>(NB, DLAT, DH);
+  const int variant = k3_variant(B, H, NB, DLAT, DH, nsplit, upproj, w_uv, seq_splits);
+  const bool merge_gemm = variant == 3;
   int sms = 148;
   {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // Split-K clusters while their grid fits one wave; beyond that (many heads at batch 1: 64 x 8
-  // CTAs) the one-round-trip merge plus the head GEMM measured faster (64 heads, B = 1, 128K:
-  // K3 13.4 -> 8.4 us)
-  const long sk_ctas = long((B + 3) / 4) * H * KP;
-  const bool many_splits = 3 * rt_sk < 2 * rt_c4;
-  const bool sk_ok = seq_splits == nullptr && upproj == 1 && NB * DLAT <= 512 && DH % (8 * KP) == 0 &&
-                     256 % (DH / KP) == 0 && sksmem <= size_t(kSmemBudget) &&
-                     (reinterpret_cast<uintptr_t>(w_uv) & 15) == 0;
-  const bool auto_sk = force == 0 ? many_splits && sk_ctas <= sms : force == 1;
-  const bool merge_gemm = force == 3 || (force == 0 && sk_ok && many_splits && sk_ctas > sms);
-  if (sk_ok && auto_sk) {
+  if (variant == 1) {
     auto kern = KP == 8 ? mlra::combine_splitk_kernel<8> : mlra::combine_splitk_kernel<4>;
     static unsigned attr4 = 0, attr8 = 0;
     if (int rc = set_smem_once(kern, KP == 8 ? attr8 : attr4, kSmemBudget)) return rc;
@@ -629,10 +654,12 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
   if (w_uk == nullptr) {
     // Pre-absorbed queries (mlra_proj_query with W^UQ.W^UK_b pre-multiplied wrote q~ and the
     // scaled rotary query): K2 as a programmatic dependent of the projection, then K3.
+    const bool late = k3_late(B, H, NB, DLAT, DH, nsplit, w_uv);
     int rc = decode_impl(q_nope, q_rope, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR,
-                         page_size, max_pages, num_pages, nsplit, stream, getenv("MLRA_NO_PDL") == nullptr);
+                         page_size, max_pages, num_pages, nsplit, stream, getenv("MLRA_NO_PDL") == nullptr, nullptr, 1,
+                         nullptr, 0, late ? 1 : 0);
     if (rc) return rc;
-    return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, false, tp, status);
+    return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, late, tp, status);
   }
   // One launch per step when the whole grid is co-resident (fused_step.cuh): K1 in K2's prologue,
   // K3 (+ the TP sum) in its epilogue. Otherwise (or with MLRA_NO_FUSE) the three kernels below.
@@ -731,11 +758,11 @@ static int decode_step_impl(const void* q_nope, const void* q_rope, const void* 
   const bool pdl = getenv("MLRA_NO_PDL") == nullptr;
   int rc = absorb_impl(q_nope, q_rope, w_uk, q_abs, q_rope_s, B, H, DH, NB, DLAT, DR, score_scale, stream);
   if (rc) return rc;
+  const bool late = k3_late(B, H, NB, DLAT, DH, nsplit, w_uv);
   rc = decode_impl(q_abs, q_rope_s, pool, block_table, seqlens, o_part, lse_part, B, H, NB, SUB, DLS, DR, page_size,
-                   max_pages, num_pages, nsplit, stream, pdl);
+                   max_pages, num_pages, nsplit, stream, pdl, nullptr, 1, nullptr, 0, late ? 1 : 0);
   if (rc) return rc;
-  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st,
-                      getenv("MLRA_K3_PDL") != nullptr, tp, status);
+  return combine_impl(o_part, lse_part, w_uv, out, zbuf, B, H, NB, DLAT, DH, nsplit, alpha, 1, st, late, tp, status);
 }
 
 int mlra_gqa_default_splits(int B, int G, int max_seqlen) {

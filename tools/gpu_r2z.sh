@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python tools/sweep.py 4096,32768,131072 1,16,64 tp4_rank,mla_tp4_rank gpurun_out/r2_sweep_24h.md > gpurun_out/sweep24.log 2>&1
-timeout 1500 python tools/sweep.py 131072,524288,1048576,2097152 1 h64_tp4_rank,h64_mla_tp4_rank gpurun_out/r2_sweep_h64_b1_long.md > gpurun_out/sweep64.log 2>&1
+timeout 900 python -m pytest tests/test_decode_gpu.py tests/test_api_gpu.py tests/test_ragged_gpu.py tests/test_bench_configs_gpu.py tests/test_layer_gpu.py -q -x > gpurun_out/pytest_merge.txt 2>&1
+echo "exit $?" >> gpurun_out/pytest_merge.txt
+( for lay in tp4 h64; do timeout 300 python tools/step_env.py $lay 1 131072; timeout 300 python tools/step_env.py $lay 1 4096; timeout 300 python tools/step_env.py $lay 16 32768; done ) > gpurun_out/step_env.txt 2>&1
