@@ -1,4 +1,9 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_decode_gpu.py tests/test_api_gpu.py tests/test_ragged_gpu.py tests/test_bench_configs_gpu.py tests/test_layer_gpu.py -q -x > gpurun_out/pytest_merge.txt 2>&1
-echo "exit $?" >> gpurun_out/pytest_merge.txt
-( for lay in tp4 h64; do timeout 300 python tools/step_env.py $lay 1 131072; timeout 300 python tools/step_env.py $lay 1 4096; timeout 300 python tools/step_env.py $lay 16 32768; done ) > gpurun_out/step_env.txt 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1
+echo "exit $?" >> gpurun_out/pytest_gpu.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --quick --no-cpu > gpurun_out/launches_bench.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/b1_launches.csv python tools/b1_launches.py > gpurun_out/b1_launches.log 2>&1
