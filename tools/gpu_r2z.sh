@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1
-echo "exit $?" >> gpurun_out/pytest_gpu.txt
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --quick --no-cpu > gpurun_out/launches_bench.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/b1_launches.csv python tools/b1_launches.py > gpurun_out/b1_launches.log 2>&1
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/k3_sanity.py > gpurun_out/sanitizer_k3_$tool.txt 2>&1
+  echo "exit $?" >> gpurun_out/sanitizer_k3_$tool.txt
+done
