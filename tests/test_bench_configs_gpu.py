@@ -58,12 +58,12 @@ def _streams(eng, s):
     return {name: eng.cache.stream(s, name).double().cpu().numpy() for name in list(eng.layout.units) + ["rope"]}
 
 
-def _check_latent(variant, phi, rank, batch, ctx, seqs=None, graph=True):
+def _check_latent(variant, phi, rank, batch, ctx, seqs=None, graph=True, cfg=None):
     from paper_2603_02188_b200.config import trained_config
     from paper_2603_02188_b200.tp import shard_ownership
 
     bench = _bench()
-    cfg = trained_config(variant)
+    cfg = cfg if cfg is not None else trained_config(variant)
     own = shard_ownership(cfg, phi, rank) if phi > 1 else None
     dev = torch.device("cuda", 0)
     eng, qn, qr = bench.make_engine(cfg, own, batch, ctx, 1000, dev)
@@ -95,7 +95,7 @@ def _check_latent(variant, phi, rank, batch, ctx, seqs=None, graph=True):
             want[head] += vec
         want = alpha * want[heads]
         errs.append(ak.max_rel_err(want, got[s]))
-    case = f"{variant}_tp{phi}_rank{rank}_b{batch}_n{ctx}"
+    case = f"{variant}{'' if cfg.h == 24 else f'_h{cfg.h}'}_tp{phi}_rank{rank}_b{batch}_n{ctx}"
     _log(case, errs, {"nsplit": eng.nsplit, "page_size": eng.cache.page_size})
     assert max(errs) <= TOL, (case, errs)
     return eng
@@ -121,8 +121,20 @@ def test_configs2_tp4_rank_b16_64k():
 
 @pytest.mark.parametrize("phi,ctx", [(4, 131072), (1, 32768)])
 def test_long_context_batch1(phi, ctx):
-    """Batch 1 (the paper's decode regime): 148 splits of one sequence, split-K K3 merge."""
+    """Batch 1 (the paper's decode regime): 148 splits of one sequence; K3 is the one-round-trip
+    split merge + head GEMM (the split-K cluster grid, 24 heads x 8, exceeds one wave)."""
     eng = _check_latent("mlra4", phi, 0, 1, ctx)
+    assert eng.nsplit == 148
+
+
+@pytest.mark.parametrize("variant", ["mlra4", "mla"])
+def test_paper_shape_64_heads_batch1(variant):
+    """The paper's decode-benchmark shape (64 heads) on a TP4 rank, B = 1, 128K --
+    the first point of the 64-head sweep (profiles/r2_sweep_h64_b1_long.md). MLRA-4 runs K2 with
+    64-head groups and the merge + head GEMM K3 released at K2's epilogue."""
+    from paper_2603_02188_b200.config import table_context
+
+    eng = _check_latent(variant, 4, 0, 1, 131072, cfg=table_context()[variant])
     assert eng.nsplit == 148
 
 

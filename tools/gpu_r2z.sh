@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/k3_sanity.py > gpurun_out/sanitizer_k3_$tool.txt 2>&1
-  echo "exit $?" >> gpurun_out/sanitizer_k3_$tool.txt
-done
+MLRA_PARITY_LOG=gpurun_out/parity_h64.jsonl timeout 900 python -m pytest tests/test_bench_configs_gpu.py -q -x -k "64_heads or long_context" -s > gpurun_out/pytest_h64.txt 2>&1
+echo "exit $?" >> gpurun_out/pytest_h64.txt
