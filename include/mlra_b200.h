@@ -67,8 +67,11 @@ int mlra_cache_append(const void* rows, const int32_t* block_table, int32_t* pos
  *           rope_base^(-2l/dr)), zero-padded to drp
  *   pool row [c_kv blocks | k_rope] bf16 written at slot slots[s] of sequence s.
  *   kv_raw [B, d_c] fp32 = h W^DKV (whole groups: the RMS spans a group's blocks), kr_raw
- *   [B, dr] fp32 = h W^KR. MLA: branches = 1. advance != 0: slots[s] += 1 after the write
- *   (slots are then the sequence lengths, as in mlra_cache_append). rope_pos == NULL: the rope
+ *   [B, dr] fp32 = h W^KR. MLA: branches = 1. advance bit 0: slots[s] += 1 after the write
+ *   (slots are then the sequence lengths, as in mlra_cache_append). advance bit 1 (value 2):
+ *   launched as a programmatic dependent of the previous kernel on the stream, releasing its
+ *   own dependent at once -- only valid when the next kernel waits for this one's completion
+ *   before reading the pool or the lengths (decode_layer's query projection does). rope_pos == NULL: the rope
  *   position is the slot written (a cache holding positions 0..n-1). slots == NULL: the B rows
  *   are ONE sequence's tokens 0..B-1 (prefill), row s written at slot s of block_table row 0.
  */

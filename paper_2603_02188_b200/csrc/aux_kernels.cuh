@@ -72,6 +72,10 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
   __shared__ float red[kMaxGroups][kK0Threads / 32];
   __shared__ float gscale[kMaxGroups];
   const int s = blockIdx.x, tid = threadIdx.x;
+  // advance bit 1: a programmatic dependent that releases its own dependent at once (the next
+  // kernel waits for this one's completion before it reads the pool: decode_layer's K-1 query)
+  if (advance & 2) griddep_launch_dependents();
+  griddep_wait();  // kv_raw / kr_raw come from the previous kernel
   // slots == NULL: ONE sequence's n rows (prefill): row s -> slot s of block_table row 0
   const int slot = slots != nullptr ? slots[s] : s;  // read before the barriers below; advanced after them
   const float* kv = kv_raw + size_t(s) * d_c;
@@ -91,7 +95,7 @@ cache_append_latent_kernel(const float* __restrict__ kv_raw, const float* __rest
     gscale[tid] = alpha_kv * rsqrtf(tot / float(gw) + eps);
   }
   __syncthreads();
-  if (advance && slots != nullptr && tid == 0) slots[s] = slot + 1;
+  if ((advance & 1) && slots != nullptr && tid == 0) slots[s] = slot + 1;
   const int page = block_table[size_t(slots != nullptr ? s : 0) * max_pages + slot / page_size];
   const int W = nblocks * dlp + drp;
   __nv_bfloat16* dst = pool + (size_t(page) * page_size + slot % page_size) * W;

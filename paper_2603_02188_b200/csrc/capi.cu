@@ -191,7 +191,8 @@ int mlra_cache_append_latent(const float* kv_raw, const float* kr_raw, const int
   if (dr < 0 || dr % 2 != 0 || drp < dr || drp % 2 != 0)
     return fail(MLRA_ERR_CONFIG, "cache_append_latent: rope width %d (padded %d) must be even", dr, drp);
   if (page_size <= 0 || max_pages <= 0) return fail(MLRA_ERR_CONFIG, "cache_append_latent: bad page geometry");
-  launch_ex(mlra::cache_append_latent_kernel, dim3(B), dim3(mlra::kK0Threads), 0, static_cast<cudaStream_t>(stream), false, 
+  launch_ex(mlra::cache_append_latent_kernel, dim3(B), dim3(mlra::kK0Threads), 0, static_cast<cudaStream_t>(stream),
+            (advance & 2) != 0 && getenv("MLRA_NO_PDL") == nullptr,
       kv_raw, kr_raw, rope_pos, slots, block_table, d_c, bs, block0, nblocks, dlp, dr, drp, alpha_kv, rope_base, eps,
       page_size, max_pages, norm_groups, advance, static_cast<__nv_bfloat16*>(pool));
   return cuda_check("cache_append_latent launch");

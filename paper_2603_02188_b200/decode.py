@@ -609,7 +609,8 @@ class DecodeEngine:
         kv_raw, kr_raw = kp.down(hidden)
         ops.cache_append_latent(kv_raw, kr_raw, None, c.seqlens, c.block_table, c.pool, c.page_size,
                                 branches=blocks, block0=block0, nblocks=nblocks, dlp=self.layout.dlp,
-                                drp=self.layout.drp, alpha_kv=kp.alpha_kv, norm_groups=norm_groups, advance=advance)
+                                drp=self.layout.drp, alpha_kv=kp.alpha_kv, norm_groups=norm_groups, advance=advance,
+                                chain=True)  # the query projection's weights stream meanwhile
         q, qr = kp.query(B, c.seqlens, pos_delta=-1 if advance else 0)
         if advance and getattr(c, "_host_lens", None) is not None:  # host mirror (eager calls)
             c._host_lens = [n + 1 for n in c._host_lens]

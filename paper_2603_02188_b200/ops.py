@@ -63,11 +63,13 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
                         slots: torch.Tensor | None,
                         block_table: torch.Tensor, pool: torch.Tensor, page_size: int, *, branches: int, block0: int,
                         nblocks: int, dlp: int, drp: int, alpha_kv: float, rope_base: float = 10000.0,
-                        eps: float = 1e-6, norm_groups: int = 1, advance: bool = False) -> None:
+                        eps: float = 1e-6, norm_groups: int = 1, advance: bool = False,
+                        chain: bool = False) -> None:
     """K0 fused: rmsnorm*alpha_kv of kv_raw [B, d_c] (owned blocks), rope of kr_raw [B, dr] at
     rope_pos (None: at the slot written), padded, appended as one bf16 pool row per sequence at
     slots[s] (then slots[s] += 1 with ``advance``). slots=None: the rows are one sequence's tokens
-    0..B-1 (prefill), row s at slot s of block_table row 0."""
+    0..B-1 (prefill), row s at slot s of block_table row 0. ``chain``: PDL launch that releases
+    the next kernel at once -- only when that kernel waits for K0 before reading the pool."""
     _need(kv_raw, torch.float32, "kv_raw", 2)
     _need(kr_raw, torch.float32, "kr_raw", 2)
     if rope_pos is not None:
@@ -85,7 +87,8 @@ def cache_append_latent(kv_raw: torch.Tensor, kr_raw: torch.Tensor, rope_pos: to
                                               None if slots is None else slots.data_ptr(), block_table.data_ptr(),
                                               B, d_c, branches, block0,
                                               nblocks, dlp, dr, drp, float(alpha_kv), float(rope_base), float(eps),
-                                              page_size, block_table.shape[1], norm_groups, int(advance),
+                                              page_size, block_table.shape[1], norm_groups,
+                                              int(advance) | (2 if chain else 0),
                                               pool.data_ptr(), _stream())
     _lib.check(rc, "mlra_cache_append_latent")
 
