@@ -1,13 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_layer_gpu.py tests/test_append_gpu.py tests/test_proj_gpu.py -q -x > gpurun_out/pytest_layer.txt 2>&1
-echo "exit $?" >> gpurun_out/pytest_layer.txt
-timeout 600 python -c "
-import sys, json, torch; sys.path.insert(0, '.')
-import bench
-for _ in range(2): print(json.dumps(bench.layer_times(torch.device('cuda', 0), None)))
-" > gpurun_out/layer.txt 2>&1
-MLRA_NO_PDL=1 timeout 600 python -c "
-import sys, json, torch; sys.path.insert(0, '.')
-import bench
-print(json.dumps(bench.layer_times(torch.device('cuda', 0), None)))
-" >> gpurun_out/layer.txt 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:merge_splits -s 1 -c 1 -f -o gpurun_out/k3m python tools/b1_launches.py h64_128k > gpurun_out/ncu_k3m.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:head_gemm -s 1 -c 1 -f -o gpurun_out/k3g python tools/b1_launches.py h64_128k > gpurun_out/ncu_k3g.log 2>&1

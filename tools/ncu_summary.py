@@ -26,7 +26,13 @@ for name, rep, algo, kname in [
         ("proj_down_b16_k3072_n1600", "gpurun_out/proj.ncu-rep", 3072 * 1600 * 2, "proj_gemm_kernel (K-1 down)"),
         # K6: causal prefill, n = 4096 (bytes are not its bound: the tensor pipe is; traffic recorded)
         ("prefill_mlra4_tp1_n4096", "gpurun_out/k6.ncu-rep", 4096 * (1152 + 24 * 512 * 2 + 24 * 64 * 2 + 24 * 128 * 4),
-         "prefill_attention_kernel (K6; tensor-bound: bytes = cache + q~ + q_rope + out)")]:
+         "prefill_attention_kernel (K6; tensor-bound: bytes = cache + q~ + q_rope + out)"),
+        # batch-1 K3 at the paper's 64-head shape (TP4 rank, 128K, 148 splits): the merge reads the
+        # split partials + lse and writes Z; the head GEMM reads W^UV (64 x 128 x 128 bf16) + Z
+        ("merge_h64_b1_n131072", "gpurun_out/k3m.ncu-rep", 148 * 64 * 128 * 4 + 148 * 64 * 4 + 64 * 128 * 4,
+         "merge_splits_kernel<16> (K3 merge, 32 columns x 16 split groups)"),
+        ("headgemm_h64_b1", "gpurun_out/k3g.ncu-rep", 64 * 128 * 128 * 2 + 2 * 64 * 128 * 4,
+         "head_gemm_kernel (K3 up-projection, PDL)")]:
     if not os.path.exists(rep):
         continue
     r = raw(rep)
