@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:merge_splits -s 1 -c 1 -f -o gpurun_out/k3m python tools/b1_launches.py h64_128k > gpurun_out/ncu_k3m.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:head_gemm -s 1 -c 1 -f -o gpurun_out/k3g python tools/b1_launches.py h64_128k > gpurun_out/ncu_k3g.log 2>&1
+( timeout 300 python tools/plan_uniform.py tp4 16 32768; timeout 300 python tools/plan_uniform.py tp1 16 32768; timeout 300 python tools/plan_uniform.py tp4 16 65536; timeout 300 python tools/plan_uniform.py tp4 1 131072 ) > gpurun_out/plan_uniform.txt 2>&1
