@@ -1,2 +1,8 @@
 mkdir -p gpurun_out
-( timeout 300 python tools/plan_uniform.py tp4 16 32768; timeout 300 python tools/plan_uniform.py tp1 16 32768; timeout 300 python tools/plan_uniform.py tp4 16 65536; timeout 300 python tools/plan_uniform.py tp4 1 131072 ) > gpurun_out/plan_uniform.txt 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1
+echo "exit $?" >> gpurun_out/pytest_gpu.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --quick --no-cpu > gpurun_out/launches_bench.log 2>&1
