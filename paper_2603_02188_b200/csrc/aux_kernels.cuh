@@ -632,9 +632,10 @@ combine4_kernel(const float* __restrict__ o_part, const float* __restrict__ lse_
                        ar_flag_words(tp.world)) + 1u;
   }
   __syncthreads();
-  // DH = 128: the up-projection runs on mma.sync and W^UV_b[h] is staged with cp.async, its
-  // 16-byte units XOR-swizzled by row (conflict-free ldmatrix.trans); otherwise one bulk copy.
-  const bool use_mma = DH == 128 && DLAT % 16 == 0;
+  // DH = 128 and >= 4 sequences: the up-projection runs on mma.sync and W^UV_b[h] is staged with
+  // cp.async, its 16-byte units XOR-swizzled by row (conflict-free ldmatrix.trans); otherwise
+  // (2 sequences would fill 2 of the MMA's 16 rows) FMAs on one bulk copy of W^UV_b[h].
+  const bool use_mma = DH == 128 && DLAT % 16 == 0 && SEQS > 2;
   const uint8_t* w_src = reinterpret_cast<const uint8_t*>(w_uv + (size_t(h) * NB + b) * DLAT * DH);
   if (use_mma) {
     const uint32_t wbase = smem_u32(c4_smem);

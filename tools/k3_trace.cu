@@ -26,9 +26,9 @@ int run(int NB) {
   attr[0].id = cudaLaunchAttributeClusterDimension; attr[0].val.clusterDim.x = 1; attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = NB; cfg.attrs = attr; cfg.numAttrs = 1;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int i = 0; i < 5; ++i) cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{});
+  for (int i = 0; i < 5; ++i) cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{}, (int*)nullptr, (const int32_t*)nullptr);
   cudaEventRecord(e0);
-  cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{});
+  cudaLaunchKernelEx(&cfg, kern, (const float*)opart, (const float*)lse, (const __nv_bfloat16*)wuv, out, B, H, NB, DLAT, DH, nsplit, 0.5f, 0, TpSum{}, (int*)nullptr, (const int32_t*)nullptr);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   const int n = ((B + SEQS - 1) / SEQS) * H * NB;
@@ -45,7 +45,7 @@ int run(int NB) {
   return 0;
 }
 int main() {
-  run<4>(4);
-  run<2>(1);
+  run<2>(4);  // TP1 (B = 16: two sequences per CTA)
+  run<2>(1);  // TP4 rank
   return 0;
 }
