@@ -433,7 +433,7 @@ def e2e_steps(engines, steps, warmup, reducer=None, rank_sync=None):
     from paper_2603_02188_b200.host_loop import MicroBatchLoop
 
     sync = rank_sync or torch.cuda.synchronize
-    loop = MicroBatchLoop(engines, reducer=reducer)
+    loop = MicroBatchLoop(engines, reducer=reducer, graphs=True)
     g = torch.Generator().manual_seed(7)
     for k in range(len(loop)):
         for t in loop.host_inputs(k):
@@ -737,7 +737,8 @@ def run_ours(args):
     # end to end through the C ABI from pinned host buffers, on every rank (the TP sum fused
     # into K3 when the group has one); whole-job bytes over the slowest rank's time
     e2e_red = reducer if runner.fused_tp else None
-    e2e_s, ser_s, bin_, bout = e2e_steps([e for e, _, _ in runner.engines], max(4, args.steps), args.warmup,
+    # (at least 40 steps: the steady-state rate of a serving loop, the pipeline fill amortised)
+    e2e_s, ser_s, bin_, bout = e2e_steps([e for e, _, _ in runner.engines], max(40, args.steps), args.warmup,
                                          reducer=e2e_red, rank_sync=rank_sync)
     tt = torch.tensor([e2e_s, ser_s], device=device)
     if world > 1:
@@ -766,7 +767,8 @@ def run_ours(args):
                          "path": "host_loop.MicroBatchLoop: per step 1 H2D (pinned rows+queries), mlra_cache_append "
                                  "(advance) + " + ("mlra_decode_step_tp (C ABI; the TP sum over the group fused into K3)"
                                                    if e2e_red is not None else "mlra_decode_step (C ABI)") +
-                                 ", 1 D2H; 2 micro-batches, the copies and K0 on side streams overlapping the other "
+                                 " (captured once per micro-batch after its first step and replayed from a CUDA "
+                                 "graph), 1 D2H; 2 micro-batches, the copies and K0 on side streams overlapping the other "
                                  "micro-batch's kernels; serial_ms_per_step = same calls on one stream, no overlap; "
                                  "per-rank bytes/step and Bi/Bo, time = max over ranks"}
         line = {

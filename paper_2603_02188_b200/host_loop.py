@@ -57,10 +57,14 @@ class _Slot:
 class MicroBatchLoop:
     """Micro-batches of one device stepped in turn with overlapped host<->device copies."""
 
-    def __init__(self, engines, reducer=None):
+    def __init__(self, engines, reducer=None, graphs=False):
         """reducer: collective.PeerAllReduce of the engines' TP group (B*h*d_h values): every step
         then runs ``decode_attention_tp`` (the sum over the group fused into K3), so the result
-        downloaded is the full TP output. All ranks must submit the same micro-batch sequence."""
+        downloaded is the full TP output. All ranks must submit the same micro-batch sequence.
+        graphs: each micro-batch's K1..K3 call (its inputs are the slot's fixed device staging
+        views, its output the engine's buffer, the lengths advance on the device) is captured
+        once, after one eager step, and replayed -- one launch instead of the per-kernel host
+        calls. The copies and K0 stay eager on their streams (the cross-step events)."""
         if not engines:
             raise ConfigError("MicroBatchLoop needs at least one engine")
         dev = engines[0].device
@@ -71,6 +75,9 @@ class MicroBatchLoop:
         self.up = torch.cuda.Stream(device=dev)
         self.down = torch.cuda.Stream(device=dev)
         self.reducer = reducer
+        self.graphs = graphs
+        self._graph = [None] * len(engines)
+        self._eager_steps = [0] * len(engines)
 
     def __len__(self) -> int:
         return len(self.slots)
@@ -102,15 +109,35 @@ class MicroBatchLoop:
             s.up_done.record(self.up)
         main.wait_event(s.up_done)
         main.wait_event(s.down_done)  # the output buffer has been drained
-        if self.reducer is not None:
-            out = eng.decode_attention_tp(qn, qr, self.reducer)
+        if self._graph[k] is not None:
+            self._graph[k].replay()
+            out = eng.out
         else:
-            out = eng.decode_attention(qn, qr)
+            out = self._attention(eng, qn, qr)
+            self._eager_steps[k] += 1
+            if self.graphs and self._eager_steps[k] == 1:
+                self._capture(k, eng, qn, qr, main)
         s.step_done.record(main)
         self.down.wait_event(s.step_done)
         with torch.cuda.stream(self.down):
             s.h_out.copy_(out, non_blocking=True)
             s.down_done.record(self.down)
+
+    def _attention(self, eng, qn, qr):
+        if self.reducer is not None:
+            return eng.decode_attention_tp(qn, qr, self.reducer, out=eng.out)
+        return eng.decode_attention(qn, qr, out=eng.out)
+
+    def _capture(self, k, eng, qn, qr, main):
+        """Capture micro-batch k's K1..K3 (after its first eager step set up the tensor maps and
+        workspace). Capture does not execute: the step just run is not repeated."""
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(main)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self._attention(eng, qn, qr)
+        main.wait_stream(side)
+        self._graph[k] = g
 
     def wait(self, k: int) -> torch.Tensor:
         self.slots[k].down_done.synchronize()

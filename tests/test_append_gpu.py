@@ -96,9 +96,11 @@ def test_plain_append_advance_flag():
     assert torch.equal(pos.cpu(), pos0 + 2)
 
 
-def test_micro_batch_loop_matches_in_order_steps():
+@pytest.mark.parametrize("graphs", [False, True])
+def test_micro_batch_loop_matches_in_order_steps(graphs):
     """host_loop.MicroBatchLoop (one H2D / D2H per step on side streams, K0 advance, two
-    micro-batches interleaved) gives exactly the outputs and cache of the plain in-order calls."""
+    micro-batches interleaved; with graphs, K1..K3 replayed from a per-micro-batch CUDA graph
+    after the first step) gives exactly the outputs and cache of the plain in-order calls."""
     import paper_2603_02188_b200 as mlra
     from paper_2603_02188_b200 import DecodeEngine
     from paper_2603_02188_b200.host_loop import MicroBatchLoop
@@ -122,7 +124,7 @@ def test_micro_batch_loop_matches_in_order_steps():
         return out
 
     ea, eb = engines(), engines()
-    loop = MicroBatchLoop(ea)
+    loop = MicroBatchLoop(ea, graphs=graphs)
     g = torch.Generator().manual_seed(3)
     host = [[[torch.randn(t.shape, generator=g).to(torch.bfloat16) for t in loop.host_inputs(k)]
              for k in range(2)] for _ in range(steps)]
