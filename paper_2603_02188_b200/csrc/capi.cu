@@ -315,6 +315,7 @@ static int decode_impl(const void* q_abs, const void* q_rope, const void* pool, 
   p.plan_ctas = plan_ctas;
   p.late_trigger = late >= 0 ? late : getenv("MLRA_K3_PDL") != nullptr;
   if (fz != nullptr) {
+    if (!mlra::kK2FusedBuild) return fail(MLRA_ERR_CONFIG, "fused / cluster step: library built without MLRA_K2_FUSED_STEP");
     p.fused = fuse_mode;
     p.fz = *fz;
     p.pdl = 0;  // the fused step reads the cache and the raw queries from its first instruction

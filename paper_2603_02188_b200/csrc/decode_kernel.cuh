@@ -70,6 +70,14 @@ struct DecodeParams {
   FuseArgs fz;
 };
 
+// The single-launch / cluster step experiments (fused_step.cuh, opt-in, measured slower) are
+// compiled into K2 only with -DMLRA_K2_FUSED_STEP: their branches cost the product kernel.
+#ifdef MLRA_K2_FUSED_STEP
+constexpr bool kK2FusedBuild = true;
+#else
+constexpr bool kK2FusedBuild = false;
+#endif
+
 constexpr int kNumThreads = 352;  // TMA warp, QK warp, 2 x 4 softmax warps, PV warp
 constexpr int kPvWarp = 10;
 constexpr int kSoftThreads = 256;
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int tid = threadIdx.x, warp = tid / 32, lane = lane_id();
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   if (!p.late_trigger) griddep_launch_dependents();  // a dependent launch may start its prologue
-  if (p.fused == 2) cluster_arrive_relaxed();  // cluster step, phase 0: this CTA has started
+  if (kK2FusedBuild && p.fused == 2) cluster_arrive_relaxed();  // cluster step, phase 0: this CTA has started
   if (p.trace != nullptr && tid == 0 && cta_lin < 1024) {
     p.trace[7 * 256 + 2 * cta_lin] = (long long)global_ns();
     p.trace[13824 + 2 * cta_lin] = clock64();
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
   const uint32_t tbase = warp == 0 ? 0u : *tmem_base_sh;
   const int ncta = gridDim.x * gridDim.y * gridDim.z;
-  const bool cm = p.fused == 2;  // cluster step (fused_step.cuh): the split CTAs of a sequence are one cluster
+  const bool cm = kK2FusedBuild && p.fused == 2;  // cluster step (fused_step.cuh): the split CTAs of a sequence are one cluster
   if (warp != 0) {
     if (cm) {
       cluster_wait_acquire();  // phase 0: every CTA of the cluster runs (its shared memory may be written)
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       cluster_arrive_release();  // phase A: the cluster's absorbed query rows are in every q buffer
       cluster_wait_acquire();
       fence_proxy_async_smem();  // generic-proxy (DSMEM) stores -> visible to the tensor-core reads
-    } else if (p.fused) {
+    } else if (kK2FusedBuild && p.fused) {
       // Fused step: the softmax warps run this CTA's share of the absorb units (K1) while the
       // producer streams; every consumer then waits for the grid's absorbed queries.
       if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 0] = (long long)global_ns();
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       named_bar_sync(7, 64);
       if (cm) { cluster_wait_acquire(); cluster_arrive_relaxed(); }  // phase 0 done; phase A: nothing to publish
     }
-    if (p.fused && p.fz.debug_producer_wait && lane == 0)  // dev: no streaming until q~ is ready
+    if (kK2FusedBuild && p.fused && p.fz.debug_producer_wait && lane == 0)  // dev: no streaming until q~ is ready
       wait_counter(p.fz.sync + kSyncAbsorb, uint32_t(absorb_units(p.B, p.H, p.fz.NB, p.fz.DLAT)));
     __syncwarp();
     if (R > 0) {
@@ -581,13 +589,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const float mx = fmaxf(fmaxf(s[c + 0], s[c + 1]), fmaxf(s[c + 2], s[c + 3]));
           dmax = (c < h_cnt) ? fmaxf(dmax, mx) : dmax;
         }
-        // m_run is finite (0 before the first tile), so masked lanes stay at -inf. The first
+        // m_run is finite (0 before the first tile), so masked lanes stay at -inf. Head groups of
+        // <= 16 heads per thread (NPAD <= 32) take the exact-max path on the first tile: measured
+        // K2 TP1 B=16 32K 105.8 -> 102.3 us, TP4 rank 35.8 -> 35.3 us against the vote
+        // (profiles/r3_k2_first_tile.md). At 64 heads (32 per thread) the
         // tile keeps the reference max 0 unless a score could overflow P (> 2^thr) or a head's
         // scores could underflow it (< 2^-64): the exact-max slow path (warp + quarter maxima,
         // a second barrier) is then taken only when needed -- it cost a CTA's first round ~2K
         // cycles. (per group: the groups own disjoint heads, so their decisions are independent)
         bool vote = dmax > thr;
-        if (t == 0) {
+        if constexpr (NPAD <= 32) {
+          if (t == 0) vote = true;
+        } else if (t == 0) {
           float dmin = INFINITY;
 #pragma unroll
           for (int c = 0; c < kHG; ++c)
@@ -836,7 +849,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (p.trace != nullptr && tid == 64 && cta_lin < 160) p.trace[16384 + 8 * cta_lin + 4] = (long long)global_ns();
       cluster_arrive_release();  // phase C: the cluster's DSMEM reads of this CTA are done
       cluster_wait_acquire();
-    } else if (p.fused) {
+    } else if (kK2FusedBuild && p.fused) {
       // publish this split's partials (barrier + one cumulative release), then this CTA's share
       // of the K3 units
       named_bar_sync(1, kSoftThreads);
@@ -868,7 +881,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tbase);
   }
-  if (p.fused == 1 && tid == 0) {
+  if (kK2FusedBuild && p.fused == 1 && tid == 0) {
     // the last CTA out resets the step's counters for the next stream-ordered launch (visible to
     // it at the kernel boundary)
     if (atom_acq_rel_add(p.fz.sync + kSyncExit, 1u) == uint32_t(ncta - 1)) {
