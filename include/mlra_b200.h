@@ -151,10 +151,12 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * Launches: K1, then K2 as a programmatic dependent of K1 (K2's TMA producer streams the cache
  * while K1 drains; its consumers wait for the absorbed queries), then K3 in plain stream order.
  * No completion counters are used on this path. MLRA_NO_PDL=1 launches K2 in plain stream order.
- * (Dev experiments, off unless their environment switch is set, both measured slower:
+ * (Dev experiments, compiled into K2 only with -DMLRA_K2_FUSED_STEP and then switched on by
+ * their environment variable; both measured slower at every shape tried, B = 1..16, 4K..128K:
  * MLRA_FUSE_GRID -- one launch with K1 / K3 inside K2 behind grid-wide counters in the
  * workspace; MLRA_FUSE_CLUSTER -- one launch with K1 / K3 inside the cluster of a sequence's
- * split CTAs, DSMEM hand-offs; fused_step.cuh.)
+ * split CTAs, DSMEM hand-offs; fused_step.cuh. The product build returns MLRA_ERR_CONFIG if
+ * either switch is set.)
  *   workspace: >= mlra_workspace_bytes(B, H, NB, DLAT, DR, nsplit) bytes (device, zeroed once)
  *   nsplit in [1, 160] (mlra_default_splits: one wave of the SMs for this batch)
  *   w_uk == NULL: the queries arrive absorbed -- q_nope is q~ [B, NB, H, DLAT] and q_rope the
