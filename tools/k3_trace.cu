@@ -45,7 +45,8 @@ int run(int NB) {
   return 0;
 }
 int main() {
-  run<2>(4);  // TP1 (B = 16: two sequences per CTA)
+  run<4>(4);  // TP1 (B = 16: four sequences per CTA -- the production variant there)
+  run<2>(4);
   run<2>(1);  // TP4 rank
   return 0;
 }
