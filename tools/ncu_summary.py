@@ -32,7 +32,13 @@ for name, rep, algo, kname in [
         ("merge_h64_b1_n131072", "gpurun_out/k3m.ncu-rep", 148 * 64 * 128 * 4 + 148 * 64 * 4 + 64 * 128 * 4,
          "merge_splits_kernel<16> (K3 merge, 32 columns x 16 split groups)"),
         ("headgemm_h64_b1", "gpurun_out/k3g.ncu-rep", 64 * 128 * 128 * 2 + 2 * 64 * 128 * 4,
-         "head_gemm_kernel (K3 up-projection, PDL)")]:
+         "head_gemm_kernel (K3 up-projection, PDL)"),
+        # the paper's 64-head shape at batch 1, 1M tokens (TP4 rank: one 128-wide latent + rope)
+        ("mlra4_h64_tp4_b1_n1048576", "gpurun_out/k2_h64.ncu-rep", 1048576 * 192 * 2, "mlra_decode_kernel (K2, 64 heads)"),
+        # K3 at TP1, B = 16, 32K: split partials + lse + W^UV (4 branches x 24 heads) + output
+        ("combine4_tp1_b16", "gpurun_out/k3_tp1.ncu-rep",
+         16 * 9 * 4 * 24 * 128 * 4 + 16 * 9 * 4 * 24 * 4 + 4 * 24 * 128 * 128 * 2 + 16 * 24 * 128 * 4,
+         "combine4_kernel<4> (K3 merge + W^UV + cluster branch sum)")]:
     if not os.path.exists(rep):
         continue
     r = raw(rep)
