@@ -445,7 +445,7 @@ static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int up
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // Split-K clusters while their grid fits one wave; beyond that (many heads at batch 1: 64 x 8
+  // Split-K clusters while their grid fits one wave; beyond that, at batch 1 (many heads: 64 x 8
   // CTAs) the one-round-trip merge plus the head GEMM measured faster (64 heads, B = 1, 128K:
   // K3 13.4 -> 8.4 us). Ragged plans (per-sequence split counts, most sequences have few) take
   // the per-branch CTAs.
@@ -457,7 +457,10 @@ static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int up
   if (force == 1) return sk_ok ? 1 : 0;
   if (force == 3) return 3;
   if (force == 2) return 0;
-  if (sk_ok && many_splits) return sk_ctas <= sms ? 1 : 3;
+  // Beyond one wave the merge + head GEMM wins only at batch 1; with 2..8 sequences the
+  // per-branch CTAs measured faster (TP4 rank, 24 heads: B = 8 4K 25.6 -> 16.2 us, B = 8 32K
+  // 38.7 -> 29.2, B = 4 4K 18.8 -> 16.2; 64 heads B = 4 4K 21.1 -> 17.7; tools/gpu_r3s.sh).
+  if (sk_ok && many_splits) return sk_ctas <= sms ? 1 : (B == 1 ? 3 : 0);
   return 0;
 }
 
