@@ -457,10 +457,15 @@ static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int up
   if (force == 1) return sk_ok ? 1 : 0;
   if (force == 3) return 3;
   if (force == 2) return 0;
-  // Beyond one wave the merge + head GEMM wins only at batch 1; with 2..8 sequences the
-  // per-branch CTAs measured faster (TP4 rank, 24 heads: B = 8 4K 25.6 -> 16.2 us, B = 8 32K
-  // 38.7 -> 29.2, B = 4 4K 18.8 -> 16.2; 64 heads B = 4 4K 21.1 -> 17.7; tools/gpu_r3s.sh).
-  if (sk_ok && many_splits) return sk_ctas <= sms ? 1 : (B == 1 ? 3 : 0);
+  // Measured per shape (MLRA_K3_FORCE, tools/gpu_r3s.sh / gpu_r3u.sh): the split-K clusters win
+  // only for 1-2 sequences, the merge + head GEMM only at batch 1 beyond one split-K wave; from
+  // 4 sequences on (and at 2 beyond one wave) the per-branch CTAs are faster (MLRA-4 TP4 rank
+  // B = 8 4K 25.6 -> 16.2 us, 32K 38.7 -> 29.2; MLA TP4 rank B = 8 4K 33.1 -> 24.6 us, 32K
+  // 73.8 -> 65.3; 64 heads B = 4 4K 21.1 -> 17.7).
+  if (sk_ok && many_splits) {
+    if (sk_ctas <= sms && B <= 2) return 1;
+    if (sk_ctas > sms && B == 1) return 3;
+  }
   return 0;
 }
 

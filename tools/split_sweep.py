@@ -1,5 +1,5 @@
 """Step time vs split count at small batches (graph of 10 alternating steps over two caches,
-like bench.StepRunner): python tools/split_sweep.py tp4|tp1|h64 B ctx nsplit,nsplit,..."""
+like bench.StepRunner): python tools/split_sweep.py tp4|tp1|h64|mla|h64mla B ctx nsplit,nsplit,..."""
 import sys, torch
 sys.path.insert(0, ".")
 import bench
@@ -9,8 +9,9 @@ from paper_2603_02188_b200.tp import shard_ownership
 
 lay, B, ctx = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 dev = torch.device("cuda", 0)
-cfg = table_context()["mlra4"] if lay == "h64" else trained_config("mlra4")
-own = shard_ownership(cfg, 4, 0) if lay in ("tp4", "h64") else None
+cfg = {"h64": lambda: table_context()["mlra4"], "mla": lambda: trained_config("mla"),
+       "h64mla": lambda: table_context()["mla"]}.get(lay, lambda: trained_config("mlra4"))()
+own = shard_ownership(cfg, 4, 0) if lay in ("tp4", "h64", "mla", "h64mla") else None
 engs = [bench.make_engine(cfg, own, B, ctx, 1000 + i, dev) for i in range(2)]
 default = engs[0][0].nsplit
 vals = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [default]
