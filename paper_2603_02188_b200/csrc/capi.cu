@@ -465,6 +465,9 @@ static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int up
   if (sk_ok && many_splits) {
     if (sk_ctas <= sms && B <= 2) return 1;
     if (sk_ctas > sms && B == 1) return 3;
+    // two sequences with very many splits: the clusters even over a second partial wave
+    // (MLRA-4 TP4 rank B = 2 32K: 22.1 -> 19.0 us)
+    if (B == 2 && sk_ctas <= 2L * sms && 4 * rt_sk <= rt_c4) return 1;
   }
   return 0;
 }
