@@ -150,7 +150,7 @@ int mlra_combine(const float* o_part, const float* lse_part, const void* w_uv, f
  * inside absorbed_decode_step) for every unit a device owns.
  * Launches: K1, then K2 as a programmatic dependent of K1 (K2's TMA producer streams the cache
  * while K1 drains; its consumers wait for the absorbed queries), then K3 in plain stream order
- * (except the merge + head-GEMM K3 variant over many heads at small batch, which K2 releases as
+ * (except the merge + head-GEMM K3 variant over many heads at batch 1, which K2 releases as
  * a programmatic dependent at its epilogue). No completion counters are used on this path. MLRA_NO_PDL=1 launches K2 in plain stream order.
  * (Dev experiments, compiled into K2 only with -DMLRA_K2_FUSED_STEP and then switched on by
  * their environment variable; both measured slower at every shape tried, B = 1..16, 4K..128K:
