@@ -468,6 +468,9 @@ static int k3_variant(int B, int H, int NB, int DLAT, int DH, int nsplit, int up
     // two sequences with very many splits: the clusters even over a second partial wave
     // (MLRA-4 TP4 rank B = 2 32K: 22.1 -> 19.0 us)
     if (B == 2 && sk_ctas <= 2L * sms && 4 * rt_sk <= rt_c4) return 1;
+    // two sequences over many heads (> 2 split-K waves) and >= 64 splits: the merge + head GEMM
+    // (64 heads B = 2 32K / 128K: 24.2 / 35.9 -> 23.4 / 34.8 us; at 33 splits it loses)
+    if (B == 2 && sk_ctas > 2L * sms && nsplit >= 64) return 3;
   }
   return 0;
 }
